@@ -1,0 +1,458 @@
+"""Benchmark of the B200-native SpecEE speculative early-exit predictor path.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Workload (Llama2-7B shape, BASELINE.json configs[1]/[4]): LM head V=32000 x
+d=4096 (bf16 in HBM), K=4 speculative ids per request, a bank of 31 per-layer
+MLP predictors (H=512, reference init_predictor), threshold 0.7.  One STEP is
+one pass of the predictor path over every predictor-capable layer (31) for B
+independent requests (default 1024 per GPU): 31 fused launches of K1+K2+K3
+(LayerNorm + K-row gather + local logits + softmax/delta features + MLP +
+sigmoid/threshold + device exit flag), each over that layer's own synthetic
+hidden rows (31 x B x 4096 f32 = 520 MB > L2, so no L2 flush is needed).
+``value`` = predictor evaluations/s over all ranks.  Requests shard across
+GPUs with no collective on the hot path (weak scaling); one NCCL all_gather
+of the per-rank fire counts after the timed region.
+
+``e2e`` = the same step through the public drop-in API with HOST buffers:
+each step copies its hidden rows/ids from pinned host memory to HBM and the
+fired flags + probabilities back.
+
+``--impl reference`` times the reference's CPU implementation of the same
+chain (oracle port of sliced_head_logits -> extract_features ->
+predictor_forward -> decide_exit with the reference's own compiled strict
+kernel from oracle/_ref when present) on this host's cores, one forked
+process per core.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+V, D, K, H, LAYERS = 32000, 4096, 4, 512, 32
+PRED_LAYERS = LAYERS - 1
+THRESHOLD = 0.7
+SEED = 1234
+METRIC = "predictor evals/sec + early-exit decode tok/s, Llama2-7B shape, 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=1024, help="requests per GPU")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="fast", choices=["fast", "strict"])
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def distinct_ids(seed, B, K, V):
+    """Per-request K distinct ids from the splitmix64 stream."""
+    from paper_2504_08850_b200 import rng
+    raw = rng.splitmix64(seed, B * K * 4) % np.uint64(V)
+    ids = np.empty((B, K), np.int32)
+    pos = 0
+    for b in range(B):
+        seen = []
+        while len(seen) < K:
+            v = int(raw[pos % raw.size]); pos += 1
+            if v not in seen:
+                seen.append(v)
+        ids[b] = seen
+    return ids
+
+
+def launch_bytes(B, U):
+    """Algorithmic HBM bytes of one fused launch."""
+    return U * D * 2 + B * D * 4 + B * (3 * K * 4 + 5) + 2 * D * 4 + (3 * K * H + 2 * H + 1) * 4
+
+
+# ------------------------------------------------------------------ clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU reference
+
+
+def cpu_reference_rate(head_dv, final_g, final_b, bank, ids, seconds, seed=7):
+    """evals/s of the reference chain on this host, one forked process per
+    available core (OPENBLAS_NUM_THREADS=1), each running for `seconds`."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle import specexit_oracle as O
+    from oracle.build import load_ref_kernels
+    kern = load_ref_kernels()
+    kind = "port+reference-ckern" if kern is not None else "port"
+    t = {"lm_head": head_dv, "final_norm.g": final_g, "final_norm.b": final_b}
+    cores = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else [0]
+    P = len(cores)
+    r_fd, w_fd = os.pipe()
+    pids = []
+    for p in range(P):
+        pid = os.fork()
+        if pid == 0:
+            try:
+                os.sched_setaffinity(0, {cores[p]})
+            except (AttributeError, OSError):
+                pass
+            rng = np.random.default_rng(seed + p)
+            hidden = rng.standard_normal((64, D)).astype(np.float32)
+            prev = np.full(K, np.float32(1.0 / K), np.float32)
+            n, t0 = 0, time.perf_counter()
+            while time.perf_counter() - t0 < seconds:
+                l = n % PRED_LAYERS
+                _, prev2 = O.reference_chain(t, hidden[n % 64], ids[(n * 7 + p) % ids.shape[0]],
+                                             prev, bank[l], THRESHOLD, kern)
+                n += 1
+            el = time.perf_counter() - t0
+            os.write(w_fd, f"{n} {el}\n".encode())
+            os._exit(0)
+        pids.append(pid)
+    os.close(w_fd)
+    data = b""
+    with os.fdopen(r_fd, "rb") as fh:
+        data = fh.read()
+    for pid in pids:
+        os.waitpid(pid, 0)
+    rates = [int(a) / float(b) for a, b in (ln.split() for ln in data.decode().splitlines())]
+    return sum(rates), P, kind, sum(int(ln.split()[0]) for ln in data.decode().splitlines())
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2504_08850_b200 import rng
+    from oracle import specexit_oracle as O
+    t0 = time.time()
+    cfg = O.ModelConfig(vocab_size=V, hidden_dim=D, num_layers=LAYERS, num_heads=32, ffn_dim=11008,
+                        max_context=512, seed=SEED)
+    head = O.init_model(cfg, bf16=True, only={"lm_head", "final_norm.g", "final_norm.b"})
+    bank = [O.init_predictor(K, H, rng.derive(SEED, 100 + l)) for l in range(PRED_LAYERS)]
+    ids = distinct_ids(SEED + 1, 4096, K, V)
+    per_step = max(0.5, min(args.cpu_seconds, 120.0 / max(args.steps + args.warmup, 1)))
+    vals = []
+    for s in range(args.warmup + args.steps):
+        rate, P, kind, n = cpu_reference_rate(head["lm_head"], head["final_norm.g"],
+                                              head["final_norm.b"], bank, ids, per_step, seed=s)
+        if s >= args.warmup:
+            vals.append(rate)
+    value = statistics.median(vals)
+    sample = (f"reference chain sliced_head_logits->extract_features->predictor_forward->"
+              f"decide_exit at d={D}, V={V}, K={K}, H={H} on random bf16-valued rows, "
+              f"{per_step:.1f}s per step per process, {P} processes x 1 core")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "predictor path, Llama2-7B head (V=32000,d=4096), K=4, H=512, "
+                               "thr 0.7, CPU reference chain", "batch_per_gpu": None},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": P, "kind": "port",
+                         "sample": sample, "strict_kernel": kind},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": round(time.time() - t0, 1)}))
+
+
+# ------------------------------------------------------------------ ours
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_08850_b200 as spx
+    from paper_2504_08850_b200 import _native as N
+    from paper_2504_08850_b200 import numerics, rng
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    numerics.set_mode(args.mode)
+    B = args.batch
+
+    # ---- model head + predictor bank (reference init, bf16 head) ------------
+    cfg = spx.ModelConfig(vocab_size=V, hidden_dim=D, num_layers=LAYERS, num_heads=32,
+                          ffn_dim=11008, max_context=512, seed=SEED)
+    model = spx.init_model(cfg, dtype="bf16", head_only=True)
+    bank_w = {l: spx.init_predictor(K, H, rng.derive(SEED, 100 + l)) for l in range(PRED_LAYERS)}
+    bank = spx.PredictorBank(bank_w, LAYERS)
+
+    # ---- synthetic requests: this rank's shard ------------------------------
+    g = torch.Generator(device=dev)
+    g.manual_seed(SEED + 17 * rank)
+    hidden = torch.randn((PRED_LAYERS, B, D), generator=g, device=dev, dtype=torch.float32)
+    hidden = hidden.to(torch.bfloat16).float()            # bf16-valued rows
+    ids_np = distinct_ids(SEED + 1 + rank, B, K, V)
+    ids = torch.as_tensor(ids_np, device=dev)
+    U = int(np.unique(ids_np).size)
+    prev0 = torch.full((B, K), float(np.float32(1.0 / K)), device=dev)
+    prev = prev0.clone()
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    outs = [spx.predictor.BatchResult(logits=None, z=None,
+                                      prob=torch.empty(B, dtype=torch.float64, device=dev),
+                                      fired=torch.empty(B, dtype=torch.uint8, device=dev), err=err)
+            for _ in range(PRED_LAYERS)]
+
+    def step():
+        prev.copy_(prev0)                                  # token start: uniform prior
+        for l in range(PRED_LAYERS):
+            spx.evaluate_batch(model, bank, hidden[l], ids, prev, threshold=THRESHOLD, layer=l,
+                               outputs=False, out=outs[l])
+
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            step()
+    torch.cuda.synchronize()
+    N.raise_device_error(err.item())
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            graph.replay()
+    barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            graph.replay()
+        e1.record(stream)
+    e1.synchronize()
+    clocks = clk.stop()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_max = float(t_local.item())
+    evals_per_step = PRED_LAYERS * B * ws
+    value = evals_per_step * args.steps / (ms_max / 1000.0)
+    launches = PRED_LAYERS * args.steps
+    t_launch = (ms / 1000.0) / launches
+    bytes_launch = launch_bytes(B, U)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = bytes_launch / t_launch / 1e9
+
+    fired = torch.stack([o.fired for o in outs]).float().mean().item()
+    fire_cnt = torch.tensor([fired], device=dev)
+    if ws > 1:
+        gathered = [torch.zeros_like(fire_cnt) for _ in range(ws)]
+        dist.all_gather(gathered, fire_cnt)               # results gather (off the hot path)
+        fired = float(torch.stack(gathered).mean().item())
+
+    # ---- batch-1 latency of one fused launch (configs[1]: batch 1) ---------
+    h1, i1, p1 = hidden[0, :1].contiguous(), ids[:1].contiguous(), prev0[:1].clone()
+    o1 = spx.predictor.BatchResult(logits=None, z=None, prob=None,
+                                   fired=torch.empty(1, dtype=torch.uint8, device=dev), err=err)
+    g1 = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        spx.evaluate_batch(model, bank, h1, i1, p1, threshold=THRESHOLD, layer=0, outputs=False, out=o1)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g1, stream=stream):
+            for l in range(PRED_LAYERS):
+                spx.evaluate_batch(model, bank, hidden[l, :1], i1, p1, threshold=THRESHOLD,
+                                   layer=l, outputs=False, out=o1)
+        for _ in range(5):
+            g1.replay()
+        torch.cuda.synchronize()
+        b0, b1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(20):
+            g1.replay()
+        b1e.record(stream)
+    b1e.synchronize()
+    us_per_eval_b1 = b0.elapsed_time(b1e) * 1000.0 / (20 * PRED_LAYERS)
+
+    # ---- e2e: public API with host buffers ---------------------------------
+    e2e = None
+    if not args.no_e2e:
+        h_host = hidden.cpu().pin_memory()
+        ids_host = ids.cpu().pin_memory()
+        fired_host = torch.empty((PRED_LAYERS, B), dtype=torch.uint8).pin_memory()
+        prob_host = torch.empty((PRED_LAYERS, B), dtype=torch.float64).pin_memory()
+        hid_dev = torch.empty_like(hidden)
+        ids_dev = torch.empty_like(ids)
+        eo = [spx.predictor.BatchResult(logits=None, z=None,
+                                        prob=torch.empty(B, dtype=torch.float64, device=dev),
+                                        fired=torch.empty(B, dtype=torch.uint8, device=dev),
+                                        err=err) for _ in range(PRED_LAYERS)]
+
+        def e2e_step():
+            hid_dev.copy_(h_host, non_blocking=True)
+            ids_dev.copy_(ids_host, non_blocking=True)
+            prev.copy_(prev0)
+            for l in range(PRED_LAYERS):
+                spx.evaluate_batch(model, bank, hid_dev[l], ids_dev, prev, threshold=THRESHOLD,
+                                   layer=l, outputs=False, out=eo[l])
+            for l in range(PRED_LAYERS):
+                fired_host[l].copy_(eo[l].fired, non_blocking=True)
+                prob_host[l].copy_(eo[l].prob, non_blocking=True)
+
+        e2e_steps = max(3, min(args.steps, 10))
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                e2e_step()
+            barrier()
+            x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            x0.record(stream)
+            for _ in range(e2e_steps):
+                e2e_step()
+            x1.record(stream)
+        x1.synchronize()
+        xms = torch.tensor([x0.elapsed_time(x1)], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(xms, op=dist.ReduceOp.MAX)
+        e2e = {"value": evals_per_step * e2e_steps / (float(xms.item()) / 1000.0),
+               "unit": "evals/s",
+               "h2d_bytes_per_step": int(hidden.numel() * 4 + ids.numel() * 4),
+               "d2h_bytes_per_step": int(PRED_LAYERS * B * (1 + 8)),
+               "path": "paper_2504_08850_b200.evaluate_batch -> spx_predictor_eval (C ABI)"}
+
+    # ---- CPU baseline (rank 0, N=1) ----------------------------------------
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        head_dv = model.lm_head.float().t().contiguous().cpu().numpy()
+        from oracle import specexit_oracle as O
+        obank = [O.PredictorWeights(w.w1, w.b1, w.w2, w.b2) for w in
+                 (bank_w[l] for l in range(PRED_LAYERS))]
+        rate, P, kind, n = cpu_reference_rate(head_dv, model.final_g.cpu().numpy(),
+                                              model.final_b.cpu().numpy(), obank, ids_np,
+                                              args.cpu_seconds)
+        cpu = {"value": rate, "unit": "evals/s", "cores": P, "kind": "port",
+               "sample": f"{n} evals of the reference chain (sliced_head_logits->extract_features->"
+                         f"predictor_forward->decide_exit, d={D}, V={V}, K={K}, H={H}) in "
+                         f"{args.cpu_seconds:.0f}s on {P} forked single-core processes; "
+                         f"strict kernel: {kind}"}
+        del head_dv
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference splitmix64 init of the 7B head + predictors, bf16 head; "
+                    "bf16-valued N(0,1) hidden rows; splitmix64 distinct ids)",
+            "config": {"workload": f"predictor path step: {PRED_LAYERS} layers x {B} requests/GPU, "
+                                   f"one fused K1-K3 launch per layer, Llama2-7B head V={V} d={D}, "
+                                   f"K={K}, H={H}, thr={THRESHOLD}, mode={args.mode}",
+                       "batch_per_gpu": B, "layers_per_step": PRED_LAYERS, "k": K,
+                       "predictor_hidden": H, "unique_ids_per_launch": U,
+                       "l2": "inputs (520 MB hidden + 262 MB head) exceed the 126 MB L2; no flush",
+                       "parallelism": f"dp{ws} (request sharding, no hot-path collective)",
+                       "cuda_graph": True},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": None,
+                         "kernel": "predictor_fast_kernel<bf16,4>",
+                         "algorithmic_bytes_per_launch": bytes_launch,
+                         "us_per_launch": t_launch * 1e6,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "fire_rate": fired,
+            "batch1_us_per_eval": us_per_eval_b1,
+            "lib": N.version(),
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

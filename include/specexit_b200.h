@@ -1,0 +1,191 @@
+/*
+ * specexit_b200.h -- C ABI of the B200-native SpecEE speculative early-exit
+ * predictor path (libspecexit_b200.so, sm_100a).
+ *
+ * This is the drop-in boundary.  In the reference (a numpy/Cython package,
+ * /root/reference/pkg) the only native slot is the kernel backend registry
+ * `_BACKENDS` (src/specexit/kernels/__init__.py:25-31) whose entries export
+ * `matmul_f32` / `seq_sum_f32` (src/specexit/kernels/_ckern.pyx:16-46).  This
+ * library replaces that slot at the OPERATOR level: each export is one fused
+ * operator of the predictor path, called by the Python drop-in package
+ * (paper_2504_08850_b200/, same names/signatures as `specexit`) through ctypes.
+ *
+ * Conventions (all exports):
+ *   - every pointer is a DEVICE pointer allocated by the caller; the library
+ *     never allocates, frees or synchronises;
+ *   - all work is enqueued on `stream` (cudaStream_t passed as void*);
+ *   - return 0 on success, SPX_EINVAL (-1) for arguments rejected on the
+ *     host, SPX_ECUDA (-2) if the launch failed;
+ *   - in-kernel input violations (token id out of range, non-finite values,
+ *     bad probability vector) OR bits into the caller's device error word
+ *     `err`; the Python wrapper maps them to the reference's ValueError
+ *     messages at its next synchronisation point;
+ *   - weight tensors are passed as void* with a SPX_DTYPE_* tag (bf16 = raw
+ *     bfloat16 bits; f32 for reference weights that are not bf16-exact).
+ */
+#ifndef SPECEXIT_B200_H
+#define SPECEXIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPX_EINVAL (-1)
+#define SPX_ECUDA (-2)
+
+#define SPX_MODE_FAST 0   /* canonical 128-partial reductions (production) */
+#define SPX_MODE_STRICT 1 /* reference order: sequential, no FMA (parity)   */
+
+#define SPX_DTYPE_BF16 0  /* weight storage: bfloat16 (production)           */
+#define SPX_DTYPE_F32 1   /* weight storage: float32 (exact reference weights) */
+
+#define SPX_POLICY_MLP 0      /* PredictorPolicy  (engine.py:83-92)             */
+#define SPX_POLICY_CONST 1    /* Never/AlwaysExitPolicy (engine.py:67-80)       */
+
+/* error-word bits */
+#define SPX_ERR_ID_RANGE 1
+#define SPX_ERR_HIDDEN_NONFINITE 2
+#define SPX_ERR_LOGIT_NONFINITE 4
+#define SPX_ERR_PREV_SUM 8
+#define SPX_ERR_BAD_LAYER 16
+
+/* K1+K2+K3 -- fused predictor evaluation for B rows at ONE layer.
+ * Replaces, per row, the reference chain
+ *   sliced_head_logits   (src/specexit/model.py:298-314)
+ *   extract_features     (src/specexit/predictor.py:42-52)
+ *   predictor_forward    (src/specexit/predictor.py:97-103)
+ *   decide_exit          (src/specexit/predictor.py:106-109)
+ * as used in ExitEngine.step (src/specexit/engine.py:192-200). */
+typedef struct {
+  const float *hidden;       /* (B, d) f32 residual rows                       */
+  int64_t hidden_stride;     /* elements between rows (0 -> d)                 */
+  const float *norm_g;       /* (d) final_norm.g                               */
+  const float *norm_b;       /* (d) final_norm.b                               */
+  const void *head;          /* (V, d) LM head, vocab-row major                */
+  int32_t head_dtype;        /* SPX_DTYPE_*                                    */
+  const int32_t *ids;        /* (B, K) speculative token ids                   */
+  float *prev;               /* (B, K) in: previous local probs, out: new ones */
+  const float *w1;           /* (3K, H) predictor W1 (row-major, as reference) */
+  const float *b1;           /* (H)                                            */
+  const float *w2;           /* (H)                                            */
+  float b2;                  /* f32 output bias                                */
+  float z_cut;               /* fire iff z2 >= z_cut  (== sigmoid(z2) > thr)   */
+  int32_t policy;            /* SPX_POLICY_*                                   */
+  double const_prob;         /* SPX_POLICY_CONST: the policy's probability     */
+  double threshold;          /* SPX_POLICY_CONST: fire iff const_prob > thr    */
+  float *logits_out;         /* (B, K) optional                                */
+  float *feat_out;           /* (B, 3K) optional FeatureVector.concat()        */
+  float *z_out;              /* (B) optional pre-sigmoid f32                   */
+  double *prob_out;          /* (B) optional f64 probability                   */
+  uint8_t *fired;            /* (B) optional decision                          */
+  const uint64_t *row_layer_mask; /* (B) optional: skip row unless bit `layer` */
+  const uint8_t *row_done;   /* (B) optional: skip row if nonzero (exited)     */
+  int32_t *evals;            /* (B) optional per-row evaluation counter        */
+  int32_t layer;
+  int32_t mode;              /* SPX_MODE_*                                     */
+  int32_t *err;              /* device error word                              */
+  int64_t B, d, V, K, H;
+} spx_predictor_args;
+int spx_predictor_eval(const spx_predictor_args *args, void *stream);
+
+/* extract_features alone (src/specexit/predictor.py:42-52) for B rows:
+ * feats_out (B, 3K) = [logits | softmax | softmax - prev]; prev is read only. */
+int spx_extract_features(const float *logits, const float *prev, float *feats_out, int32_t *err,
+                         int64_t B, int64_t K, void *stream);
+/* predictor_forward alone (src/specexit/predictor.py:97-103) + decide_exit
+ * (:106-109) for B feature rows (B, 3K); any output pointer may be NULL. */
+int spx_predictor_mlp(const float *feats, const float *w1, const float *b1, const float *w2,
+                      float b2, float z_cut, float *z_out, double *prob_out, uint8_t *fired_out,
+                      int64_t B, int64_t K, int64_t H, void *stream);
+
+/* K4 -- full-head verification: argmax over V of LN(h) . head for each gated
+ * row, lowest index on ties (np.argmax), membership in the row's verify set.
+ * Replaces verify_exit (src/specexit/engine.py:59-64) / full_head_logits
+ * (src/specexit/model.py:289-295) / the final-layer argmax (engine.py:208-210)
+ * / TreeEngine._verify_path (src/specexit/tree.py:274-283).
+ * On a verified row with `done_out` given it also writes the device exit
+ * flag: done_out[r]=1, exit_layer_out[r]=layer -- later layer kernels read it
+ * and return early (no host sync). */
+typedef struct {
+  const float *hidden; int64_t hidden_stride;   /* (B, d) */
+  const float *norm_g, *norm_b;
+  const void *head;                             /* (V, d) */
+  int32_t head_dtype;                           /* SPX_DTYPE_* */
+  const uint8_t *gate;        /* (B) optional: row computed iff gate[r] != 0  */
+  const uint8_t *row_done;    /* (B) optional: row skipped if nonzero         */
+  const int32_t *spec_ptr;    /* (B+1) optional CSR offsets of verify sets    */
+  const int32_t *spec_ids;    /* verify-set ids                               */
+  int32_t *token_out;         /* (B) argmax token (written for computed rows) */
+  uint8_t *verified_out;      /* (B) optional argmax in verify set            */
+  float *maxlogit_out;        /* (B) optional                                 */
+  float *logits_out;          /* (B, V) optional full logits                  */
+  uint8_t *done_out;          /* (B) optional exit flag, set when verified    */
+  int32_t *exit_layer_out;    /* (B) optional                                 */
+  int32_t *full_heads;        /* (B) optional counter += 1 per computed row   */
+  int32_t layer;
+  unsigned long long *scratch;  /* (B) zeroed once by the caller; self-reset  */
+  unsigned int *counter;        /* (1) zeroed once by the caller; self-reset  */
+  int32_t mode;
+  int32_t *err;
+  int64_t B, d, V;
+} spx_verify_args;
+int spx_verify(const spx_verify_args *args, void *stream);
+
+/* K5 -- two-level scheduler on device (src/specexit/scheduler.py:49-102).
+ * Per row: ring of the last `queue_len` exit layers + neighbour counts. */
+typedef struct {
+  int32_t *queue;    /* (B, queue_len) ring storage                            */
+  int32_t *head;     /* (B) slot of the oldest entry                           */
+  int32_t *len;      /* (B) entries held                                       */
+  int32_t *counts;   /* (B, L) neighbour counts (scheduler.py:54-58)           */
+} spx_online_state;
+/* update_online (scheduler.py:65-79) for each row r with gate[r] (or all). */
+int spx_sched_update(spx_online_state st, const int32_t *exit_layer, const uint8_t *gate,
+                     int64_t B, int32_t L, int32_t queue_len, int32_t radius, int32_t *err,
+                     void *stream);
+/* active_layers (scheduler.py:95-102): bit i of active_out[r] set iff
+ * i <= L-2 and (offline bit i or counts[r][i] > 0); mode 0 = "all" layers
+ * (engine.py:170-174). L <= 64. */
+int spx_sched_active(spx_online_state st, uint64_t offline_mask, int64_t B, int32_t L,
+                     int32_t mode, uint64_t *active_out, void *stream);
+
+/* K6 -- context-aware merged mapping (src/specexit/tree.py:92-113): logits of
+ * node n for ids[ptr[n]..ptr[n+1]) with each UNIQUE id's LM-head row read
+ * once.  uniq (U) are the distinct ids, pair_uid / pair_node / pair_out (P)
+ * map every (node, id) pair to its unique row; hn (N, d) are the final-normed
+ * node rows (spx_final_norm).  Bit-identical to K1's logits (FAST order). */
+int spx_tree_merged_logits(const float *hn, int64_t N, const void *head, int32_t head_dtype,
+                           int64_t V, int64_t d, const int32_t *uniq, int64_t U, const int32_t *uniq_ptr,
+                           const int32_t *pair_node, const int32_t *pair_out, float *logits,
+                           int32_t *err, void *stream);
+/* final LayerNorm of N rows into hn (model.py:140-146), FAST or STRICT. */
+int spx_final_norm(const float *hidden, int64_t hidden_stride, const float *g, const float *b,
+                   float *hn, int64_t N, int64_t d, int32_t mode, int32_t *err, void *stream);
+
+/* K7 -- hyper-token conjunction (src/specexit/tree.py:116-122, :389-390):
+ * path_fire[p] = AND over nodes j of path p (CSR) of node_fired[j]; only for
+ * live paths (live[p] != 0). */
+int spx_path_and(const uint8_t *node_fired, const int32_t *path_ptr, const int32_t *path_nodes,
+                 const uint8_t *live, int64_t P, uint8_t *path_fire, void *stream);
+
+/* Synthetic weights on device: reference rng.uniform (src/specexit/rng.py:24-27)
+ * of stream `seed` over a (rows, cols) row-major tensor, written as bf16 (or
+ * f32 when out_f32 != 0).  transpose != 0 stores element (r, c) at
+ * out[c*rows + r] (e.g. the (d, V) lm_head as (V, d)). Bit-identical to
+ * numpy's float32 result, then RNE-rounded to bf16. */
+int spx_init_uniform(void *out, int32_t out_f32, int64_t rows, int64_t cols, int32_t transpose,
+                     uint64_t seed, double low, double high, void *stream);
+
+/* numpy float32 exp restated on device (the exp of softmax_1d, model.py:151),
+ * elementwise -- test hook for the bit-exactness of the softmax. */
+int spx_np_expf(const float *x, float *y, int64_t n, void *stream);
+
+/* Library identification (for the loaded-.so evidence). */
+const char *spx_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECEXIT_B200_H */

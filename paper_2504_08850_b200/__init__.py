@@ -1,0 +1,20 @@
+"""B200-native SpecEE speculative early-exit predictor path.
+
+Drop-in for the hot path of the reference package ``specexit``: the same
+function / class names, backed by hand-written sm_100a CUDA kernels in
+libspecexit_b200.so (C ABI: include/specexit_b200.h).  No CPU fallback.
+"""
+from . import numerics  # noqa: F401
+from .model import (LN_EPS, ModelConfig, TransformerModel, final_norm, from_tensors,  # noqa: F401
+                    full_head_logits, head_argmax, init_model, layer_norm, load_weights,
+                    sliced_head_logits, tensor_specs)
+from .predictor import (FeatureVector, PredictorBank, PredictorWeights, decide_exit,  # noqa: F401
+                        evaluate_batch, extract_features, init_predictor, load_predictors,
+                        predictor_forward, predictor_param_count, save_predictors,
+                        uniform_probs, z_cut)
+from .scheduler import (OfflineProfile, OnlineState, ScheduleConfig, active_layers,  # noqa: F401
+                        load_profile, online_hot_layers, profile_offline, recompute_counts,
+                        save_profile, update_online, weight_fingerprint)
+from .tree import grouped_speculative_logits, hypertoken_exit_decision  # noqa: F401
+
+__version__ = "0.1.0"

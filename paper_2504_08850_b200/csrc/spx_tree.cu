@@ -1,0 +1,107 @@
+// K6: context-aware merged mapping for token trees (sm_100a).
+//
+// Reference: grouped_speculative_logits (tree.py:92-113) -- per live tree
+// node j, LN(h_j) . lm_head[:, ids_j].  The reference computes the FULL
+// vocabulary per node and gathers (tree.py:111-113).  Here the feature ids of
+// all live nodes are de-duplicated into U unique LM-head rows (the merged
+// mapping of the paper, §6.2); one warp owns one unique row, holds it in
+// registers (read from HBM exactly once), and dots it with every node that
+// asked for it (normed node rows come from L2).  The dot is the canonical
+// CDOT order, so every logit is bit-identical to the predictor kernel's
+// sliced logit for the same (row, id) -- the reference's "grouped == sliced"
+// contract (tests/test_tree.py:32-42).
+#include "spx_common.cuh"
+#include "../../include/specexit_b200.h"
+
+namespace spx {
+
+constexpr int TREE_THREADS = 128;
+
+template <typename TW, int CPL>
+__global__ void __launch_bounds__(TREE_THREADS)
+tree_merged_kernel(const float *hn, int N, const TW *head, int V, int d,
+                   const int32_t *uniq, int U, const int32_t *uniq_ptr, const int32_t *pair_node,
+                   const int32_t *pair_out, float *logits, int *err) {
+  const int lane = threadIdx.x & 31;
+  const int u = blockIdx.x * (TREE_THREADS / 32) + (threadIdx.x >> 5);
+  if (u >= U) return;
+  const int id = uniq[u];
+  if (id < 0 || id >= V) {
+    if (lane == 0) atomicOr(err, ERR_ID_RANGE);
+    return;
+  }
+  const int nchunk = d / CHUNK;
+  const TW *wrow = head + (size_t)id * d;
+  Chunk<TW> w[4][CPL];
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+#pragma unroll
+    for (int s = 0; s < CPL; ++s) {
+      const int c = 32 * g + lane + NPART * s;
+      if (c < nchunk) w[g][s].load(wrow + CHUNK * c);
+      else w[g][s].zero();
+    }
+  for (int q = uniq_ptr[u]; q < uniq_ptr[u + 1]; ++q) {
+    const int node = pair_node[q];
+    const float *h = hn + (size_t)node * d;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int s = 0; s < CPL; ++s) {
+        const int c = 32 * g + lane + NPART * s;
+        if (c < nchunk) {
+          const float4 h0 = __ldg(reinterpret_cast<const float4 *>(h + CHUNK * c));
+          const float4 h1 = __ldg(reinterpret_cast<const float4 *>(h + CHUNK * c + 4));
+          const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+          float wf[8];
+          w[g][s].to_f32(wf);
+#pragma unroll
+          for (int e = 0; e < CHUNK; ++e) acc[g] = __fmaf_rn(hv[e], wf[e], acc[g]);
+        }
+      }
+    float gs[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) gs[g] = warp_butterfly_sum(acc[g]);
+    const float lg = canon_combine(gs[0], gs[1], gs[2], gs[3]);
+    if (lane == 0) logits[pair_out[q]] = lg;
+  }
+}
+
+}  // namespace spx
+
+using namespace spx;
+
+extern "C" int spx_tree_merged_logits(const float *hn, int64_t N, const void *head,
+                                      int32_t head_dtype, int64_t V,
+                                      int64_t d, const int32_t *uniq, int64_t U,
+                                      const int32_t *uniq_ptr, const int32_t *pair_node,
+                                      const int32_t *pair_out, float *logits, int32_t *err,
+                                      void *stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!hn || !head || !uniq || !uniq_ptr || !pair_node || !pair_out || !logits || !err ||
+      N < 0 || U < 0 || d <= 0 || d % CHUNK || V <= 0)
+    return SPX_EINVAL;
+  if (U == 0) return 0;
+  const int wpc = TREE_THREADS / 32;
+  const unsigned grid = (unsigned)((U + wpc - 1) / wpc);
+  const int nchunk = (int)(d / CHUNK);
+#define SPX_LAUNCH_TREE(CPL)                                                                   \
+  do {                                                                                         \
+    if (head_dtype == SPX_DTYPE_F32)                                                           \
+      tree_merged_kernel<float, CPL><<<grid, TREE_THREADS, 0, stream>>>(                        \
+          hn, (int)N, (const float *)head, (int)V, (int)d, uniq, (int)U, uniq_ptr, pair_node,  \
+          pair_out, logits, err);                                                              \
+    else                                                                                       \
+      tree_merged_kernel<__nv_bfloat16, CPL><<<grid, TREE_THREADS, 0, stream>>>(                \
+          hn, (int)N, (const __nv_bfloat16 *)head, (int)V, (int)d, uniq, (int)U, uniq_ptr,     \
+          pair_node, pair_out, logits, err);                                                   \
+  } while (0)
+  if (nchunk <= NPART) SPX_LAUNCH_TREE(1);
+  else if (nchunk <= 2 * NPART) SPX_LAUNCH_TREE(2);
+  else if (nchunk <= 4 * NPART) SPX_LAUNCH_TREE(4);
+  else if (nchunk <= 8 * NPART) SPX_LAUNCH_TREE(8);
+  else return SPX_EINVAL;
+#undef SPX_LAUNCH_TREE
+  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+}

@@ -1,0 +1,360 @@
+// K4: full-head verification GEMV + argmax + membership (sm_100a), and the
+// final LayerNorm kernel shared with the tree path.
+//
+// Reference: verify_exit (engine.py:59-64) = argmax(full_head_logits) in the
+// speculative set; full_head_logits (model.py:289-295); the fall-through
+// final argmax (engine.py:208-210); TreeEngine._verify_path (tree.py:274-283).
+//
+// HBM-bound: one pass over the (V, d) bf16 head (262 MB at Llama2-7B shape)
+// for up to VER_ROWS gated rows at once; each vocab row is read by one warp
+// with 16-byte loads and dotted in the canonical CDOT order (4 partials per
+// lane == the 128 partials of the predictor kernel), so logits are
+// bit-identical to K1's speculative logits.  The argmax is reduced with a
+// 64-bit (orderable value, ~index) atomicMax -- value first, lowest index on
+// ties, as np.argmax -- and the last CTA to finish resolves membership and
+// writes the device exit flag.
+#include "spx_common.cuh"
+#include "../../include/specexit_b200.h"
+
+namespace spx {
+
+constexpr int VER_THREADS = 256;
+constexpr int VER_ROWS = 4;          // gated rows handled per pass
+
+struct VerParams {
+  const float *hidden; int64_t hidden_stride;
+  const float *g, *b;
+  const void *head;
+  const uint8_t *gate, *row_done;
+  const int32_t *spec_ptr, *spec_ids;
+  int32_t *token_out; uint8_t *verified_out; float *maxlogit_out, *logits_out;
+  uint8_t *done_out; int32_t *exit_layer_out, *full_heads;
+  int layer;
+  unsigned long long *scratch; unsigned int *counter;
+  int mode; int *err;
+  int B, d, V;
+};
+
+__device__ __forceinline__ bool ver_row_on(const VerParams &p, int r) {
+  if (p.row_done && p.row_done[r]) return false;
+  if (p.gate && !p.gate[r]) return false;
+  return true;
+}
+
+// Canonical LayerNorm of one row into smem `hn` by one warp (FAST) or one
+// thread (STRICT).  Identical bits to predictor_fast_kernel's LN.
+__device__ void warp_layernorm(const VerParams &p, int r, float *hn, int lane, bool strict,
+                               int *bad) {
+  const float *x = p.hidden + (size_t)r * p.hidden_stride;
+  const int d = p.d, nchunk = d / CHUNK;
+  const float df = (float)d;
+  for (int j = lane; j < d; j += 32) hn[j] = x[j];
+  __syncwarp();
+  float mean, denom;
+  if (!strict) {
+    float part[4] = {0.f, 0.f, 0.f, 0.f};
+    bool fin = true;
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+      for (int c = 32 * g + lane; c < nchunk; c += NPART)
+#pragma unroll
+        for (int e = 0; e < CHUNK; ++e) {
+          part[g] = __fadd_rn(part[g], hn[CHUNK * c + e]);
+          fin &= is_finite(hn[CHUNK * c + e]);
+        }
+    if (!fin) *bad = 1;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) part[g] = warp_butterfly_sum(part[g]);
+    mean = __fdiv_rn(canon_combine(part[0], part[1], part[2], part[3]), df);
+    float sq[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+      for (int c = 32 * g + lane; c < nchunk; c += NPART)
+#pragma unroll
+        for (int e = 0; e < CHUNK; ++e) {
+          const float xc = __fsub_rn(hn[CHUNK * c + e], mean);
+          sq[g] = __fmaf_rn(xc, xc, sq[g]);
+        }
+#pragma unroll
+    for (int g = 0; g < 4; ++g) sq[g] = warp_butterfly_sum(sq[g]);
+    const float var = __fdiv_rn(canon_combine(sq[0], sq[1], sq[2], sq[3]), df);
+    denom = __fsqrt_rn(__fadd_rn(var, 1e-5f));
+  } else {
+    float m = 0.f, v = 0.f;
+    bool fin = true;
+    if (lane == 0) {
+      for (int j = 0; j < d; ++j) { m = __fadd_rn(m, hn[j]); fin &= is_finite(hn[j]); }
+      m = __fdiv_rn(m, df);
+      for (int j = 0; j < d; ++j) {
+        const float xc = __fsub_rn(hn[j], m);
+        v = __fadd_rn(v, __fmul_rn(xc, xc));
+      }
+      v = __fsqrt_rn(__fadd_rn(__fdiv_rn(v, df), 1e-5f));
+      if (!fin) *bad = 1;
+    }
+    mean = __shfl_sync(0xffffffffu, m, 0);
+    denom = __shfl_sync(0xffffffffu, v, 0);
+  }
+  __syncwarp();
+  for (int j = lane; j < d; j += 32)
+    hn[j] = __fadd_rn(__fmul_rn(__fdiv_rn(__fsub_rn(hn[j], mean), denom), p.g[j]), p.b[j]);
+  __syncwarp();
+}
+
+// Canonical dot of one bf16 vocab row with R normed rows; warp-cooperative.
+template <typename TW, int R, int CPL>
+__device__ __forceinline__ void warp_cdot(const TW *wrow, const float *hn, int d,
+                                          int nr, int lane, float *out) {
+  const int nchunk = d / CHUNK;
+  float acc[R][4];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int g = 0; g < 4; ++g) acc[r][g] = 0.f;
+  // CPL = chunk steps per partial (nchunk <= 128*CPL)
+  Chunk<TW> w[4][CPL];
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+#pragma unroll
+    for (int s = 0; s < CPL; ++s) {
+      const int c = 32 * g + lane + NPART * s;
+      if (c < nchunk) w[g][s].load(wrow + CHUNK * c);
+      else w[g][s].zero();
+    }
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+#pragma unroll
+    for (int s = 0; s < CPL; ++s) {
+      const int c = 32 * g + lane + NPART * s;
+      if (c < nchunk) {
+        float wf[8];
+        w[g][s].to_f32(wf);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (r < nr) {
+            const float4 h0 = *reinterpret_cast<const float4 *>(hn + (size_t)r * d + CHUNK * c);
+            const float4 h1 = *reinterpret_cast<const float4 *>(hn + (size_t)r * d + CHUNK * c + 4);
+            const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+#pragma unroll
+            for (int e = 0; e < CHUNK; ++e) acc[r][g] = __fmaf_rn(hv[e], wf[e], acc[r][g]);
+          }
+        }
+      }
+    }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    float gs[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) gs[g] = warp_butterfly_sum(acc[r][g]);
+    out[r] = canon_combine(gs[0], gs[1], gs[2], gs[3]);
+  }
+}
+
+template <typename TW, int CPL>
+__global__ void __launch_bounds__(VER_THREADS)
+verify_kernel(VerParams p) {
+  const TW *head = reinterpret_cast<const TW *>(p.head);
+  extern __shared__ float hn[];           // VER_ROWS * d
+  __shared__ int s_rows[VER_ROWS];
+  __shared__ int s_nr, s_bad;
+  __shared__ unsigned long long s_best[VER_THREADS / 32][VER_ROWS];
+  __shared__ bool s_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = VER_THREADS / 32;
+  const bool strict = p.mode == SPX_MODE_STRICT;
+
+  __shared__ int s_next;
+  int r0 = 0;
+  while (true) {
+    // collect the next <= VER_ROWS gated rows (same on every CTA)
+    if (threadIdx.x == 0) {
+      int nr = 0, r = r0;
+      for (; r < p.B && nr < VER_ROWS; ++r)
+        if (ver_row_on(p, r)) s_rows[nr++] = r;
+      s_nr = nr;
+      s_bad = 0;
+      s_next = r;
+    }
+    __syncthreads();
+    r0 = s_next;
+    const int nr = s_nr;
+    if (nr == 0) break;
+    if (warp < nr) {
+      int bad = 0;
+      warp_layernorm(p, s_rows[warp], hn + (size_t)warp * p.d, lane, strict, &bad);
+      if (bad && lane == 0) { atomicOr(p.err, ERR_HIDDEN_NONFINITE); s_bad = 1; }
+    }
+    __syncthreads();
+    unsigned long long best[VER_ROWS];
+#pragma unroll
+    for (int r = 0; r < VER_ROWS; ++r) best[r] = 0ull;
+    const int gw = blockIdx.x * nwarps + warp, tw = gridDim.x * nwarps;
+    if (!strict) {
+      for (int v = gw; v < p.V; v += tw) {
+        float lg[VER_ROWS];
+        warp_cdot<TW, VER_ROWS, CPL>(head + (size_t)v * p.d, hn, p.d, nr, lane, lg);
+#pragma unroll
+        for (int r = 0; r < VER_ROWS; ++r) {
+          if (r < nr) {
+            const unsigned long long k = argmax_key(lg[r], (uint32_t)v);
+            best[r] = k > best[r] ? k : best[r];
+            if (p.logits_out && lane == 0) p.logits_out[(size_t)s_rows[r] * p.V + v] = lg[r];
+          }
+        }
+      }
+    } else {
+      // STRICT: one thread per vocab row, sequential chain over d (no FMA)
+      const int gt = blockIdx.x * VER_THREADS + threadIdx.x, tt = gridDim.x * VER_THREADS;
+      for (int v = gt; v < p.V; v += tt) {
+        const TW *wr = head + (size_t)v * p.d;
+        float acc[VER_ROWS] = {0.f, 0.f, 0.f, 0.f};
+        for (int j = 0; j < p.d; j += CHUNK) {
+          float wf[8];
+          load8_f32<TW>(wr + j, wf);
+#pragma unroll
+          for (int r = 0; r < VER_ROWS; ++r)
+            if (r < nr)
+#pragma unroll
+              for (int e = 0; e < CHUNK; ++e)
+                acc[r] = __fadd_rn(acc[r], __fmul_rn(hn[(size_t)r * p.d + j + e], wf[e]));
+        }
+#pragma unroll
+        for (int r = 0; r < VER_ROWS; ++r)
+          if (r < nr) {
+            const unsigned long long k = argmax_key(acc[r], (uint32_t)v);
+            best[r] = k > best[r] ? k : best[r];
+            if (p.logits_out) p.logits_out[(size_t)s_rows[r] * p.V + v] = acc[r];
+          }
+      }
+#pragma unroll
+      for (int r = 0; r < VER_ROWS; ++r)
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) {
+          const unsigned long long o = __shfl_xor_sync(0xffffffffu, best[r], m);
+          best[r] = o > best[r] ? o : best[r];
+        }
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int r = 0; r < VER_ROWS; ++r) s_best[warp][r] = best[r];
+    __syncthreads();
+    if (threadIdx.x < nr) {
+      unsigned long long b = 0ull;
+      for (int w = 0; w < nwarps; ++w) b = s_best[w][threadIdx.x] > b ? s_best[w][threadIdx.x] : b;
+      atomicMax(p.scratch + s_rows[threadIdx.x], b);
+    }
+    __syncthreads();
+    if (r0 >= p.B) break;
+  }
+  // ---- last CTA resolves argmax tokens, membership and the exit flag
+  __threadfence();
+  if (threadIdx.x == 0) s_last = (atomicAdd(p.counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int r = threadIdx.x; r < p.B; r += VER_THREADS) {
+    if (!ver_row_on(p, r)) continue;
+    const unsigned long long k = atomicExch(p.scratch + r, 0ull);
+    const int tok = (int)(0xffffffffu - (uint32_t)(k & 0xffffffffull));
+    const float mx = f32_from_order_key((uint32_t)(k >> 32));
+    bool in = false;
+    if (p.spec_ptr)
+      for (int i = p.spec_ptr[r]; i < p.spec_ptr[r + 1]; ++i) in |= (p.spec_ids[i] == tok);
+    p.token_out[r] = tok;
+    if (p.maxlogit_out) p.maxlogit_out[r] = mx;
+    if (p.verified_out) p.verified_out[r] = in ? 1 : 0;
+    if (p.full_heads) p.full_heads[r] += 1;
+    if (in && p.done_out) {
+      p.done_out[r] = 1;
+      if (p.exit_layer_out) p.exit_layer_out[r] = p.layer;
+    }
+  }
+  if (threadIdx.x == 0) *p.counter = 0u;
+}
+
+// Final LayerNorm of N rows into hn (FAST: canonical, STRICT: sequential).
+__global__ void final_norm_kernel(const float *x, int64_t stride, const float *g, const float *b,
+                                  float *hn, int N, int d, int mode, int *err) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= N) return;
+  VerParams p;
+  p.hidden = x; p.hidden_stride = stride; p.g = g; p.b = b; p.d = d;
+  int bad = 0;
+  warp_layernorm(p, row, hn + (size_t)row * d, lane, mode == SPX_MODE_STRICT, &bad);
+  if (bad && lane == 0) atomicOr(err, ERR_HIDDEN_NONFINITE);
+}
+
+}  // namespace spx
+
+using namespace spx;
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <typename TW>
+static int launch_verify(const VerParams &p, int nchunk, int grid, size_t smem,
+                         cudaStream_t stream) {
+#define SPX_LAUNCH_VER(CPL)                                                                    \
+  do {                                                                                         \
+    if (smem > 48 * 1024)                                                                      \
+      cudaFuncSetAttribute(verify_kernel<TW, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)smem);                                                         \
+    verify_kernel<TW, CPL><<<grid, VER_THREADS, smem, stream>>>(p);                            \
+  } while (0)
+  if (nchunk <= NPART) SPX_LAUNCH_VER(1);
+  else if (nchunk <= 2 * NPART) SPX_LAUNCH_VER(2);
+  else if (nchunk <= 4 * NPART) SPX_LAUNCH_VER(4);
+  else if (nchunk <= 8 * NPART) SPX_LAUNCH_VER(8);
+  else return SPX_EINVAL;
+#undef SPX_LAUNCH_VER
+  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+}
+
+extern "C" int spx_verify(const spx_verify_args *a, void *stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!a || a->B < 0 || a->d <= 0 || a->d % CHUNK || a->V <= 0 || a->V > 0x7fffffff) return SPX_EINVAL;
+  if (!a->hidden || !a->norm_g || !a->norm_b || !a->head || !a->token_out || !a->scratch ||
+      !a->counter || !a->err)
+    return SPX_EINVAL;
+  if (a->B == 0) return 0;
+  VerParams p;
+  p.hidden = a->hidden; p.hidden_stride = a->hidden_stride ? a->hidden_stride : a->d;
+  p.g = a->norm_g; p.b = a->norm_b;
+  p.head = a->head;
+  p.gate = a->gate; p.row_done = a->row_done; p.spec_ptr = a->spec_ptr; p.spec_ids = a->spec_ids;
+  p.token_out = a->token_out; p.verified_out = a->verified_out; p.maxlogit_out = a->maxlogit_out;
+  p.logits_out = a->logits_out; p.done_out = a->done_out; p.exit_layer_out = a->exit_layer_out;
+  p.full_heads = a->full_heads; p.layer = a->layer; p.scratch = a->scratch; p.counter = a->counter;
+  p.mode = a->mode; p.err = a->err; p.B = (int)a->B; p.d = (int)a->d; p.V = (int)a->V;
+  const size_t smem = (size_t)VER_ROWS * a->d * sizeof(float);
+  const int nchunk = (int)(a->d / CHUNK);
+  const int warps_per_cta = VER_THREADS / 32;
+  int grid = (int)((a->V + warps_per_cta - 1) / warps_per_cta);
+  const int cap = num_sms() * 2;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  if (a->head_dtype == SPX_DTYPE_BF16)
+    return launch_verify<__nv_bfloat16>(p, nchunk, grid, smem, stream);
+  if (a->head_dtype == SPX_DTYPE_F32) return launch_verify<float>(p, nchunk, grid, smem, stream);
+  return SPX_EINVAL;
+}
+
+extern "C" int spx_final_norm(const float *hidden, int64_t hidden_stride, const float *g,
+                              const float *b, float *hn, int64_t N, int64_t d, int32_t mode,
+                              int32_t *err, void *stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!hidden || !g || !b || !hn || !err || N < 0 || d <= 0 || d % CHUNK) return SPX_EINVAL;
+  if (N == 0) return 0;
+  const int wpc = 4;
+  final_norm_kernel<<<(unsigned)((N + wpc - 1) / wpc), wpc * 32, 0, stream>>>(
+      hidden, hidden_stride ? hidden_stride : d, g, b, hn, (int)N, (int)d, mode, err);
+  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+}

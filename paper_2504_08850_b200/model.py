@@ -1,0 +1,388 @@
+"""Device-resident model weights in B200 layouts plus the head operators --
+drop-in for the hot-path part of the reference's ``specexit.model``
+(src/specexit/model.py).
+
+Layouts in HBM (the reference keeps (in, out) f32 matrices):
+  lm_head      (V, d)      vocab-row major, so a speculative gather reads K
+                           contiguous rows (reference stores (d, V) and gathers
+                           strided columns, model.py:82, :313)
+  embedding    (V, d)
+  wqkv         (3d, d)     out-row major [wq^T; wk^T; wv^T]
+  wo           (d, d)      wo^T
+  ffn_w1       (ffn, d)    ffn.w1^T
+  ffn_w2       (d, ffn)    ffn.w2^T
+  norms/biases f32
+Weight storage is bf16 (production, ``dtype="bf16"``) or f32 (``dtype="f32"``,
+exact for reference weights that are not bf16-representable).  Accumulation
+is always fp32.
+"""
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import numerics, rng
+
+LN_EPS = np.float32(1e-5)                      # model.py:27
+CONFIG_FIELDS = ("vocab_size", "hidden_dim", "num_layers", "num_heads", "ffn_dim", "max_context")
+_TORCH_DTYPE = {"bf16": torch.bfloat16, "f32": torch.float32}
+_SPX_DTYPE = {"bf16": N.SPX_DTYPE_BF16, "f32": N.SPX_DTYPE_F32}
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    """model.py:32-56."""
+    vocab_size: int = 256
+    hidden_dim: int = 64
+    num_layers: int = 8
+    num_heads: int = 4
+    ffn_dim: int = 256
+    max_context: int = 512
+    seed: int = 0
+
+    def validate(self):
+        if self.vocab_size < 2:
+            raise ValueError("vocab_size must be >= 2")
+        if self.num_layers < 1:
+            raise ValueError("num_layers must be >= 1")
+        if min(self.hidden_dim, self.num_heads, self.ffn_dim, self.max_context) < 1:
+            raise ValueError("all dimensions must be positive")
+        if self.hidden_dim % self.num_heads != 0:
+            raise ValueError("hidden_dim must be divisible by num_heads")
+        if not 0 <= self.seed < 2 ** 64:
+            raise ValueError("seed must fit in 64 bits")
+
+    @property
+    def head_dim(self):
+        return self.hidden_dim // self.num_heads
+
+
+def tensor_specs(config: ModelConfig):
+    """model.py:59-84 -- declaration order fixes each tensor's seed index."""
+    d, f, v = config.hidden_dim, config.ffn_dim, config.vocab_size
+    specs = [("embedding", (v, d), "uniform")]
+    for i in range(config.num_layers):
+        p = f"layers.{i}"
+        specs += [(f"{p}.ln1.g", (d,), "ones"), (f"{p}.ln1.b", (d,), "zeros"),
+                  (f"{p}.attn.wq", (d, d), "uniform"), (f"{p}.attn.wk", (d, d), "uniform"),
+                  (f"{p}.attn.wv", (d, d), "uniform"), (f"{p}.attn.wo", (d, d), "uniform"),
+                  (f"{p}.ln2.g", (d,), "ones"), (f"{p}.ln2.b", (d,), "zeros"),
+                  (f"{p}.ffn.w1", (d, f), "uniform"), (f"{p}.ffn.b1", (f,), "zeros"),
+                  (f"{p}.ffn.w2", (f, d), "uniform"), (f"{p}.ffn.b2", (d,), "zeros")]
+    specs += [("final_norm.g", (d,), "ones"), ("final_norm.b", (d,), "zeros"),
+              ("lm_head", (d, v), "uniform")]
+    return specs
+
+
+def sinusoidal_encoding(max_len: int, dim: int) -> np.ndarray:
+    """model.py:112-118 (host, float64 then float32)."""
+    pe = np.zeros((max_len, dim), dtype=np.float64)
+    pos = np.arange(max_len)[:, None]
+    div = np.exp(np.arange(0, dim, 2) * (-math.log(10000.0) / dim))
+    pe[:, 0::2] = np.sin(pos * div)
+    pe[:, 1::2] = np.cos(pos * div)
+    return pe.astype(np.float32)
+
+
+# name suffix -> (device attribute, transpose-to-out-major)
+_LAYER_MAT = {"attn.wq": ("wqkv", 0), "attn.wk": ("wqkv", 1), "attn.wv": ("wqkv", 2),
+              "attn.wo": ("wo", None), "ffn.w1": ("ffn_w1", None), "ffn.w2": ("ffn_w2", None)}
+_LAYER_VEC = {"ln1.g": "ln1_g", "ln1.b": "ln1_b", "ln2.g": "ln2_g", "ln2.b": "ln2_b",
+              "ffn.b1": "ffn_b1", "ffn.b2": "ffn_b2"}
+
+
+class TransformerModel:
+    """Immutable device weights of one model (target or draft).  Shareable
+    across engines/streams (reference SPEC.md:112)."""
+
+    def __init__(self, config: ModelConfig, dtype: str = "bf16", head_only: bool = False):
+        config.validate()
+        if dtype not in _TORCH_DTYPE:
+            raise ValueError(f"unknown weight dtype {dtype!r}")
+        if config.hidden_dim % 8:
+            raise ValueError("hidden_dim must be a multiple of 8 on the B200 path")
+        N.require_cuda()
+        self.config, self.dtype, self.head_only = config, dtype, head_only
+        self.spx_dtype = _SPX_DTYPE[dtype]
+        td = _TORCH_DTYPE[dtype]
+        d, f, v, L = config.hidden_dim, config.ffn_dim, config.vocab_size, config.num_layers
+        dev = "cuda"
+        self.lm_head = torch.empty((v, d), dtype=td, device=dev)
+        self.final_g = torch.ones(d, dtype=torch.float32, device=dev)
+        self.final_b = torch.zeros(d, dtype=torch.float32, device=dev)
+        self.layers = []
+        if not head_only:
+            self.embedding = torch.empty((v, d), dtype=torch.float32, device=dev)
+            self.pos_encoding = torch.as_tensor(sinusoidal_encoding(config.max_context, d),
+                                                device=dev)
+            for _ in range(L):
+                self.layers.append({
+                    "ln1_g": torch.ones(d, device=dev), "ln1_b": torch.zeros(d, device=dev),
+                    "wqkv": torch.empty((3 * d, d), dtype=td, device=dev),
+                    "wo": torch.empty((d, d), dtype=td, device=dev),
+                    "ln2_g": torch.ones(d, device=dev), "ln2_b": torch.zeros(d, device=dev),
+                    "ffn_w1": torch.empty((f, d), dtype=td, device=dev),
+                    "ffn_b1": torch.zeros(f, device=dev),
+                    "ffn_w2": torch.empty((d, f), dtype=td, device=dev),
+                    "ffn_b2": torch.zeros(d, device=dev)})
+
+    # -- construction -------------------------------------------------------
+
+    def _target(self, name):
+        """(tensor, transpose flag) receiving reference tensor `name`."""
+        d = self.config.hidden_dim
+        if name == "lm_head":
+            return self.lm_head, True
+        if name == "embedding":
+            return (None if self.head_only else self.embedding), False
+        if name == "final_norm.g":
+            return self.final_g, False
+        if name == "final_norm.b":
+            return self.final_b, False
+        _, i, rest = name.split(".", 2)
+        if self.head_only:
+            return None, False
+        lay = self.layers[int(i)]
+        if rest in _LAYER_VEC:
+            return lay[_LAYER_VEC[rest]], False
+        attr, part = _LAYER_MAT[rest]
+        t = lay[attr]
+        if part is not None:
+            t = t[part * d:(part + 1) * d]
+        return t, True
+
+    def numel(self):
+        n = self.lm_head.numel() + 2 * self.config.hidden_dim
+        if not self.head_only:
+            n += self.embedding.numel() + sum(t.numel() for lay in self.layers for t in lay.values())
+        return n
+
+    def nbytes(self):
+        tot = self.lm_head.numel() * self.lm_head.element_size()
+        for lay in self.layers:
+            tot += sum(t.numel() * t.element_size() for t in lay.values())
+        return tot
+
+
+def init_model(config: ModelConfig, dtype: str = "bf16", head_only: bool = False) -> TransformerModel:
+    """model.py:121-137 evaluated on device (spx_init_uniform): the same
+    splitmix64 stream per tensor in declaration order, uniform(+-sqrt(6/(fan_in+
+    fan_out))), biases 0, gains 1 -- then stored as bf16 (RNE) or f32."""
+    m = TransformerModel(config, dtype, head_only)
+    L = N.lib()
+    for idx, (name, shape, kind) in enumerate(tensor_specs(config)):
+        if kind != "uniform":
+            continue                         # ones/zeros already in place
+        t, transpose = m._target(name)
+        if t is None:
+            continue
+        b = math.sqrt(6.0 / (shape[0] + shape[1]))
+        is_f32 = t.dtype == torch.float32
+        assert t.is_contiguous()
+        N.check(L.spx_init_uniform(N.ptr(t), int(is_f32), shape[0], shape[1], int(transpose),
+                                   rng.derive(config.seed, idx), -b, b, N.stream_ptr()),
+                "spx_init_uniform")
+    return m
+
+
+def from_tensors(config: ModelConfig, tensors: dict, dtype: str = "f32",
+                 head_only: bool = False) -> TransformerModel:
+    """Device model from reference-layout float32 tensors (e.g. a
+    ``TransformerModel.tensors`` dict of the reference, or SPXW contents)."""
+    expected = tensor_specs(config)
+    for name, shape, _ in expected:
+        if name not in tensors:
+            if head_only and name.startswith("layers."):
+                continue
+            raise ValueError("tensor names do not match config")
+        t = np.asarray(tensors[name])
+        if t.shape != shape:
+            raise ValueError(f"tensor {name}: bad shape/dtype {t.shape}/{t.dtype}")
+        if not np.all(np.isfinite(t)):
+            raise ValueError(f"tensor {name}: non-finite values")
+    m = TransformerModel(config, dtype, head_only)
+    for name, _, _ in expected:
+        dst, transpose = m._target(name)
+        if dst is None:
+            continue
+        src = torch.as_tensor(np.ascontiguousarray(tensors[name], dtype=np.float32))
+        if transpose:
+            src = src.t()
+        dst.copy_(src.to(dst.dtype))
+    return m
+
+
+# --- SPXW (model.py:355-434) -----------------------------------------------------
+
+
+def load_weights(path, dtype: str = "f32") -> TransformerModel:
+    """Read a reference SPXW weight file into device layouts."""
+    with open(path, "rb") as fh:
+        data = fh.read()
+    off = 0
+
+    def take(n):
+        nonlocal off
+        if off + n > len(data):
+            raise ValueError("truncated weight file")
+        b = data[off:off + n]
+        off += n
+        return b
+
+    if take(4) != b"SPXW":
+        raise ValueError("bad magic: not a weight file")
+    version = int.from_bytes(take(4), "little")
+    if version != 1:
+        raise ValueError(f"unsupported weight file version {version}")
+    count = int.from_bytes(take(4), "little")
+    tensors = {}
+    for _ in range(count):
+        nlen = int.from_bytes(take(2), "little")
+        name = take(nlen).decode()
+        rank = int.from_bytes(take(1), "little")
+        shape = tuple(int.from_bytes(take(4), "little") for _ in range(rank))
+        n = int(np.prod(shape)) if shape else 1
+        tensors[name] = np.frombuffer(take(4 * n), "<f4").reshape(shape)
+    if "config" not in tensors:
+        raise ValueError("weight file missing config pseudo-tensor")
+    vec = tensors.pop("config")
+    if vec.size != len(CONFIG_FIELDS) + 4:
+        raise ValueError("bad config pseudo-tensor length")
+    fields = {f: int(v) for f, v in zip(CONFIG_FIELDS, vec)}
+    seed = sum(int(v) << (16 * i) for i, v in enumerate(vec[len(CONFIG_FIELDS):]))
+    return from_tensors(ModelConfig(seed=seed, **fields), tensors, dtype)
+
+
+# --- head operators (the function-level drop-ins) --------------------------------
+
+
+def _rows(hidden, d):
+    h = hidden if isinstance(hidden, torch.Tensor) else torch.as_tensor(np.asarray(hidden, np.float32))
+    h = h.to(device="cuda", dtype=torch.float32)
+    if h.dim() == 1:
+        h = h.reshape(1, -1)
+    if h.shape[-1] != d:
+        raise ValueError("hidden dimension mismatch")
+    return h.contiguous()
+
+
+def final_norm(model: TransformerModel, hidden) -> torch.Tensor:
+    """Final LayerNorm of (N, d) rows (model.py:140-146 with final_norm.*)."""
+    h = _rows(hidden, model.config.hidden_dim)
+    out = torch.empty_like(h)
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.check(N.lib().spx_final_norm(N.ptr(h), h.shape[1], N.ptr(model.final_g),
+                                   N.ptr(model.final_b), N.ptr(out), h.shape[0], h.shape[1],
+                                   numerics.mode(), N.ptr(err), N.stream_ptr()), "spx_final_norm")
+    N.raise_device_error(err.item())
+    return out
+
+
+def merged_logits(model: TransformerModel, hn: torch.Tensor, id_lists) -> list:
+    """K6: logits of node j for id_lists[j], one HBM read per unique id."""
+    flat = np.concatenate([np.asarray(ids, np.int64).reshape(-1) for ids in id_lists])
+    sizes = [len(ids) for ids in id_lists]
+    node = np.repeat(np.arange(len(id_lists), dtype=np.int64), sizes)
+    out_idx = np.arange(flat.size, dtype=np.int64)
+    if flat.size and (flat.min() < 0 or flat.max() >= model.config.vocab_size):
+        raise ValueError("token id out of range")
+    uniq, inv = np.unique(flat, return_inverse=True)
+    order = np.argsort(inv, kind="stable")
+    counts = np.bincount(inv, minlength=uniq.size)
+    uptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    dev = lambda a: torch.as_tensor(np.ascontiguousarray(a, np.int32), device="cuda")  # noqa: E731
+    d_uniq, d_uptr = dev(uniq), dev(uptr)
+    d_node, d_out = dev(node[order]), dev(out_idx[order])
+    logits = torch.empty(flat.size, dtype=torch.float32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.check(N.lib().spx_tree_merged_logits(N.ptr(hn), hn.shape[0], N.ptr(model.lm_head),
+                                           model.spx_dtype, model.config.vocab_size,
+                                           model.config.hidden_dim, N.ptr(d_uniq), uniq.size,
+                                           N.ptr(d_uptr), N.ptr(d_node), N.ptr(d_out),
+                                           N.ptr(logits), N.ptr(err), N.stream_ptr()),
+            "spx_tree_merged_logits")
+    N.raise_device_error(err.item())
+    return list(torch.split(logits, sizes))
+
+
+def sliced_head_logits(model: TransformerModel, hidden, token_ids) -> torch.Tensor:
+    """model.py:298-314: logits of selected vocabulary rows only (K1 order)."""
+    ids = np.asarray(token_ids.cpu() if isinstance(token_ids, torch.Tensor) else token_ids,
+                     dtype=np.int64).reshape(-1)
+    if ids.size == 0:
+        raise ValueError("empty token id list")
+    if ids.min() < 0 or ids.max() >= model.config.vocab_size:
+        raise ValueError("token id out of range")
+    hn = final_norm(model, hidden)
+    return merged_logits(model, hn, [ids])[0]
+
+
+class _VerifyScratch:
+    _per_device = {}
+
+    @classmethod
+    def get(cls, B):
+        key = torch.cuda.current_device()
+        s = cls._per_device.get(key)
+        if s is None or s[0].numel() < B:
+            s = (torch.zeros(max(B, 64), dtype=torch.int64, device="cuda"),
+                 torch.zeros(1, dtype=torch.int32, device="cuda"))
+            cls._per_device[key] = s
+        return s
+
+
+def head_argmax(model: TransformerModel, hidden, spec_lists=None, want_logits=False):
+    """K4 on N rows: (tokens, verified, logits|None).  spec_lists: per-row
+    verify sets (or None)."""
+    h = _rows(hidden, model.config.hidden_dim)
+    B, V = h.shape[0], model.config.vocab_size
+    tok = torch.empty(B, dtype=torch.int32, device="cuda")
+    ver = torch.zeros(B, dtype=torch.uint8, device="cuda")
+    logits = torch.empty((B, V), dtype=torch.float32, device="cuda") if want_logits else None
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    scratch, counter = _VerifyScratch.get(B)
+    a = N.VerifyArgs()
+    a.hidden, a.hidden_stride = N.ptr(h), h.shape[1]
+    a.norm_g, a.norm_b = N.ptr(model.final_g), N.ptr(model.final_b)
+    a.head, a.head_dtype = N.ptr(model.lm_head), model.spx_dtype
+    keep = []
+    if spec_lists is not None:
+        ptr_ = np.concatenate([[0], np.cumsum([len(s) for s in spec_lists])]).astype(np.int32)
+        ids = np.concatenate([np.asarray(s, np.int32).reshape(-1) for s in spec_lists]
+                             ) if len(spec_lists) else np.zeros(0, np.int32)
+        d_ptr = torch.as_tensor(ptr_, device="cuda")
+        d_ids = torch.as_tensor(np.ascontiguousarray(ids, np.int32), device="cuda")
+        keep += [d_ptr, d_ids]
+        a.spec_ptr, a.spec_ids = N.ptr(d_ptr), N.ptr(d_ids) if ids.size else N.ptr(d_ptr)
+    a.token_out, a.verified_out = N.ptr(tok), N.ptr(ver)
+    a.logits_out = N.ptr(logits)
+    a.scratch, a.counter = N.ptr(scratch), N.ptr(counter)
+    a.mode, a.err = numerics.mode(), N.ptr(err)
+    a.B, a.d, a.V = B, model.config.hidden_dim, V
+    N.check(N.lib().spx_verify(a, N.stream_ptr()), "spx_verify")
+    N.raise_device_error(err.item())
+    return tok, ver, logits
+
+
+def full_head_logits(model: TransformerModel, hidden) -> torch.Tensor:
+    """model.py:289-295: final norm then the full LM-head projection."""
+    _, _, logits = head_argmax(model, hidden, want_logits=True)
+    return logits[0] if (isinstance(hidden, torch.Tensor) and hidden.dim() == 1) or \
+        np.ndim(hidden) == 1 else logits
+
+
+def layer_norm(x, g, b) -> torch.Tensor:
+    """model.py:140-146 for (n, d) rows with arbitrary gain/bias on device."""
+    h = _rows(x, int(np.shape(x)[-1]))
+    gt = torch.as_tensor(np.asarray(g, np.float32) if not isinstance(g, torch.Tensor) else g,
+                         device="cuda", dtype=torch.float32).contiguous()
+    bt = torch.as_tensor(np.asarray(b, np.float32) if not isinstance(b, torch.Tensor) else b,
+                         device="cuda", dtype=torch.float32).contiguous()
+    out = torch.empty_like(h)
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.check(N.lib().spx_final_norm(N.ptr(h), h.shape[1], N.ptr(gt), N.ptr(bt), N.ptr(out),
+                                   h.shape[0], h.shape[1], numerics.mode(), N.ptr(err),
+                                   N.stream_ptr()), "spx_final_norm")
+    return out

@@ -1,0 +1,345 @@
+"""Exit features and the per-layer MLP exit predictor -- drop-in for the
+reference's ``specexit.predictor`` (src/specexit/predictor.py), evaluated by
+the sm_100a kernels of libspecexit_b200.so.
+
+Same names, signatures and error behaviour as the reference:
+``FeatureVector``, ``uniform_probs``, ``extract_features``,
+``PredictorWeights``, ``init_predictor``, ``predictor_forward``,
+``decide_exit``, ``predictor_param_count``, ``save_predictors`` /
+``load_predictors`` (SPXP).  Arrays may be numpy arrays or torch tensors;
+returned arrays are torch CUDA tensors.
+
+``PredictorBank`` packs a ``{layer: PredictorWeights}`` dict into one device
+buffer per field (the layout the fused kernel reads), and ``z_cut`` turns the
+reference's float64 ``sigmoid(z) > threshold`` into the equivalent exact f32
+comparison ``z >= z_cut`` evaluated in-kernel.
+"""
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from . import numerics, rng
+
+
+def _dev(x, dtype=torch.float32):
+    if isinstance(x, torch.Tensor):
+        return x.to(device="cuda", dtype=dtype).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device="cuda")
+
+
+@dataclass(frozen=True)
+class FeatureVector:
+    """predictor.py:22-33: [spec_logits | local_probs | prob_variation]."""
+    spec_logits: torch.Tensor
+    local_probs: torch.Tensor
+    prob_variation: torch.Tensor
+
+    @property
+    def k(self):
+        return int(self.spec_logits.numel())
+
+    def concat(self) -> torch.Tensor:
+        return torch.cat([self.spec_logits, self.local_probs, self.prob_variation]).float()
+
+
+def uniform_probs(k: int) -> torch.Tensor:
+    """predictor.py:36-39."""
+    return torch.full((k,), np.float32(1.0 / k).item(), dtype=torch.float32, device="cuda")
+
+
+def extract_features(spec_logits, prev_local_probs) -> FeatureVector:
+    """predictor.py:42-52 on device (spx_extract_features)."""
+    N.require_cuda()
+    lg = _dev(spec_logits).reshape(-1)
+    pv = _dev(prev_local_probs).reshape(-1)
+    if lg.numel() < 1 or tuple(np.shape(spec_logits)) != tuple(np.shape(prev_local_probs)):
+        raise ValueError("bad feature input shapes")
+    k = lg.numel()
+    if k > 64:
+        raise ValueError("speculative set larger than 64 is not supported on device")
+    out = torch.empty(3 * k, dtype=torch.float32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.check(N.lib().spx_extract_features(N.ptr(lg), N.ptr(pv), N.ptr(out), N.ptr(err), 1, k,
+                                         N.stream_ptr()), "spx_extract_features")
+    N.raise_device_error(err.item())
+    return FeatureVector(spec_logits=lg, local_probs=out[k:2 * k], prob_variation=out[2 * k:])
+
+
+@dataclass
+class PredictorWeights:
+    """predictor.py:55-75 (host arrays; validated like the reference)."""
+    w1: np.ndarray
+    b1: np.ndarray
+    w2: np.ndarray
+    b2: float
+    threshold: float = 0.5
+
+    def __post_init__(self):
+        if self.w1.shape[1] != np.size(self.b1) or self.w1.shape[1] != np.size(self.w2):
+            raise ValueError("predictor weight shapes inconsistent")
+        if not 0.0 < self.threshold < 1.0:
+            raise ValueError("threshold must lie in (0, 1)")
+
+    @property
+    def k(self):
+        return self.w1.shape[0] // 3
+
+    @property
+    def hidden(self):
+        return self.w1.shape[1]
+
+
+def init_predictor(k: int, hidden: int, seed: int, threshold: float = 0.5) -> PredictorWeights:
+    """predictor.py:78-84 (same seeded values)."""
+    d = 3 * k
+    b = np.sqrt(6.0 / (d + hidden))
+    w1 = rng.uniform(rng.derive(seed, 0), d * hidden, -b, b).reshape(d, hidden)
+    b2 = np.sqrt(6.0 / (hidden + 1))
+    w2 = rng.uniform(rng.derive(seed, 1), hidden, -b2, b2)
+    return PredictorWeights(w1=w1, b1=np.zeros(hidden, np.float32), w2=w2, b2=0.0,
+                            threshold=threshold)
+
+
+def _sigmoid64(z):
+    """predictor.py:87-94 (float64), host side, for the cut search."""
+    z = np.asarray(z, dtype=np.float64)
+    out = np.empty_like(z)
+    pos = z >= 0
+    out[pos] = 1.0 / (1.0 + np.exp(-z[pos]))
+    ez = np.exp(z[~pos])
+    out[~pos] = ez / (1.0 + ez)
+    return out
+
+
+def _ord_to_f32(o):
+    o = np.asarray(o, dtype=np.int64)
+    bits = np.where(o >= 0, o, (-o) | 0x80000000).astype(np.uint32)
+    return bits.view(np.float32)
+
+
+_ZCUT_CACHE = {}
+
+
+def z_cut(threshold: float) -> float:
+    """Smallest float32 z with sigmoid(float64(z)) > threshold (the reference's
+    decision, predictor.py:87-109, is monotone in the f32 logit, so
+    ``prob > threshold`` == ``z >= z_cut``).  +inf/NaN edge cases: never fires
+    returns NaN; always fires returns -inf."""
+    thr = float(threshold)
+    if thr in _ZCUT_CACHE:
+        return _ZCUT_CACHE[thr]
+    lo, hi = -0x7F800000, 0x7F800000        # ordered ints of -inf, +inf
+    fires = lambda o: bool(_sigmoid64(_ord_to_f32(o).astype(np.float64)) > thr)  # noqa: E731
+    if not fires(hi):
+        cut = float("nan")
+    elif fires(lo):
+        cut = float("-inf")
+    else:
+        while hi - lo > 1:                  # invariant: !fires(lo), fires(hi)
+            mid = (lo + hi) // 2
+            if fires(mid):
+                hi = mid
+            else:
+                lo = mid
+        cut = float(_ord_to_f32(hi))
+    _ZCUT_CACHE[thr] = cut
+    return cut
+
+
+def predictor_forward(w: PredictorWeights, features) -> float:
+    """predictor.py:97-103 on device (spx_predictor_mlp); returns the float64
+    probability as a Python float."""
+    N.require_cuda()
+    f = features.concat() if isinstance(features, FeatureVector) else _dev(features).reshape(-1)
+    if tuple(f.shape) != (w.w1.shape[0],):
+        raise ValueError(f"feature dimension {tuple(f.shape)} does not match predictor {w.w1.shape}")
+    k, H = w.k, w.hidden
+    dw = _DeviceWeights.of(w)
+    prob = torch.empty(1, dtype=torch.float64, device="cuda")
+    N.check(N.lib().spx_predictor_mlp(N.ptr(f.contiguous()), N.ptr(dw.w1), N.ptr(dw.b1),
+                                      N.ptr(dw.w2), float(np.float32(w.b2)), float("nan"), None,
+                                      N.ptr(prob), None, 1, k, H, N.stream_ptr()),
+            "spx_predictor_mlp")
+    return float(prob.item())
+
+
+def decide_exit(prob: float, threshold: float) -> bool:
+    """predictor.py:106-109 (strict >)."""
+    return prob > threshold
+
+
+def predictor_param_count(k: int, hidden: int, num_layers: int):
+    """predictor.py:204-213: (4, 512, 32) -> (212992, 416.0)."""
+    if min(k, hidden, num_layers) < 1:
+        raise ValueError("arguments must be positive")
+    per_layer = 3 * k * hidden + hidden
+    return per_layer * num_layers, per_layer * num_layers * 2 / 1024
+
+
+class _DeviceWeights:
+    """One PredictorWeights on device (cached per object identity)."""
+    _cache = {}
+
+    def __init__(self, w):
+        self.w1 = _dev(np.asarray(w.w1, np.float32))
+        self.b1 = _dev(np.asarray(w.b1, np.float32))
+        self.w2 = _dev(np.asarray(w.w2, np.float32))
+
+    @classmethod
+    def of(cls, w):
+        key = id(w)
+        ent = cls._cache.get(key)
+        if ent is None or ent[0] is not w:
+            ent = (w, cls(w))
+            cls._cache[key] = ent
+        return ent[1]
+
+
+class PredictorBank:
+    """Device-packed per-layer predictors: w1 (L, 3K, H), b1 (L, H), w2 (L, H),
+    b2 (L,) f32, plus the set of covered layers (PredictorPolicy raises
+    KeyError for an active layer without a predictor, engine.py:90-91)."""
+
+    def __init__(self, bank: dict, num_layers: int):
+        if not bank:
+            raise ValueError("empty predictor bank")
+        ks = {w.k for w in bank.values()}
+        hs = {w.hidden for w in bank.values()}
+        if len(ks) != 1 or len(hs) != 1:
+            raise ValueError("mixed predictor shapes in bank")
+        self.k, self.hidden = ks.pop(), hs.pop()
+        self.layers = frozenset(int(l) for l in bank)
+        self.num_layers = num_layers
+        n = 3 * self.k
+        w1 = np.zeros((num_layers, n, self.hidden), np.float32)
+        b1 = np.zeros((num_layers, self.hidden), np.float32)
+        w2 = np.zeros((num_layers, self.hidden), np.float32)
+        self.b2 = np.zeros(num_layers, np.float32)
+        for l, w in bank.items():
+            if not 0 <= l < num_layers:
+                continue
+            w1[l], b1[l], w2[l] = w.w1, w.b1, w.w2
+            self.b2[l] = np.float32(w.b2)
+        self.w1, self.b1, self.w2 = _dev(w1), _dev(b1), _dev(w2)
+        self.mask = sum(1 << l for l in self.layers if l < 64)
+
+
+# --- SPXP persistence (predictor.py:284-342), same byte format -----------------
+
+SPXP_MAGIC = b"SPXP"
+SPXP_VERSION = 1
+
+
+def save_predictors(bank: dict, path):
+    if not bank:
+        raise ValueError("empty predictor bank")
+    ks = {w.k for w in bank.values()}
+    hs = {w.hidden for w in bank.values()}
+    if len(ks) != 1 or len(hs) != 1:
+        raise ValueError("mixed predictor shapes in bank")
+    k, hidden = ks.pop(), hs.pop()
+    with open(path, "wb") as fh:
+        fh.write(SPXP_MAGIC)
+        fh.write(SPXP_VERSION.to_bytes(4, "little"))
+        fh.write(k.to_bytes(4, "little"))
+        fh.write(hidden.to_bytes(4, "little"))
+        fh.write(len(bank).to_bytes(4, "little"))
+        for layer in sorted(bank):
+            w = bank[layer]
+            fh.write(int(layer).to_bytes(4, "little"))
+            fh.write(np.float32(w.threshold).tobytes())
+            for arr in (w.w1, w.b1, w.w2, np.array([w.b2], np.float32)):
+                fh.write(np.ascontiguousarray(arr, dtype="<f4").tobytes())
+
+
+def load_predictors(path) -> dict:
+    with open(path, "rb") as fh:
+        data = fh.read()
+    off = 0
+
+    def read(n):
+        nonlocal off
+        if off + n > len(data):
+            raise ValueError("truncated predictor file")
+        b = data[off:off + n]
+        off += n
+        return b
+
+    if read(4) != SPXP_MAGIC:
+        raise ValueError("bad magic: not a predictor file")
+    version = int.from_bytes(read(4), "little")
+    if version != SPXP_VERSION:
+        raise ValueError(f"unsupported predictor file version {version}")
+    k = int.from_bytes(read(4), "little")
+    hidden = int.from_bytes(read(4), "little")
+    count = int.from_bytes(read(4), "little")
+    bank = {}
+    for _ in range(count):
+        layer = int.from_bytes(read(4), "little")
+        threshold = float(np.frombuffer(read(4), "<f4")[0])
+        w1 = np.frombuffer(read(4 * 3 * k * hidden), "<f4").reshape(3 * k, hidden).copy()
+        b1 = np.frombuffer(read(4 * hidden), "<f4").copy()
+        w2 = np.frombuffer(read(4 * hidden), "<f4").copy()
+        b2 = float(np.frombuffer(read(4), "<f4")[0])
+        bank[layer] = PredictorWeights(w1=w1, b1=b1, w2=w2, b2=b2, threshold=threshold)
+    return bank
+
+
+class BatchResult:
+    """Outputs of one fused launch (device tensors)."""
+
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+def evaluate_batch(model, weights, hidden, ids, prev, threshold=0.5, layer=0, outputs=True,
+                   row_layer_mask=None, row_done=None, evals=None, err=None, mode=None,
+                   policy=None, out=None):
+    """K1+K2+K3 for B rows at one layer in ONE launch (spx_predictor_eval).
+
+    model: TransformerModel (head + final norm used); weights: PredictorWeights
+    or PredictorBank (row `layer` used); hidden (B, d) f32 CUDA; ids (B, K)
+    int32 CUDA; prev (B, K) f32 CUDA, updated in place with the new local
+    probabilities.  policy: None (MLP) or a constant probability (Never /
+    Always policies).  Returns a BatchResult of device tensors (no sync)."""
+    B, d = hidden.shape
+    K = ids.shape[1]
+    dev = hidden.device
+    if out is None:
+        out = BatchResult(
+            logits=torch.empty((B, K), dtype=torch.float32, device=dev) if outputs else None,
+            z=torch.empty(B, dtype=torch.float32, device=dev) if outputs else None,
+            prob=torch.empty(B, dtype=torch.float64, device=dev) if outputs else None,
+            fired=torch.empty(B, dtype=torch.uint8, device=dev),
+            err=err if err is not None else torch.zeros(1, dtype=torch.int32, device=dev))
+    a = N.PredictorArgs()
+    a.hidden, a.hidden_stride = N.ptr(hidden), hidden.stride(0)
+    a.norm_g, a.norm_b = N.ptr(model.final_g), N.ptr(model.final_b)
+    a.head, a.head_dtype = N.ptr(model.lm_head), model.spx_dtype
+    a.ids, a.prev = N.ptr(ids), N.ptr(prev)
+    if policy is None:
+        if isinstance(weights, PredictorBank):
+            a.w1 = N._vp(weights.w1[layer].data_ptr())
+            a.b1 = N._vp(weights.b1[layer].data_ptr())
+            a.w2 = N._vp(weights.w2[layer].data_ptr())
+            a.b2 = float(weights.b2[layer])
+            H = weights.hidden
+        else:
+            dw = _DeviceWeights.of(weights)
+            a.w1, a.b1, a.w2, a.b2 = N.ptr(dw.w1), N.ptr(dw.b1), N.ptr(dw.w2), float(np.float32(weights.b2))
+            H = weights.hidden
+        a.policy = N.SPX_POLICY_MLP
+        a.z_cut = z_cut(threshold)
+    else:
+        a.policy, a.const_prob, a.threshold, H = N.SPX_POLICY_CONST, float(policy), float(threshold), 0
+    a.logits_out, a.z_out, a.prob_out = N.ptr(out.logits), N.ptr(out.z), N.ptr(out.prob)
+    a.fired = N.ptr(out.fired)
+    a.row_layer_mask, a.row_done, a.evals = N.ptr(row_layer_mask), N.ptr(row_done), N.ptr(evals)
+    a.layer = layer
+    a.mode = numerics.mode() if mode is None else mode
+    a.err = N.ptr(out.err)
+    a.B, a.d, a.V, a.K, a.H = B, d, model.config.vocab_size, K, H
+    N.check(N.lib().spx_predictor_eval(a, N.stream_ptr()), "spx_predictor_eval")
+    return out
