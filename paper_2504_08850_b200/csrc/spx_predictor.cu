@@ -1,10 +1,10 @@
 // K1+K2+K3: fused speculative early-exit predictor evaluation (sm_100a).
 //
 // One launch evaluates one decoder layer's exit predictor for B rows
-// (independent requests, or tree nodes).  Per row it does, in one CTA:
+// (independent requests, or tree nodes).  Per row:
 //   final LayerNorm of the hidden row        reference model.py:140-146, :312
 //   gather of the K speculative LM-head rows reference model.py:313 (our head
-//     is stored (V, d) bf16 so a gather is K contiguous 8 KiB rows)
+//     is stored (V, d) so the gather is K contiguous rows, fetched by TMA)
 //   K local logits                          reference model.py:314
 //   softmax over the K ids + delta vs prev  reference predictor.py:42-52,
 //                                           model.py:149-152
@@ -13,23 +13,32 @@
 //                                           :106-109
 // and writes prob / fired / the updated local probs (the next layer's
 // "prev", engine.py:196) to device memory.  Rows whose engine state says
-// "already exited" or "layer not scheduled" return at entry: that is how the
-// device exit flag gates later launches without a host sync.
+// "already exited" or "layer not scheduled" are skipped at entry: that is how
+// the device exit flag gates later launches without a host sync.
+//
+// FAST kernel (production): persistent, one CTA per SM, one WARP per row.
+// Each warp owns a shared-memory stage (hidden row + G LM-head rows) filled by
+// 1-D TMA bulk copies (cp.async.bulk, mbarrier completion); the next row's
+// copies are issued as soon as the current row's dot products are done, so
+// HBM traffic overlaps the softmax/MLP tail.  The predictor weights (W1, b1,
+// w2) and the final-norm params are staged in shared memory once per CTA.
+// Every reduction is the canonical CDOT order (spx_common.cuh).
 //
 // MLP arithmetic reproduces the reference's numpy/OpenBLAS (SkylakeX
 // kernels) order exactly: z1 = ascending FMA chain from 0 (3K <= 48) or
 // 8/4/2/1-column blocks each chained from 0 and added (3K >= 51), then + b1;
-// z2 = the AVX-512 sdot tree.  The decision is
-// z2 >= z_cut with z_cut the smallest f32 whose f64 sigmoid exceeds the
-// threshold, so the decision is exactly the reference's `prob > threshold`.
+// z2 = the AVX-512 sdot tree.  The decision is z2 >= z_cut with z_cut the
+// smallest f32 whose f64 sigmoid exceeds the threshold, i.e. exactly the
+// reference's `prob > threshold`.
 #include "spx_common.cuh"
 #include "../../include/specexit_b200.h"
 
 namespace spx {
 
-constexpr int PRED_THREADS = 128;     // 4 warps == the 128 canonical partials
 constexpr int MAXK = 64;
 constexpr int MAXH = 1024;
+constexpr int GROUP = 4;              // LM-head rows per TMA stage
+constexpr int MAXW = 8;               // warps (row slots) per CTA
 
 struct PredParams {
   const float *hidden; int64_t hidden_stride;
@@ -54,297 +63,404 @@ struct PredParams {
   int B, d, V, K, H;
 };
 
-template <int G>
-__device__ __forceinline__ void cta_canon_reduce(float (&v)[G], float *red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int g = 0; g < G; ++g) v[g] = warp_butterfly_sum(v[g]);
-  if (lane == 0) {
-#pragma unroll
-    for (int g = 0; g < G; ++g) red[g * 4 + warp] = v[g];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-    v[g] = canon_combine(red[g * 4 + 0], red[g * 4 + 1], red[g * 4 + 2], red[g * 4 + 3]);
-  __syncthreads();
-}
-
-// ---------------------------------------------------------------- MLP tail
-// Shared by both reduction policies; runs after feats[0..3K) are in smem.
-__device__ void mlp_and_decide(const PredParams &p, int row, const float *feats, float *hs,
-                               float *as, bool row_ok) {
-  const int tid = threadIdx.x;
-  const int n = 3 * p.K, H = p.H;
-  // z1 / ReLU for units j = tid + 128 m
-  for (int j = tid; j < H; j += PRED_THREADS) {
-    float y;
-    if (n <= 48) {
-      float acc = 0.0f;
-      for (int i = 0; i < n; ++i) acc = __fmaf_rn(feats[i], __ldg(p.w1 + (size_t)i * H + j), acc);
-      y = acc;
-    } else {
-      y = 0.0f;
-      int i = 0;
-      const int blocks[4] = {8, 4, 2, 1};
-      for (int bi = 0; bi < 4; ++bi) {
-        const int bs = blocks[bi];
-        while (n - i >= bs) {
-          float t = 0.0f;
-          for (int q = 0; q < bs; ++q)
-            t = __fmaf_rn(feats[i + q], __ldg(p.w1 + (size_t)(i + q) * H + j), t);
-          y = __fadd_rn(y, t);
-          i += bs;
-          if (bs != 8) break;
-        }
-      }
-    }
-    const float z1 = __fadd_rn(y, __ldg(p.b1 + j));
-    hs[j] = z1 > 0.0f ? z1 : 0.0f;
-  }
-  __syncthreads();
-  // z2: OpenBLAS SkylakeX sdot order (sdot.c + sdot_microk_skylakex-2.c)
-  const int n1 = H & ~31, n64 = n1 & ~63;
-  if (tid < 64) {
-    float a = 0.0f;
-    for (int b = 0; b < n64; b += 64) a = __fmaf_rn(hs[b + tid], __ldg(p.w2 + b + tid), a);
-    as[tid] = a;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    float dot = 0.0f;
-    if (n1) {
-      float s[8];
-#pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        float acc[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          acc[a] = __fadd_rn(as[16 * a + m], as[16 * a + m + 8]);
-          if (n1 > n64) acc[a] = __fmaf_rn(hs[n64 + 8 * a + m], __ldg(p.w2 + n64 + 8 * a + m), acc[a]);
-        }
-        s[m] = __fadd_rn(__fadd_rn(__fadd_rn(acc[0], acc[1]), acc[2]), acc[3]);
-      }
-      float hh[4];
-#pragma unroll
-      for (int m = 0; m < 4; ++m) hh[m] = __fadd_rn(s[m], s[m + 4]);
-      dot = __fadd_rn(__fadd_rn(hh[0], hh[1]), __fadd_rn(hh[2], hh[3]));
-    }
-    for (int i = n1; i < H; ++i) dot = __fadd_rn(dot, __fmul_rn(hs[i], __ldg(p.w2 + i)));
-    const float z2 = __fadd_rn(dot, p.b2);
-    // predictor.py:87-94 in float64
-    const double z = (double)z2;
-    double prob;
-    if (z >= 0.0) prob = 1.0 / (1.0 + exp(-z));
-    else { const double ez = exp(z); prob = ez / (1.0 + ez); }
-    const bool fire = row_ok && (z2 >= p.z_cut);
-    if (p.z_out) p.z_out[row] = z2;
-    if (p.prob_out) p.prob_out[row] = prob;
-    if (p.fired) p.fired[row] = fire ? 1 : 0;
-  }
-}
-
-// Softmax over the K logits (model.py:149-152), features (predictor.py:51-52),
-// validation (predictor.py:45-50).  logits in feats[0..K); writes feats[K..3K).
-__device__ bool softmax_features(const PredParams &p, int row, float *feats, float *scratch) {
-  const int tid = threadIdx.x, K = p.K;
-  __shared__ float s_max, s_sum;
-  __shared__ int s_bad;
-  if (tid == 0) {
-    float m = feats[0];
-    bool bad = false;
-    double ps = 0.0;
-    float psf = 0.0f;
-    for (int c = 0; c < K; ++c) {
-      const float x = feats[c];
-      bad |= !is_finite(x);
-      m = fmaxf(m, x);
-      psf = __fadd_rn(psf, p.prev[(size_t)row * K + c]);
-    }
-    ps = (double)psf;
-    int e = 0;
-    if (bad) e |= ERR_LOGIT_NONFINITE;
-    if (fabs(ps - 1.0) > 1e-5) e |= ERR_PREV_SUM;
-    s_bad = e;
-    s_max = m;
-    if (e) atomicOr(p.err, e);
-  }
-  __syncthreads();
-  if (s_bad) return false;
-  if (tid < K) scratch[tid] = np_expf(__fsub_rn(feats[tid], s_max));
-  __syncthreads();
-  if (tid == 0) {
-    float acc = 0.0f;
-    for (int c = 0; c < K; ++c) acc = __fadd_rn(acc, scratch[c]);   // seq_sum
-    s_sum = acc;
-  }
-  __syncthreads();
-  if (tid < K) {
-    const float pr = __fdiv_rn(scratch[tid], s_sum);
-    const float pv = p.prev[(size_t)row * K + tid];
-    feats[K + tid] = pr;
-    feats[2 * K + tid] = __fsub_rn(pr, pv);
-  }
-  __syncthreads();
-  return true;
-}
-
 __device__ __forceinline__ bool row_skipped(const PredParams &p, int row) {
   if (p.row_done && p.row_done[row]) return true;
   if (p.row_layer_mask && !((p.row_layer_mask[row] >> p.layer) & 1ull)) return true;
   return false;
 }
 
-__device__ void finish_row(const PredParams &p, int row, float *feats, float *hs, float *as,
-                           float *scratch) {
-  const int tid = threadIdx.x, K = p.K;
-  const bool ok = softmax_features(p, row, feats, scratch);
-  if (tid < K) {
-    if (p.logits_out) p.logits_out[(size_t)row * K + tid] = feats[tid];
+// ---------------------------------------------------------------- warp tail
+// Softmax over the K logits in feats[0..K) (model.py:149-152), features
+// (predictor.py:51-52) into feats[K..3K), validation (predictor.py:45-50).
+// Whole warp; returns false (and flags err) on invalid input.
+__device__ bool warp_softmax_features(const PredParams &p, int row, float *feats, int lane) {
+  const int K = p.K;
+  const bool v0 = lane < K, v1 = lane + 32 < K;
+  const float x0 = v0 ? feats[lane] : 0.f, x1 = v1 ? feats[lane + 32] : 0.f;
+  const float pv0 = v0 ? p.prev[(size_t)row * K + lane] : 0.f;
+  const float pv1 = v1 ? p.prev[(size_t)row * K + lane + 32] : 0.f;
+  bool bad = (v0 && !is_finite(x0)) || (v1 && !is_finite(x1));
+  bad = __any_sync(0xffffffffu, bad);
+  float m = v0 ? x0 : -INFINITY;
+  if (v1) m = fmaxf(m, x1);
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, s));
+  const float e0 = v0 ? np_expf(__fsub_rn(x0, m)) : 0.f;
+  const float e1 = v1 ? np_expf(__fsub_rn(x1, m)) : 0.f;
+  // strict left-to-right sums (seq_sum) over c = 0..K-1, replicated per lane
+  float esum = 0.f, psum = 0.f;
+  for (int c = 0; c < K; ++c) {
+    const float ec = __shfl_sync(0xffffffffu, c < 32 ? e0 : e1, c & 31);
+    const float pc = __shfl_sync(0xffffffffu, c < 32 ? pv0 : pv1, c & 31);
+    esum = __fadd_rn(esum, ec);
+    psum = __fadd_rn(psum, pc);
+  }
+  int e = 0;
+  if (bad) e |= ERR_LOGIT_NONFINITE;
+  if (fabs((double)psum - 1.0) > 1e-5) e |= ERR_PREV_SUM;
+  if (e) {
+    if (lane == 0) atomicOr(p.err, e);
+    return false;
+  }
+  if (v0) {
+    const float pr = __fdiv_rn(e0, esum);
+    feats[K + lane] = pr;
+    feats[2 * K + lane] = __fsub_rn(pr, pv0);
+  }
+  if (v1) {
+    const float pr = __fdiv_rn(e1, esum);
+    feats[K + lane + 32] = pr;
+    feats[2 * K + lane + 32] = __fsub_rn(pr, pv1);
+  }
+  __syncwarp();
+  return true;
+}
+
+// z1 of one unit j (scalar path; ragged H tails).
+__device__ __forceinline__ float z1_unit(const float *feats, const float *w1, int n, int H,
+                                         int j) {
+  float acc = 0.f;
+  if (n <= 48) {
+    for (int i = 0; i < n; ++i) acc = __fmaf_rn(feats[i], w1[(size_t)i * H + j], acc);
+    return acc;
+  }
+  int i = 0;
+  const int blocks[4] = {8, 4, 2, 1};
+  for (int bi = 0; bi < 4; ++bi) {
+    const int bs = blocks[bi];
+    while (n - i >= bs) {
+      float t = 0.f;
+      for (int q = 0; q < bs; ++q) t = __fmaf_rn(feats[i + q], w1[(size_t)(i + q) * H + j], t);
+      acc = __fadd_rn(acc, t);
+      i += bs;
+      if (bs != 8) break;
+    }
+  }
+  return acc;
+}
+
+// MLP of one row, whole warp.  w1/b1/w2 may point to shared or global
+// memory; hs: per-warp scratch of H floats.  Returns z2 in every lane.
+__device__ float warp_mlp(const float *feats, const float *w1, const float *b1, const float *w2,
+                          float b2, int K, int H, float *hs, int lane) {
+  const int n = 3 * K;
+  // z1 / ReLU for units j = 4*lane + 128*u + e  (16-byte, conflict-free reads)
+  const bool vec = (H % 4) == 0;
+  for (int j0 = 4 * lane; j0 < H; j0 += 128) {
+    if (vec) {
+      float y[4] = {0.f, 0.f, 0.f, 0.f};
+      if (n <= 48) {
+        for (int i = 0; i < n; ++i) {
+          const float f = feats[i];
+          const float4 w = *reinterpret_cast<const float4 *>(w1 + (size_t)i * H + j0);
+          y[0] = __fmaf_rn(f, w.x, y[0]); y[1] = __fmaf_rn(f, w.y, y[1]);
+          y[2] = __fmaf_rn(f, w.z, y[2]); y[3] = __fmaf_rn(f, w.w, y[3]);
+        }
+      } else {
+        int i = 0;
+        const int blocks[4] = {8, 4, 2, 1};
+        for (int bi = 0; bi < 4; ++bi) {
+          const int bs = blocks[bi];
+          while (n - i >= bs) {
+            float t[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int q = 0; q < bs; ++q) {
+              const float f = feats[i + q];
+              const float4 w = *reinterpret_cast<const float4 *>(w1 + (size_t)(i + q) * H + j0);
+              t[0] = __fmaf_rn(f, w.x, t[0]); t[1] = __fmaf_rn(f, w.y, t[1]);
+              t[2] = __fmaf_rn(f, w.z, t[2]); t[3] = __fmaf_rn(f, w.w, t[3]);
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) y[e] = __fadd_rn(y[e], t[e]);
+            i += bs;
+            if (bs != 8) break;
+          }
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float z1 = __fadd_rn(y[e], b1[j0 + e]);
+        hs[j0 + e] = z1 > 0.f ? z1 : 0.f;
+      }
+    } else {
+      for (int e = 0; e < 4 && j0 + e < H; ++e) {
+        const float z1 = __fadd_rn(z1_unit(feats, w1, n, H, j0 + e), b1[j0 + e]);
+        hs[j0 + e] = z1 > 0.f ? z1 : 0.f;
+      }
+    }
+  }
+  __syncwarp();
+  // z2: OpenBLAS SkylakeX sdot order (sdot.c + sdot_microk_skylakex-2.c):
+  // 4 x 16-lane FMA accumulators over 64-element blocks, fold 16->8, optional
+  // 32-element AVX2 step, lane-wise ((a0+a1)+a2)+a3, 8->4, ((q0+q1)+(q2+q3)),
+  // scalar tail, + b2.
+  const int n1 = H & ~31, n64 = n1 & ~63;
+  float alo = 0.f, ahi = 0.f;              // A[lane], A[lane + 32]
+  for (int b = 0; b < n64; b += 64) {
+    alo = __fmaf_rn(hs[b + lane], w2[b + lane], alo);
+    ahi = __fmaf_rn(hs[b + lane + 32], w2[b + lane + 32], ahi);
+  }
+  float blo = __fadd_rn(alo, __shfl_down_sync(0xffffffffu, alo, 8));
+  float bhi = __fadd_rn(ahi, __shfl_down_sync(0xffffffffu, ahi, 8));
+  const int m = lane & 15;
+  if (n1 > n64 && m < 8) {
+    const int a = lane >> 4;                 // 0 or 1 (lo), 2 or 3 (hi)
+    blo = __fmaf_rn(hs[n64 + 8 * a + m], w2[n64 + 8 * a + m], blo);
+    bhi = __fmaf_rn(hs[n64 + 8 * (a + 2) + m], w2[n64 + 8 * (a + 2) + m], bhi);
+  }
+  const float b1v = __shfl_down_sync(0xffffffffu, blo, 16);   // B_1[m] for lanes 0..7
+  const float b3v = __shfl_down_sync(0xffffffffu, bhi, 16);   // B_3[m]
+  const float s = __fadd_rn(__fadd_rn(__fadd_rn(blo, b1v), bhi), b3v);
+  const float q = __fadd_rn(s, __shfl_down_sync(0xffffffffu, s, 4));
+  const float q0 = __shfl_sync(0xffffffffu, q, 0), q1 = __shfl_sync(0xffffffffu, q, 1);
+  const float q2 = __shfl_sync(0xffffffffu, q, 2), q3 = __shfl_sync(0xffffffffu, q, 3);
+  float dot = n1 ? __fadd_rn(__fadd_rn(q0, q1), __fadd_rn(q2, q3)) : 0.f;
+  for (int i = n1; i < H; ++i) dot = __fadd_rn(dot, __fmul_rn(hs[i], w2[i]));
+  __syncwarp();
+  return __fadd_rn(dot, b2);
+}
+
+__device__ __forceinline__ double sigmoid64(float z2) {   // predictor.py:87-94
+  const double z = (double)z2;
+  if (z >= 0.0) return 1.0 / (1.0 + exp(-z));
+  const double ez = exp(z);
+  return ez / (1.0 + ez);
+}
+
+// Everything after the logits, for one row (whole warp).
+__device__ void warp_row_tail(const PredParams &p, int row, float *feats, const float *w1,
+                              const float *b1, const float *w2, float *hs, int lane) {
+  const int K = p.K;
+  const bool ok = warp_softmax_features(p, row, feats, lane);
+  if (p.logits_out) {
+    if (lane < K) p.logits_out[(size_t)row * K + lane] = feats[lane];
+    if (lane + 32 < K) p.logits_out[(size_t)row * K + lane + 32] = feats[lane + 32];
   }
   if (!ok) {
-    if (tid == 0 && p.fired) p.fired[row] = 0;
+    if (lane == 0 && p.fired) p.fired[row] = 0;
     return;
   }
   if (p.feat_out)
-    for (int i = tid; i < 3 * K; i += PRED_THREADS) p.feat_out[(size_t)row * 3 * K + i] = feats[i];
-  if (tid < K) p.prev[(size_t)row * K + tid] = feats[K + tid];   // engine.py:196
-  if (tid == 0 && p.evals) p.evals[row] += 1;
-  if (p.policy == 0) {
-    mlp_and_decide(p, row, feats, hs, as, true);
-  } else if (tid == 0) {
-    const bool fire = p.const_prob > p.threshold;
+    for (int i = lane; i < 3 * K; i += 32) p.feat_out[(size_t)row * 3 * K + i] = feats[i];
+  if (lane < K) p.prev[(size_t)row * K + lane] = feats[K + lane];            // engine.py:196
+  if (lane + 32 < K) p.prev[(size_t)row * K + lane + 32] = feats[K + lane + 32];
+  if (lane == 0 && p.evals) p.evals[row] += 1;
+  if (p.policy == SPX_POLICY_MLP) {
+    const float z2 = warp_mlp(feats, w1, b1, w2, p.b2, K, p.H, hs, lane);
+    if (lane == 0) {
+      if (p.z_out) p.z_out[row] = z2;
+      if (p.prob_out) p.prob_out[row] = sigmoid64(z2);
+      if (p.fired) p.fired[row] = (z2 >= p.z_cut) ? 1 : 0;
+    }
+  } else if (lane == 0) {
     if (p.prob_out) p.prob_out[row] = p.const_prob;
     if (p.z_out) p.z_out[row] = 0.0f;
-    if (p.fired) p.fired[row] = fire ? 1 : 0;
+    if (p.fired) p.fired[row] = (p.const_prob > p.threshold) ? 1 : 0;
   }
 }
 
-// ------------------------------------------------------------ FAST (CDOT)
-// CPT = canonical chunks per thread (d <= 1024*CPT).
-template <typename TW, int CPT>
-__global__ void __launch_bounds__(PRED_THREADS)
-predictor_fast_kernel(PredParams p) {
-  const int row = blockIdx.x;
-  if (row >= p.B) return;
-  if (row_skipped(p, row)) {
-    if (threadIdx.x == 0 && p.fired) p.fired[row] = 0;
-    return;
-  }
-  __shared__ float red[4 * 4];
-  __shared__ float feats[3 * MAXK];
-  __shared__ float hs[MAXH];
-  __shared__ float as[64];
-  __shared__ float scratch[MAXK];
-  __shared__ int s_flag;
-  const int tid = threadIdx.x;
-  const int nchunk = p.d / CHUNK;
-  const float *x = p.hidden + (size_t)row * p.hidden_stride;
-  if (tid == 0) s_flag = 0;
-  __syncthreads();
+// ------------------------------------------------------------ FAST (TMA)
+struct SmemPlan {
+  int nw;          // warps (= row stages) per CTA
+  int w1_smem;     // stage W1 in shared memory?
+  size_t bytes;
+  size_t off_g, off_b, off_w2, off_b1, off_w1, off_warp, warp_bytes, scratch_bytes, off_bar;
+};
 
-  // ---- load the hidden row and the norm params (canonical chunk ownership)
-  float xv[CPT][CHUNK];
-#pragma unroll
-  for (int s = 0; s < CPT; ++s) {
-    const int c = tid + NPART * s;
-    if (c < nchunk) {
-      const float4 a = ldg_f4(x + CHUNK * c), b = ldg_f4(x + CHUNK * c + 4);
-      xv[s][0] = a.x; xv[s][1] = a.y; xv[s][2] = a.z; xv[s][3] = a.w;
-      xv[s][4] = b.x; xv[s][5] = b.y; xv[s][6] = b.z; xv[s][7] = b.w;
-    } else {
-#pragma unroll
-      for (int e = 0; e < CHUNK; ++e) xv[s][e] = 0.0f;
+template <typename TW>
+inline SmemPlan plan_smem(int d, int K, int H, int max_bytes, int nw_cap) {
+  SmemPlan s{};
+  const size_t stage = (size_t)d * 4 + (size_t)GROUP * d * sizeof(TW);
+  const size_t scratch = ((size_t)(3 * MAXK + (H > 0 ? H : 1)) * 4 + 127) / 128 * 128;
+  const size_t per_warp = scratch + (stage + 127) / 128 * 128;
+  const size_t w1b = (size_t)3 * K * H * 4;
+  const size_t fixed0 = (((size_t)2 * d + 2 * H) * 4 + 127) / 128 * 128 + 256;
+  for (int w1 = (H > 0 ? 1 : 0); w1 >= 0; --w1) {
+    const size_t fixed = fixed0 + (w1 ? (w1b + 127) / 128 * 128 : 0);
+    int nw = 0;
+    for (int t = nw_cap; t >= 1; --t)
+      if (fixed + (size_t)t * per_warp + 64 <= (size_t)max_bytes) { nw = t; break; }
+    if (nw >= (w1 ? 3 : 1)) {
+      s.nw = nw; s.w1_smem = w1;
+      size_t o = 0;
+      s.off_g = o; o += (size_t)d * 4;
+      s.off_b = o; o += (size_t)d * 4;
+      s.off_w2 = o; o += (size_t)H * 4;
+      s.off_b1 = o; o += (size_t)H * 4;
+      o = (o + 127) / 128 * 128;
+      s.off_w1 = o; if (w1) o += (w1b + 127) / 128 * 128;
+      s.off_warp = o; s.warp_bytes = per_warp; s.scratch_bytes = scratch;
+      o += (size_t)nw * per_warp;
+      s.off_bar = o; o += (size_t)(nw + 1) * 8;
+      s.bytes = o;
+      return s;
     }
   }
-  // ---- LayerNorm stats (model.py:140-146) in canonical order
-  float part[1] = {0.0f};
-  bool finite = true;
-#pragma unroll
-  for (int s = 0; s < CPT; ++s)
-#pragma unroll
-    for (int e = 0; e < CHUNK; ++e) {
-      part[0] = __fadd_rn(part[0], xv[s][e]);
-      finite &= is_finite(xv[s][e]);
-    }
-  if (!finite) { atomicOr(p.err, ERR_HIDDEN_NONFINITE); s_flag = 1; }
-  cta_canon_reduce<1>(part, red);
-  const float df = (float)p.d;
-  const float mean = __fdiv_rn(part[0], df);
-  float sq[1] = {0.0f};
-#pragma unroll
-  for (int s = 0; s < CPT; ++s)
-#pragma unroll
-    for (int e = 0; e < CHUNK; ++e) {
-      const int c = tid + NPART * s;
-      if (c < nchunk) {
-        xv[s][e] = __fsub_rn(xv[s][e], mean);
-        sq[0] = __fmaf_rn(xv[s][e], xv[s][e], sq[0]);
-      }
-    }
-  cta_canon_reduce<1>(sq, red);
-  const float var = __fdiv_rn(sq[0], df);
-  const float denom = __fsqrt_rn(__fadd_rn(var, 1e-5f));
-#pragma unroll
-  for (int s = 0; s < CPT; ++s) {
-    const int c = tid + NPART * s;
-    if (c < nchunk) {
-      const float4 g0 = ldg_f4(p.norm_g + CHUNK * c), g1 = ldg_f4(p.norm_g + CHUNK * c + 4);
-      const float4 b0 = ldg_f4(p.norm_b + CHUNK * c), b1 = ldg_f4(p.norm_b + CHUNK * c + 4);
-      const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-      const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-      for (int e = 0; e < CHUNK; ++e)
-        xv[s][e] = __fadd_rn(__fmul_rn(__fdiv_rn(xv[s][e], denom), gg[e]), bb[e]);
-    }
-  }
-  // ---- K speculative logits, 4 ids per pass
-  const int K = p.K;
-  for (int c0 = 0; c0 < K; c0 += 4) {
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    Chunk<TW> wv[4][CPT];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      int id = (c0 + q < K) ? p.ids[(size_t)row * K + c0 + q] : 0;
-      if (id < 0 || id >= p.V) {
-        if (tid == 0) atomicOr(p.err, ERR_ID_RANGE);
-        s_flag = 1;
-        id = 0;
-      }
-      const TW *wr = reinterpret_cast<const TW *>(p.head) + (size_t)id * p.d;
-#pragma unroll
-      for (int s = 0; s < CPT; ++s) {
-        const int c = tid + NPART * s;
-        if (c0 + q < K && c < nchunk) wv[q][s].load(wr + CHUNK * c);
-        else wv[q][s].zero();
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int s = 0; s < CPT; ++s) {
-        float w[8];
-        wv[q][s].to_f32(w);
-#pragma unroll
-        for (int e = 0; e < CHUNK; ++e) acc[q] = __fmaf_rn(xv[s][e], w[e], acc[q]);
-      }
-    cta_canon_reduce<4>(acc, red);
-    if (tid < 4 && c0 + tid < K) feats[c0 + tid] = acc[tid];
-  }
+  return s;   // nw == 0: does not fit
+}
+
+template <typename TW>
+__global__ void __launch_bounds__(32 * MAXW)
+predictor_tma_kernel(PredParams p, SmemPlan sp) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = sp.nw;
+  const int d = p.d, K = p.K, H = p.H, nchunk = d / CHUNK;
+  float *gs = reinterpret_cast<float *>(smem + sp.off_g);
+  float *bs = reinterpret_cast<float *>(smem + sp.off_b);
+  float *w2s = reinterpret_cast<float *>(smem + sp.off_w2);
+  float *b1s = reinterpret_cast<float *>(smem + sp.off_b1);
+  float *w1s = reinterpret_cast<float *>(smem + sp.off_w1);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + sp.off_bar) + warp;
+  uint8_t *wbase = smem + sp.off_warp + (size_t)warp * sp.warp_bytes;
+  float *feats = reinterpret_cast<float *>(wbase);
+  float *hs = feats + 3 * MAXK;
+  float *sh = reinterpret_cast<float *>(wbase + sp.scratch_bytes);
+  TW *sw = reinterpret_cast<TW *>(wbase + sp.scratch_bytes + (size_t)d * 4);
+
+  uint64_t *setup_bar = reinterpret_cast<uint64_t *>(smem + sp.off_bar) + nw;
+  const bool mlp = p.policy == SPX_POLICY_MLP;
+  const bool bulk_consts = (H % 4) == 0;
+  if (lane == 0) mbar_init(bar, 1);
+  if (threadIdx.x == 0) mbar_init(setup_bar, 1);
+  fence_mbar_init();
   __syncthreads();
-  if (s_flag) {
-    if (tid == 0 && p.fired) p.fired[row] = 0;
-    return;
+  // ---- per-CTA constants -> shared memory (TMA bulk; plain loads if ragged)
+  if (threadIdx.x == 0) {
+    uint32_t bytes = 2u * d * 4u;
+    if (mlp && bulk_consts) bytes += 2u * H * 4u + (sp.w1_smem ? 3u * K * H * 4u : 0u);
+    mbar_arrive_expect_tx(setup_bar, bytes);
+    bulk_g2s(gs, p.norm_g, (uint32_t)d * 4u, setup_bar);
+    bulk_g2s(bs, p.norm_b, (uint32_t)d * 4u, setup_bar);
+    if (mlp && bulk_consts) {
+      bulk_g2s(w2s, p.w2, (uint32_t)H * 4u, setup_bar);
+      bulk_g2s(b1s, p.b1, (uint32_t)H * 4u, setup_bar);
+      if (sp.w1_smem) bulk_g2s(w1s, p.w1, 3u * K * H * 4u, setup_bar);
+    }
   }
-  finish_row(p, row, feats, hs, as, scratch);
+  if (mlp && !bulk_consts) {
+    for (int i = threadIdx.x; i < H; i += blockDim.x) { w2s[i] = p.w2[i]; b1s[i] = p.b1[i]; }
+    if (sp.w1_smem)
+      for (int i = threadIdx.x; i < 3 * K * H; i += blockDim.x) w1s[i] = p.w1[i];
+  }
+  const float *w1 = sp.w1_smem ? w1s : p.w1;
+
+  const int stride = gridDim.x * nw;
+  const uint32_t wrow_bytes = (uint32_t)((size_t)d * sizeof(TW));
+  uint32_t phase = 0;
+  int id_bad = 0;
+
+  // lane 0 issues the TMA copies of the W rows of ids [c0, c0+ng) of `row`
+  auto issue_group = [&](int row, int c0, int ng, bool with_hidden) {
+    fence_proxy_async();
+    mbar_arrive_expect_tx(bar, (with_hidden ? (uint32_t)d * 4u : 0u) + (uint32_t)ng * wrow_bytes);
+    if (with_hidden)
+      bulk_g2s(sh, p.hidden + (size_t)row * p.hidden_stride, (uint32_t)d * 4u, bar);
+    for (int q = 0; q < ng; ++q) {
+      int id = p.ids[(size_t)row * K + c0 + q];
+      if (id < 0 || id >= p.V) { id_bad = 1; id = 0; }
+      bulk_g2s(sw + (size_t)q * d, reinterpret_cast<const TW *>(p.head) + (size_t)id * d,
+               wrow_bytes, bar);
+    }
+  };
+  // issue (hidden row + first id group) for `row`; returns 1 if skipped.
+  auto issue = [&](int row) -> int {
+    int skip = 1;
+    if (lane == 0 && row < p.B) {
+      skip = row_skipped(p, row) ? 1 : 0;
+      if (!skip) issue_group(row, 0, K < GROUP ? K : GROUP, true);
+    }
+    return __shfl_sync(0xffffffffu, skip, 0);
+  };
+
+  int row = blockIdx.x * nw + warp;
+  int skip = issue(row);                // first row's copies overlap the setup copies
+  mbar_wait(setup_bar, 0);
+  if (mlp && !bulk_consts) __syncthreads();
+  while (row < p.B) {
+    const int next = row + stride;
+    if (skip) {
+      if (lane == 0 && p.fired) p.fired[row] = 0;
+      row = next;
+      skip = issue(row);
+      continue;
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    float mean, denom;
+    bool bad;
+    warp_ln_stats(sh, d, lane, mean, denom, bad);
+    const float rinv = __frcp_rn(denom);
+    for (int c0 = 0; c0 < K; c0 += GROUP) {
+      const int ng = (K - c0) < GROUP ? (K - c0) : GROUP;
+      if (c0 > 0) {                       // next id group into the W stage
+        __syncwarp();
+        if (lane == 0) issue_group(row, c0, ng, false);
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+      }
+      float acc[GROUP][4];
+#pragma unroll
+      for (int q = 0; q < GROUP; ++q)
+#pragma unroll
+        for (int g = 0; g < 4; ++g) acc[q][g] = 0.f;
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        for (int c = 32 * g + lane; c < nchunk; c += NPART) {
+          const float4 xv = *reinterpret_cast<const float4 *>(sh + CHUNK * c);
+          const float4 gv = *reinterpret_cast<const float4 *>(gs + CHUNK * c);
+          const float4 bv = *reinterpret_cast<const float4 *>(bs + CHUNK * c);
+          const float hn[4] = {
+              __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv.x, mean), rinv), gv.x), bv.x),
+              __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv.y, mean), rinv), gv.y), bv.y),
+              __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv.z, mean), rinv), gv.z), bv.z),
+              __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv.w, mean), rinv), gv.w), bv.w)};
+#pragma unroll
+          for (int q = 0; q < GROUP; ++q) {
+            if (q < ng) {
+              Chunk<TW> ch;
+              ch.lds(sw + (size_t)q * d + CHUNK * c);
+              float w[4];
+              ch.to_f32(w);
+#pragma unroll
+              for (int e = 0; e < CHUNK; ++e) acc[q][g] = __fmaf_rn(hn[e], w[e], acc[q][g]);
+            }
+          }
+        }
+#pragma unroll
+      for (int q = 0; q < GROUP; ++q) {
+        if (q < ng) {
+          float gsum[4];
+#pragma unroll
+          for (int g = 0; g < 4; ++g) gsum[g] = warp_butterfly_sum(acc[q][g]);
+          if (lane == 0) feats[c0 + q] = canon_combine(gsum[0], gsum[1], gsum[2], gsum[3]);
+        }
+      }
+    }
+    __syncwarp();
+    const int ibad = __shfl_sync(0xffffffffu, id_bad, 0);
+    id_bad = 0;
+    // the stage is free: prefetch the next row while this row's tail runs
+    const int nskip = issue(next);
+    if (ibad || bad) {
+      if (lane == 0) {
+        atomicOr(p.err, (ibad ? ERR_ID_RANGE : 0) | (bad ? ERR_HIDDEN_NONFINITE : 0));
+        if (p.fired) p.fired[row] = 0;
+      }
+    } else {
+      warp_row_tail(p, row, feats, w1, b1s, w2s, hs, lane);
+    }
+    row = next;
+    skip = nskip;
+  }
 }
 
 // ----------------------------------------------------------- STRICT (parity)
 // The reference's own operation sequence: every sum a left-to-right chain of
-// separately rounded adds from 0, every product rounded (no FMA).  Uses
-// dynamic smem of d floats.
+// separately rounded adds from 0, every product rounded (no FMA).  One CTA
+// per row; the softmax/MLP tail is the same warp code as the FAST kernel.
+constexpr int STRICT_THREADS = 128;
+
 template <typename TW>
-__global__ void __launch_bounds__(PRED_THREADS)
+__global__ void __launch_bounds__(STRICT_THREADS)
 predictor_strict_kernel(PredParams p) {
   const int row = blockIdx.x;
   if (row >= p.B) return;
@@ -355,8 +471,6 @@ predictor_strict_kernel(PredParams p) {
   extern __shared__ float hn[];   // d floats
   __shared__ float feats[3 * MAXK];
   __shared__ float hs[MAXH];
-  __shared__ float as[64];
-  __shared__ float scratch[MAXK];
   __shared__ float s_mean, s_denom;
   __shared__ int s_flag;
   const int tid = threadIdx.x, d = p.d;
@@ -364,7 +478,7 @@ predictor_strict_kernel(PredParams p) {
   if (tid == 0) s_flag = 0;
   __syncthreads();
   bool finite = true;
-  for (int j = tid; j < d; j += PRED_THREADS) { hn[j] = x[j]; finite &= is_finite(hn[j]); }
+  for (int j = tid; j < d; j += STRICT_THREADS) { hn[j] = x[j]; finite &= is_finite(hn[j]); }
   if (!finite) { atomicOr(p.err, ERR_HIDDEN_NONFINITE); s_flag = 1; }
   __syncthreads();
   const float df = (float)d;
@@ -375,7 +489,7 @@ predictor_strict_kernel(PredParams p) {
   }
   __syncthreads();
   const float mean = s_mean;
-  for (int j = tid; j < d; j += PRED_THREADS) hn[j] = __fsub_rn(hn[j], mean);
+  for (int j = tid; j < d; j += STRICT_THREADS) hn[j] = __fsub_rn(hn[j], mean);
   __syncthreads();
   if (tid == 0) {
     float acc = 0.0f;
@@ -384,8 +498,7 @@ predictor_strict_kernel(PredParams p) {
   }
   __syncthreads();
   const float denom = s_denom;
-  for (int j = tid; j < d; j += PRED_THREADS)
-    hn[j] = __fadd_rn(__fmul_rn(__fdiv_rn(hn[j], denom), p.norm_g[j]), p.norm_b[j]);
+  for (int j = tid; j < d; j += STRICT_THREADS) hn[j] = ln_elem(hn[j], denom, p.norm_g[j], p.norm_b[j]);
   __syncthreads();
   const int K = p.K;
   if (tid < K) {
@@ -394,41 +507,94 @@ predictor_strict_kernel(PredParams p) {
     const TW *wr = reinterpret_cast<const TW *>(p.head) + (size_t)id * d;
     float acc = 0.0f;
     for (int j = 0; j < d; j += CHUNK) {
-      float w[8];
-      load8_f32<TW>(wr + j, w);
+      float w[4];
+      load4_f32<TW>(wr + j, w);
 #pragma unroll
       for (int e = 0; e < CHUNK; ++e) acc = __fadd_rn(acc, __fmul_rn(hn[j + e], w[e]));
     }
     feats[tid] = acc;
   }
   __syncthreads();
+  if (tid >= 32) return;
   if (s_flag) {
     if (tid == 0 && p.fired) p.fired[row] = 0;
     return;
   }
-  finish_row(p, row, feats, hs, as, scratch);
+  warp_row_tail(p, row, feats, p.w1, p.b1, p.w2, hs, tid);
+}
+
+// ---------------------------------------------------------------------------
+// Function-level operators (the reference's extract_features and
+// predictor_forward called on their own, predictor.py:42-52 / :97-103).  They
+// run the same warp code as the fused kernel, so results are identical.
+
+__global__ void features_kernel(const float *logits, float *prev, float *feats_out, int *err,
+                                int B, int K) {
+  const int row = blockIdx.x;
+  if (row >= B) return;
+  __shared__ float feats[3 * MAXK];
+  PredParams p{};
+  p.prev = prev; p.err = err; p.K = K;
+  for (int i = threadIdx.x; i < K; i += 32) feats[i] = logits[(size_t)row * K + i];
+  __syncwarp();
+  if (!warp_softmax_features(p, row, feats, threadIdx.x)) return;
+  for (int i = threadIdx.x; i < 3 * K; i += 32) feats_out[(size_t)row * 3 * K + i] = feats[i];
+}
+
+__global__ void mlp_kernel(PredParams p, const float *feats_in) {
+  const int row = blockIdx.x;
+  if (row >= p.B) return;
+  __shared__ float feats[3 * MAXK];
+  __shared__ float hs[MAXH];
+  const int lane = threadIdx.x;
+  for (int i = lane; i < 3 * p.K; i += 32) feats[i] = feats_in[(size_t)row * 3 * p.K + i];
+  __syncwarp();
+  const float z2 = warp_mlp(feats, p.w1, p.b1, p.w2, p.b2, p.K, p.H, hs, lane);
+  if (lane == 0) {
+    if (p.z_out) p.z_out[row] = z2;
+    if (p.prob_out) p.prob_out[row] = sigmoid64(z2);
+    if (p.fired) p.fired[row] = (z2 >= p.z_cut) ? 1 : 0;
+  }
 }
 
 }  // namespace spx
 
 using namespace spx;
 
+static int g_sms = 0, g_smem_optin = 0;
+static void device_limits() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (g_sms <= 0) g_sms = 148;
+    if (g_smem_optin <= 0) g_smem_optin = 227 * 1024;
+  }
+}
+
 template <typename TW>
-static int launch_predictor(const PredParams &p, const spx_predictor_args *a, dim3 grid,
-                            dim3 block, cudaStream_t stream) {
+static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cudaStream_t stream) {
+  device_limits();
   if (a->mode == SPX_MODE_STRICT) {
     const size_t smem = (size_t)a->d * sizeof(float);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(predictor_strict_kernel<TW>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    predictor_strict_kernel<TW><<<grid, block, smem, stream>>>(p);
+    predictor_strict_kernel<TW><<<(unsigned)a->B, STRICT_THREADS, smem, stream>>>(p);
   } else {
-    const int nchunk = (int)(a->d / CHUNK);
-    if (nchunk <= NPART * 1) predictor_fast_kernel<TW, 1><<<grid, block, 0, stream>>>(p);
-    else if (nchunk <= NPART * 2) predictor_fast_kernel<TW, 2><<<grid, block, 0, stream>>>(p);
-    else if (nchunk <= NPART * 4) predictor_fast_kernel<TW, 4><<<grid, block, 0, stream>>>(p);
-    else if (nchunk <= NPART * 8) predictor_fast_kernel<TW, 8><<<grid, block, 0, stream>>>(p);
-    else return SPX_EINVAL;
+    if (((size_t)p.d * sizeof(TW)) % 16) return SPX_EINVAL;   // TMA bulk: 16-byte rows
+    SmemPlan sp = plan_smem<TW>(p.d, p.K, p.H, g_smem_optin, MAXW);
+    if (sp.nw == 0) return SPX_EINVAL;
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(predictor_tma_kernel<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           g_smem_optin);
+      configured = true;
+    }
+    const long long need = (a->B + sp.nw - 1) / sp.nw;
+    const int grid = (int)(need < g_sms ? need : g_sms);
+    predictor_tma_kernel<TW><<<grid > 0 ? grid : 1, 32 * sp.nw, sp.bytes, stream>>>(p, sp);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
 }
@@ -442,6 +608,7 @@ extern "C" int spx_predictor_eval(const spx_predictor_args *a, void *stream_) {
   if (!a->hidden || !a->norm_g || !a->norm_b || !a->head || !a->ids || !a->prev || !a->err)
     return SPX_EINVAL;
   if (a->policy == SPX_POLICY_MLP && (!a->w1 || !a->b1 || !a->w2)) return SPX_EINVAL;
+  if (a->hidden_stride % CHUNK) return SPX_EINVAL;
   if (a->B == 0) return 0;
   PredParams p;
   p.hidden = a->hidden; p.hidden_stride = a->hidden_stride ? a->hidden_stride : a->d;
@@ -454,54 +621,18 @@ extern "C" int spx_predictor_eval(const spx_predictor_args *a, void *stream_) {
   p.prob_out = a->prob_out; p.fired = a->fired;
   p.row_layer_mask = a->row_layer_mask; p.row_done = a->row_done; p.evals = a->evals;
   p.layer = a->layer; p.err = a->err;
-  p.B = (int)a->B; p.d = (int)a->d; p.V = (int)a->V; p.K = (int)a->K; p.H = (int)a->H;
-  const dim3 grid((unsigned)a->B), block(PRED_THREADS);
-  if (a->head_dtype == SPX_DTYPE_F32) return launch_predictor<float>(p, a, grid, block, stream);
-  if (a->head_dtype == SPX_DTYPE_BF16)
-    return launch_predictor<__nv_bfloat16>(p, a, grid, block, stream);
+  p.B = (int)a->B; p.d = (int)a->d; p.V = (int)a->V; p.K = (int)a->K;
+  p.H = a->policy == SPX_POLICY_MLP ? (int)a->H : 0;
+  if (a->head_dtype == SPX_DTYPE_F32) return launch_predictor<float>(p, a, stream);
+  if (a->head_dtype == SPX_DTYPE_BF16) return launch_predictor<__nv_bfloat16>(p, a, stream);
   return SPX_EINVAL;
 }
-
-// ---------------------------------------------------------------------------
-// Function-level operators (the reference's extract_features and
-// predictor_forward called on their own, predictor.py:42-52 / :97-103).  They
-// run the same device code as the fused kernel, so results are identical.
-
-namespace spx {
-
-__global__ void __launch_bounds__(PRED_THREADS)
-features_kernel(const float *logits, float *prev, float *feats_out, int *err, int B, int K) {
-  const int row = blockIdx.x;
-  if (row >= B) return;
-  __shared__ float feats[3 * MAXK];
-  __shared__ float scratch[MAXK];
-  PredParams p{};
-  p.prev = prev; p.err = err; p.K = K;
-  if (threadIdx.x < K) feats[threadIdx.x] = logits[(size_t)row * K + threadIdx.x];
-  __syncthreads();
-  if (!softmax_features(p, row, feats, scratch)) return;
-  for (int i = threadIdx.x; i < 3 * K; i += PRED_THREADS) feats_out[(size_t)row * 3 * K + i] = feats[i];
-}
-
-__global__ void __launch_bounds__(PRED_THREADS)
-mlp_kernel(PredParams p, const float *feats_in) {
-  const int row = blockIdx.x;
-  if (row >= p.B) return;
-  __shared__ float feats[3 * MAXK];
-  __shared__ float hs[MAXH];
-  __shared__ float as[64];
-  for (int i = threadIdx.x; i < 3 * p.K; i += PRED_THREADS) feats[i] = feats_in[(size_t)row * 3 * p.K + i];
-  __syncthreads();
-  mlp_and_decide(p, row, feats, hs, as, true);
-}
-
-}  // namespace spx
 
 extern "C" int spx_extract_features(const float *logits, const float *prev, float *feats_out,
                                     int32_t *err, int64_t B, int64_t K, void *stream) {
   if (!logits || !prev || !feats_out || !err || B < 0 || K < 1 || K > MAXK) return SPX_EINVAL;
   if (B == 0) return 0;
-  features_kernel<<<(unsigned)B, PRED_THREADS, 0, (cudaStream_t)stream>>>(
+  features_kernel<<<(unsigned)B, 32, 0, (cudaStream_t)stream>>>(
       logits, const_cast<float *>(prev), feats_out, err, (int)B, (int)K);
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
 }
@@ -517,6 +648,6 @@ extern "C" int spx_predictor_mlp(const float *feats, const float *w1, const floa
   p.w1 = w1; p.b1 = b1; p.w2 = w2; p.b2 = b2; p.z_cut = z_cut;
   p.z_out = z_out; p.prob_out = prob_out; p.fired = fired_out;
   p.B = (int)B; p.K = (int)K; p.H = (int)H;
-  mlp_kernel<<<(unsigned)B, PRED_THREADS, 0, (cudaStream_t)stream>>>(p, feats);
+  mlp_kernel<<<(unsigned)B, 32, 0, (cudaStream_t)stream>>>(p, feats);
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
 }

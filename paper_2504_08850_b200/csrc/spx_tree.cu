@@ -52,12 +52,12 @@ tree_merged_kernel(const float *hn, int N, const TW *head, int V, int d,
         const int c = 32 * g + lane + NPART * s;
         if (c < nchunk) {
           const float4 h0 = __ldg(reinterpret_cast<const float4 *>(h + CHUNK * c));
-          const float4 h1 = __ldg(reinterpret_cast<const float4 *>(h + CHUNK * c + 4));
-          const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-          float wf[8];
+          float wf[4];
           w[g][s].to_f32(wf);
-#pragma unroll
-          for (int e = 0; e < CHUNK; ++e) acc[g] = __fmaf_rn(hv[e], wf[e], acc[g]);
+          acc[g] = __fmaf_rn(h0.x, wf[0], acc[g]);
+          acc[g] = __fmaf_rn(h0.y, wf[1], acc[g]);
+          acc[g] = __fmaf_rn(h0.z, wf[2], acc[g]);
+          acc[g] = __fmaf_rn(h0.w, wf[3], acc[g]);
         }
       }
     float gs[4];

@@ -41,44 +41,24 @@ __device__ __forceinline__ bool ver_row_on(const VerParams &p, int r) {
   return true;
 }
 
-// Canonical LayerNorm of one row into smem `hn` by one warp (FAST) or one
-// thread (STRICT).  Identical bits to predictor_fast_kernel's LN.
+// Canonical LayerNorm of one row into smem `hn` by one warp (FAST: the CDOT
+// statistics + reciprocal scaling, identical bits to the predictor kernel) or
+// one thread (STRICT: the reference's sequential sums and division).
 __device__ void warp_layernorm(const VerParams &p, int r, float *hn, int lane, bool strict,
                                int *bad) {
   const float *x = p.hidden + (size_t)r * p.hidden_stride;
-  const int d = p.d, nchunk = d / CHUNK;
+  const int d = p.d;
   const float df = (float)d;
   for (int j = lane; j < d; j += 32) hn[j] = x[j];
   __syncwarp();
-  float mean, denom;
   if (!strict) {
-    float part[4] = {0.f, 0.f, 0.f, 0.f};
-    bool fin = true;
-#pragma unroll
-    for (int g = 0; g < 4; ++g)
-      for (int c = 32 * g + lane; c < nchunk; c += NPART)
-#pragma unroll
-        for (int e = 0; e < CHUNK; ++e) {
-          part[g] = __fadd_rn(part[g], hn[CHUNK * c + e]);
-          fin &= is_finite(hn[CHUNK * c + e]);
-        }
-    if (!fin) *bad = 1;
-#pragma unroll
-    for (int g = 0; g < 4; ++g) part[g] = warp_butterfly_sum(part[g]);
-    mean = __fdiv_rn(canon_combine(part[0], part[1], part[2], part[3]), df);
-    float sq[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int g = 0; g < 4; ++g)
-      for (int c = 32 * g + lane; c < nchunk; c += NPART)
-#pragma unroll
-        for (int e = 0; e < CHUNK; ++e) {
-          const float xc = __fsub_rn(hn[CHUNK * c + e], mean);
-          sq[g] = __fmaf_rn(xc, xc, sq[g]);
-        }
-#pragma unroll
-    for (int g = 0; g < 4; ++g) sq[g] = warp_butterfly_sum(sq[g]);
-    const float var = __fdiv_rn(canon_combine(sq[0], sq[1], sq[2], sq[3]), df);
-    denom = __fsqrt_rn(__fadd_rn(var, 1e-5f));
+    float mean, denom;
+    bool b;
+    warp_ln_stats(hn, d, lane, mean, denom, b);
+    if (b) *bad = 1;
+    const float rinv = __frcp_rn(denom);
+    for (int j = lane; j < d; j += 32)
+      hn[j] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(hn[j], mean), rinv), p.g[j]), p.b[j]);
   } else {
     float m = 0.f, v = 0.f;
     bool fin = true;
@@ -92,16 +72,15 @@ __device__ void warp_layernorm(const VerParams &p, int r, float *hn, int lane, b
       v = __fsqrt_rn(__fadd_rn(__fdiv_rn(v, df), 1e-5f));
       if (!fin) *bad = 1;
     }
-    mean = __shfl_sync(0xffffffffu, m, 0);
-    denom = __shfl_sync(0xffffffffu, v, 0);
+    const float mean = __shfl_sync(0xffffffffu, m, 0);
+    const float denom = __shfl_sync(0xffffffffu, v, 0);
+    __syncwarp();
+    for (int j = lane; j < d; j += 32) hn[j] = ln_elem(__fsub_rn(hn[j], mean), denom, p.g[j], p.b[j]);
   }
-  __syncwarp();
-  for (int j = lane; j < d; j += 32)
-    hn[j] = __fadd_rn(__fmul_rn(__fdiv_rn(__fsub_rn(hn[j], mean), denom), p.g[j]), p.b[j]);
   __syncwarp();
 }
 
-// Canonical dot of one bf16 vocab row with R normed rows; warp-cooperative.
+// Canonical dot of one vocab row with R normed rows (smem); warp-cooperative.
 template <typename TW, int R, int CPL>
 __device__ __forceinline__ void warp_cdot(const TW *wrow, const float *hn, int d,
                                           int nr, int lane, float *out) {
@@ -127,16 +106,16 @@ __device__ __forceinline__ void warp_cdot(const TW *wrow, const float *hn, int d
     for (int s = 0; s < CPL; ++s) {
       const int c = 32 * g + lane + NPART * s;
       if (c < nchunk) {
-        float wf[8];
+        float wf[4];
         w[g][s].to_f32(wf);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (r < nr) {
-            const float4 h0 = *reinterpret_cast<const float4 *>(hn + (size_t)r * d + CHUNK * c);
-            const float4 h1 = *reinterpret_cast<const float4 *>(hn + (size_t)r * d + CHUNK * c + 4);
-            const float hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-#pragma unroll
-            for (int e = 0; e < CHUNK; ++e) acc[r][g] = __fmaf_rn(hv[e], wf[e], acc[r][g]);
+            const float4 h = *reinterpret_cast<const float4 *>(hn + (size_t)r * d + CHUNK * c);
+            acc[r][g] = __fmaf_rn(h.x, wf[0], acc[r][g]);
+            acc[r][g] = __fmaf_rn(h.y, wf[1], acc[r][g]);
+            acc[r][g] = __fmaf_rn(h.z, wf[2], acc[r][g]);
+            acc[r][g] = __fmaf_rn(h.w, wf[3], acc[r][g]);
           }
         }
       }
@@ -208,8 +187,8 @@ verify_kernel(VerParams p) {
         const TW *wr = head + (size_t)v * p.d;
         float acc[VER_ROWS] = {0.f, 0.f, 0.f, 0.f};
         for (int j = 0; j < p.d; j += CHUNK) {
-          float wf[8];
-          load8_f32<TW>(wr + j, wf);
+          float wf[4];
+          load4_f32<TW>(wr + j, wf);
 #pragma unroll
           for (int r = 0; r < VER_ROWS; ++r)
             if (r < nr)

@@ -114,7 +114,7 @@ class TransformerModel:
         self.final_b = torch.zeros(d, dtype=torch.float32, device=dev)
         self.layers = []
         if not head_only:
-            self.embedding = torch.empty((v, d), dtype=torch.float32, device=dev)
+            self.embedding = torch.empty((v, d), dtype=td, device=dev)
             self.pos_encoding = torch.as_tensor(sinusoidal_encoding(config.max_context, d),
                                                 device=dev)
             for _ in range(L):

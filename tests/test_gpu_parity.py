@@ -54,7 +54,7 @@ def test_device_init_matches_reference_init(golden, oracle, name):
     m = tiny_device_model()
     t = oracle.init_model(oracle.ModelConfig(num_layers=4, seed=3), bf16=True)
     assert np.array_equal(m.lm_head.float().cpu().numpy(), t["lm_head"].T)
-    assert np.array_equal(m.embedding.cpu().numpy(), t["embedding"])
+    assert np.array_equal(m.embedding.float().cpu().numpy(), t["embedding"])
     wq = m.layers[2]["wqkv"][:64].float().cpu().numpy()
     assert np.array_equal(wq, t["layers.2.attn.wq"].T)
     assert np.array_equal(m.layers[3]["ffn_w2"].float().cpu().numpy(), t["layers.3.ffn.w2"].T)
