@@ -153,13 +153,14 @@ int spx_sched_active(spx_online_state st, uint64_t offline_mask, int64_t B, int3
 
 /* K6 -- context-aware merged mapping (src/specexit/tree.py:92-113): logits of
  * node n for ids[ptr[n]..ptr[n+1]) with each UNIQUE id's LM-head row read
- * once.  uniq (U) are the distinct ids, pair_uid / pair_node / pair_out (P)
+ * once.  uniq (U) are the distinct ids (grouped: pairs of unique id u are
+ * uniq_ptr[u]..uniq_ptr[u+1]), pair_uid / pair_node / pair_out (P)
  * map every (node, id) pair to its unique row; hn (N, d) are the final-normed
  * node rows (spx_final_norm).  Bit-identical to K1's logits (FAST order). */
 int spx_tree_merged_logits(const float *hn, int64_t N, const void *head, int32_t head_dtype,
                            int64_t V, int64_t d, const int32_t *uniq, int64_t U, const int32_t *uniq_ptr,
                            const int32_t *pair_node, const int32_t *pair_out, float *logits,
-                           int32_t *err, void *stream);
+                           int32_t mode, int32_t *err, void *stream);
 /* final LayerNorm of N rows into hn (model.py:140-146), FAST or STRICT. */
 int spx_final_norm(const float *hidden, int64_t hidden_stride, const float *g, const float *b,
                    float *hn, int64_t N, int64_t d, int32_t mode, int32_t *err, void *stream);

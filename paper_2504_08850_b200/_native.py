@@ -72,7 +72,7 @@ def lib():
     L.spx_sched_update.argtypes = [OnlineStateC, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]
     L.spx_sched_active.argtypes = [OnlineStateC, ctypes.c_uint64, _i64, _i32, _i32, _vp, _vp]
     L.spx_tree_merged_logits.argtypes = [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _i64, _vp, _vp,
-                                         _vp, _vp, _vp, _vp]
+                                         _vp, _vp, _i32, _vp, _vp]
     L.spx_final_norm.argtypes = [_vp, _i64, _vp, _vp, _vp, _i64, _i64, _i32, _vp, _vp]
     L.spx_path_and.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _vp]
     L.spx_init_uniform.argtypes = [_vp, _i32, _i64, _i64, _i32, ctypes.c_uint64, _f64, _f64, _vp]

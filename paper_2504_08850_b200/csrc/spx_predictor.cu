@@ -144,17 +144,28 @@ __device__ __forceinline__ float z1_unit(const float *feats, const float *w1, in
 __device__ float warp_mlp(const float *feats, const float *w1, const float *b1, const float *w2,
                           float b2, int K, int H, float *hs, int lane) {
   const int n = 3 * K;
-  // z1 / ReLU for units j = 4*lane + 128*u + e  (16-byte, conflict-free reads)
-  const bool vec = (H % 4) == 0;
-  for (int j0 = 4 * lane; j0 < H; j0 += 128) {
-    if (vec) {
-      float y[4] = {0.f, 0.f, 0.f, 0.f};
+  // z1 / ReLU.  Lane owns units j = jb + 4*lane + 128*u + e (u, e < 4): 16
+  // independent FMA chains per lane, 16-byte conflict-free W1 reads.
+  if ((H % 4) == 0) {
+    for (int jb = 0; jb < H; jb += 512) {
+      float y[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) y[u][e] = 0.f;
       if (n <= 48) {
+#pragma unroll 4
         for (int i = 0; i < n; ++i) {
           const float f = feats[i];
-          const float4 w = *reinterpret_cast<const float4 *>(w1 + (size_t)i * H + j0);
-          y[0] = __fmaf_rn(f, w.x, y[0]); y[1] = __fmaf_rn(f, w.y, y[1]);
-          y[2] = __fmaf_rn(f, w.z, y[2]); y[3] = __fmaf_rn(f, w.w, y[3]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j0 = jb + 4 * lane + 128 * u;
+            if (j0 < H) {
+              const float4 w = *reinterpret_cast<const float4 *>(w1 + (size_t)i * H + j0);
+              y[u][0] = __fmaf_rn(f, w.x, y[u][0]); y[u][1] = __fmaf_rn(f, w.y, y[u][1]);
+              y[u][2] = __fmaf_rn(f, w.z, y[u][2]); y[u][3] = __fmaf_rn(f, w.w, y[u][3]);
+            }
+          }
         }
       } else {
         int i = 0;
@@ -162,30 +173,48 @@ __device__ float warp_mlp(const float *feats, const float *w1, const float *b1, 
         for (int bi = 0; bi < 4; ++bi) {
           const int bs = blocks[bi];
           while (n - i >= bs) {
-            float t[4] = {0.f, 0.f, 0.f, 0.f};
+            float t[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) t[u][e] = 0.f;
             for (int q = 0; q < bs; ++q) {
               const float f = feats[i + q];
-              const float4 w = *reinterpret_cast<const float4 *>(w1 + (size_t)(i + q) * H + j0);
-              t[0] = __fmaf_rn(f, w.x, t[0]); t[1] = __fmaf_rn(f, w.y, t[1]);
-              t[2] = __fmaf_rn(f, w.z, t[2]); t[3] = __fmaf_rn(f, w.w, t[3]);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int j0 = jb + 4 * lane + 128 * u;
+                if (j0 < H) {
+                  const float4 w = *reinterpret_cast<const float4 *>(w1 + (size_t)(i + q) * H + j0);
+                  t[u][0] = __fmaf_rn(f, w.x, t[u][0]); t[u][1] = __fmaf_rn(f, w.y, t[u][1]);
+                  t[u][2] = __fmaf_rn(f, w.z, t[u][2]); t[u][3] = __fmaf_rn(f, w.w, t[u][3]);
+                }
+              }
             }
 #pragma unroll
-            for (int e = 0; e < 4; ++e) y[e] = __fadd_rn(y[e], t[e]);
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) y[u][e] = __fadd_rn(y[u][e], t[u][e]);
             i += bs;
             if (bs != 8) break;
           }
         }
       }
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float z1 = __fadd_rn(y[e], b1[j0 + e]);
-        hs[j0 + e] = z1 > 0.f ? z1 : 0.f;
+      for (int u = 0; u < 4; ++u) {
+        const int j0 = jb + 4 * lane + 128 * u;
+        if (j0 < H) {
+          const float4 bb = *reinterpret_cast<const float4 *>(b1 + j0);
+          float4 r;
+          r.x = fmaxf(__fadd_rn(y[u][0], bb.x), 0.f); r.y = fmaxf(__fadd_rn(y[u][1], bb.y), 0.f);
+          r.z = fmaxf(__fadd_rn(y[u][2], bb.z), 0.f); r.w = fmaxf(__fadd_rn(y[u][3], bb.w), 0.f);
+          *reinterpret_cast<float4 *>(hs + j0) = r;
+        }
       }
-    } else {
-      for (int e = 0; e < 4 && j0 + e < H; ++e) {
-        const float z1 = __fadd_rn(z1_unit(feats, w1, n, H, j0 + e), b1[j0 + e]);
-        hs[j0 + e] = z1 > 0.f ? z1 : 0.f;
-      }
+    }
+  } else {
+    for (int j = lane; j < H; j += 32) {
+      const float z1 = __fadd_rn(z1_unit(feats, w1, n, H, j), b1[j]);
+      hs[j] = z1 > 0.f ? z1 : 0.f;
     }
   }
   __syncwarp();
@@ -298,7 +327,7 @@ inline SmemPlan plan_smem(int d, int K, int H, int max_bytes, int nw_cap) {
   return s;   // nw == 0: does not fit
 }
 
-template <typename TW>
+template <typename TW, int CPL>
 __global__ void __launch_bounds__(32 * MAXW)
 predictor_tma_kernel(PredParams p, SmemPlan sp) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -387,7 +416,7 @@ predictor_tma_kernel(PredParams p, SmemPlan sp) {
     phase ^= 1u;
     float mean, denom;
     bool bad;
-    warp_ln_stats(sh, d, lane, mean, denom, bad);
+    warp_ln_stats<CPL>(sh, d, lane, mean, denom, bad);
     const float rinv = __frcp_rn(denom);
     for (int c0 = 0; c0 < K; c0 += GROUP) {
       const int ng = (K - c0) < GROUP ? (K - c0) : GROUP;
@@ -403,8 +432,11 @@ predictor_tma_kernel(PredParams p, SmemPlan sp) {
 #pragma unroll
         for (int g = 0; g < 4; ++g) acc[q][g] = 0.f;
 #pragma unroll
-      for (int g = 0; g < 4; ++g)
-        for (int c = 32 * g + lane; c < nchunk; c += NPART) {
+      for (int s = 0; s < CPL; ++s)
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+          const int c = 32 * g + lane + NPART * s;
+          if (c >= nchunk) continue;
           const float4 xv = *reinterpret_cast<const float4 *>(sh + CHUNK * c);
           const float4 gv = *reinterpret_cast<const float4 *>(gs + CHUNK * c);
           const float4 bv = *reinterpret_cast<const float4 *>(bs + CHUNK * c);
@@ -574,6 +606,20 @@ static void device_limits() {
 }
 
 template <typename TW>
+struct TmaLaunch {
+  const PredParams &p; const SmemPlan &sp; int grid; cudaStream_t stream;
+  template <int CPL> void operator()() const {
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(predictor_tma_kernel<TW, CPL>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_optin);
+      configured = true;
+    }
+    predictor_tma_kernel<TW, CPL><<<grid > 0 ? grid : 1, 32 * sp.nw, sp.bytes, stream>>>(p, sp);
+  }
+};
+
+template <typename TW>
 static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cudaStream_t stream) {
   device_limits();
   if (a->mode == SPX_MODE_STRICT) {
@@ -586,15 +632,9 @@ static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cu
     if (((size_t)p.d * sizeof(TW)) % 16) return SPX_EINVAL;   // TMA bulk: 16-byte rows
     SmemPlan sp = plan_smem<TW>(p.d, p.K, p.H, g_smem_optin, MAXW);
     if (sp.nw == 0) return SPX_EINVAL;
-    static bool configured = false;
-    if (!configured) {
-      cudaFuncSetAttribute(predictor_tma_kernel<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           g_smem_optin);
-      configured = true;
-    }
     const long long need = (a->B + sp.nw - 1) / sp.nw;
     const int grid = (int)(need < g_sms ? need : g_sms);
-    predictor_tma_kernel<TW><<<grid > 0 ? grid : 1, 32 * sp.nw, sp.bytes, stream>>>(p, sp);
+    if (!dispatch_cpl(p.d, TmaLaunch<TW>{p, sp, grid, stream})) return SPX_EINVAL;
   }
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
 }

@@ -6,10 +6,11 @@
 // all live nodes are de-duplicated into U unique LM-head rows (the merged
 // mapping of the paper, §6.2); one warp owns one unique row, holds it in
 // registers (read from HBM exactly once), and dots it with every node that
-// asked for it (normed node rows come from L2).  The dot is the canonical
-// CDOT order, so every logit is bit-identical to the predictor kernel's
-// sliced logit for the same (row, id) -- the reference's "grouped == sliced"
-// contract (tests/test_tree.py:32-42).
+// asked for it (normed node rows come from L2).  FAST: the canonical CDOT
+// order, so every logit is bit-identical to the predictor kernel's sliced
+// logit for the same (row, id) -- the reference's "grouped == sliced"
+// contract (tests/test_tree.py:32-42).  STRICT: each (node, id) dot is the
+// reference's sequential chain (kernels/_ckern.pyx:16-31), one lane per pair.
 #include "spx_common.cuh"
 #include "../../include/specexit_b200.h"
 
@@ -21,7 +22,7 @@ template <typename TW, int CPL>
 __global__ void __launch_bounds__(TREE_THREADS)
 tree_merged_kernel(const float *hn, int N, const TW *head, int V, int d,
                    const int32_t *uniq, int U, const int32_t *uniq_ptr, const int32_t *pair_node,
-                   const int32_t *pair_out, float *logits, int *err) {
+                   const int32_t *pair_out, float *logits, int strict, int *err) {
   const int lane = threadIdx.x & 31;
   const int u = blockIdx.x * (TREE_THREADS / 32) + (threadIdx.x >> 5);
   if (u >= U) return;
@@ -30,25 +31,38 @@ tree_merged_kernel(const float *hn, int N, const TW *head, int V, int d,
     if (lane == 0) atomicOr(err, ERR_ID_RANGE);
     return;
   }
-  const int nchunk = d / CHUNK;
   const TW *wrow = head + (size_t)id * d;
+  if (strict) {
+    for (int q = uniq_ptr[u] + lane; q < uniq_ptr[u + 1]; q += 32) {
+      const float *h = hn + (size_t)pair_node[q] * d;
+      float acc = 0.f;
+      for (int j = 0; j < d; j += CHUNK) {
+        float w[4];
+        load4_f32<TW>(wrow + j, w);
+#pragma unroll
+        for (int e = 0; e < CHUNK; ++e) acc = __fadd_rn(acc, __fmul_rn(h[j + e], w[e]));
+      }
+      logits[pair_out[q]] = acc;
+    }
+    return;
+  }
+  const int nchunk = d / CHUNK;
   Chunk<TW> w[4][CPL];
 #pragma unroll
-  for (int g = 0; g < 4; ++g)
+  for (int s = 0; s < CPL; ++s)
 #pragma unroll
-    for (int s = 0; s < CPL; ++s) {
+    for (int g = 0; g < 4; ++g) {
       const int c = 32 * g + lane + NPART * s;
       if (c < nchunk) w[g][s].load(wrow + CHUNK * c);
       else w[g][s].zero();
     }
   for (int q = uniq_ptr[u]; q < uniq_ptr[u + 1]; ++q) {
-    const int node = pair_node[q];
-    const float *h = hn + (size_t)node * d;
+    const float *h = hn + (size_t)pair_node[q] * d;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int g = 0; g < 4; ++g)
+    for (int s = 0; s < CPL; ++s)
 #pragma unroll
-      for (int s = 0; s < CPL; ++s) {
+      for (int g = 0; g < 4; ++g) {
         const int c = 32 * g + lane + NPART * s;
         if (c < nchunk) {
           const float4 h0 = __ldg(reinterpret_cast<const float4 *>(h + CHUNK * c));
@@ -68,16 +82,26 @@ tree_merged_kernel(const float *hn, int N, const TW *head, int V, int d,
   }
 }
 
+template <typename TW>
+struct TreeLaunch {
+  const float *hn; int N; const TW *head; int V, d;
+  const int32_t *uniq; int U; const int32_t *uniq_ptr, *pair_node, *pair_out;
+  float *logits; int strict; int *err; unsigned grid; cudaStream_t stream;
+  template <int CPL> void operator()() const {
+    tree_merged_kernel<TW, CPL><<<grid, TREE_THREADS, 0, stream>>>(
+        hn, N, head, V, d, uniq, U, uniq_ptr, pair_node, pair_out, logits, strict, err);
+  }
+};
+
 }  // namespace spx
 
 using namespace spx;
 
 extern "C" int spx_tree_merged_logits(const float *hn, int64_t N, const void *head,
-                                      int32_t head_dtype, int64_t V,
-                                      int64_t d, const int32_t *uniq, int64_t U,
-                                      const int32_t *uniq_ptr, const int32_t *pair_node,
-                                      const int32_t *pair_out, float *logits, int32_t *err,
-                                      void *stream_) {
+                                      int32_t head_dtype, int64_t V, int64_t d,
+                                      const int32_t *uniq, int64_t U, const int32_t *uniq_ptr,
+                                      const int32_t *pair_node, const int32_t *pair_out,
+                                      float *logits, int32_t mode, int32_t *err, void *stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
   if (!hn || !head || !uniq || !uniq_ptr || !pair_node || !pair_out || !logits || !err ||
       N < 0 || U < 0 || d <= 0 || d % CHUNK || V <= 0)
@@ -85,23 +109,19 @@ extern "C" int spx_tree_merged_logits(const float *hn, int64_t N, const void *he
   if (U == 0) return 0;
   const int wpc = TREE_THREADS / 32;
   const unsigned grid = (unsigned)((U + wpc - 1) / wpc);
-  const int nchunk = (int)(d / CHUNK);
-#define SPX_LAUNCH_TREE(CPL)                                                                   \
-  do {                                                                                         \
-    if (head_dtype == SPX_DTYPE_F32)                                                           \
-      tree_merged_kernel<float, CPL><<<grid, TREE_THREADS, 0, stream>>>(                        \
-          hn, (int)N, (const float *)head, (int)V, (int)d, uniq, (int)U, uniq_ptr, pair_node,  \
-          pair_out, logits, err);                                                              \
-    else                                                                                       \
-      tree_merged_kernel<__nv_bfloat16, CPL><<<grid, TREE_THREADS, 0, stream>>>(                \
-          hn, (int)N, (const __nv_bfloat16 *)head, (int)V, (int)d, uniq, (int)U, uniq_ptr,     \
-          pair_node, pair_out, logits, err);                                                   \
-  } while (0)
-  if (nchunk <= NPART) SPX_LAUNCH_TREE(1);
-  else if (nchunk <= 2 * NPART) SPX_LAUNCH_TREE(2);
-  else if (nchunk <= 4 * NPART) SPX_LAUNCH_TREE(4);
-  else if (nchunk <= 8 * NPART) SPX_LAUNCH_TREE(8);
-  else return SPX_EINVAL;
-#undef SPX_LAUNCH_TREE
+  const int strict = mode == SPX_MODE_STRICT;
+  bool ok;
+  if (head_dtype == SPX_DTYPE_F32)
+    ok = dispatch_cpl((int)d, TreeLaunch<float>{hn, (int)N, (const float *)head, (int)V, (int)d,
+                                                uniq, (int)U, uniq_ptr, pair_node, pair_out,
+                                                logits, strict, err, grid, stream});
+  else if (head_dtype == SPX_DTYPE_BF16)
+    ok = dispatch_cpl((int)d, TreeLaunch<__nv_bfloat16>{
+                                  hn, (int)N, (const __nv_bfloat16 *)head, (int)V, (int)d, uniq,
+                                  (int)U, uniq_ptr, pair_node, pair_out, logits, strict, err,
+                                  grid, stream});
+  else
+    return SPX_EINVAL;
+  if (!ok) return SPX_EINVAL;
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
 }

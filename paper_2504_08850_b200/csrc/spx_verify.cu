@@ -44,6 +44,7 @@ __device__ __forceinline__ bool ver_row_on(const VerParams &p, int r) {
 // Canonical LayerNorm of one row into smem `hn` by one warp (FAST: the CDOT
 // statistics + reciprocal scaling, identical bits to the predictor kernel) or
 // one thread (STRICT: the reference's sequential sums and division).
+template <int CPL>
 __device__ void warp_layernorm(const VerParams &p, int r, float *hn, int lane, bool strict,
                                int *bad) {
   const float *x = p.hidden + (size_t)r * p.hidden_stride;
@@ -54,7 +55,7 @@ __device__ void warp_layernorm(const VerParams &p, int r, float *hn, int lane, b
   if (!strict) {
     float mean, denom;
     bool b;
-    warp_ln_stats(hn, d, lane, mean, denom, b);
+    warp_ln_stats<CPL>(hn, d, lane, mean, denom, b);
     if (b) *bad = 1;
     const float rinv = __frcp_rn(denom);
     for (int j = lane; j < d; j += 32)
@@ -159,7 +160,7 @@ verify_kernel(VerParams p) {
     if (nr == 0) break;
     if (warp < nr) {
       int bad = 0;
-      warp_layernorm(p, s_rows[warp], hn + (size_t)warp * p.d, lane, strict, &bad);
+      warp_layernorm<CPL>(p, s_rows[warp], hn + (size_t)warp * p.d, lane, strict, &bad);
       if (bad && lane == 0) { atomicOr(p.err, ERR_HIDDEN_NONFINITE); s_bad = 1; }
     }
     __syncthreads();
@@ -251,6 +252,7 @@ verify_kernel(VerParams p) {
 }
 
 // Final LayerNorm of N rows into hn (FAST: canonical, STRICT: sequential).
+template <int CPL>
 __global__ void final_norm_kernel(const float *x, int64_t stride, const float *g, const float *b,
                                   float *hn, int N, int d, int mode, int *err) {
   const int lane = threadIdx.x & 31;
@@ -259,7 +261,7 @@ __global__ void final_norm_kernel(const float *x, int64_t stride, const float *g
   VerParams p;
   p.hidden = x; p.hidden_stride = stride; p.g = g; p.b = b; p.d = d;
   int bad = 0;
-  warp_layernorm(p, row, hn + (size_t)row * d, lane, mode == SPX_MODE_STRICT, &bad);
+  warp_layernorm<CPL>(p, row, hn + (size_t)row * d, lane, mode == SPX_MODE_STRICT, &bad);
   if (bad && lane == 0) atomicOr(err, ERR_HIDDEN_NONFINITE);
 }
 
@@ -333,7 +335,20 @@ extern "C" int spx_final_norm(const float *hidden, int64_t hidden_stride, const 
   if (!hidden || !g || !b || !hn || !err || N < 0 || d <= 0 || d % CHUNK) return SPX_EINVAL;
   if (N == 0) return 0;
   const int wpc = 4;
-  final_norm_kernel<<<(unsigned)((N + wpc - 1) / wpc), wpc * 32, 0, stream>>>(
-      hidden, hidden_stride ? hidden_stride : d, g, b, hn, (int)N, (int)d, mode, err);
+  const unsigned grid = (unsigned)((N + wpc - 1) / wpc);
+  const int64_t st = hidden_stride ? hidden_stride : d;
+  bool ok;
+  switch (((int)d / CHUNK + NPART - 1) / NPART) {
+    case 1: final_norm_kernel<1><<<grid, wpc * 32, 0, stream>>>(hidden, st, g, b, hn, (int)N, (int)d, mode, err); ok = true; break;
+    case 2: final_norm_kernel<2><<<grid, wpc * 32, 0, stream>>>(hidden, st, g, b, hn, (int)N, (int)d, mode, err); ok = true; break;
+    case 3: case 4: final_norm_kernel<4><<<grid, wpc * 32, 0, stream>>>(hidden, st, g, b, hn, (int)N, (int)d, mode, err); ok = true; break;
+    case 5: case 6: case 7: case 8: final_norm_kernel<8><<<grid, wpc * 32, 0, stream>>>(hidden, st, g, b, hn, (int)N, (int)d, mode, err); ok = true; break;
+    default:
+      if (d / CHUNK <= 16 * NPART) {
+        final_norm_kernel<16><<<grid, wpc * 32, 0, stream>>>(hidden, st, g, b, hn, (int)N, (int)d, mode, err);
+        ok = true;
+      } else ok = false;
+  }
+  if (!ok) return SPX_EINVAL;
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
 }

@@ -301,7 +301,8 @@ def merged_logits(model: TransformerModel, hn: torch.Tensor, id_lists) -> list:
                                            model.spx_dtype, model.config.vocab_size,
                                            model.config.hidden_dim, N.ptr(d_uniq), uniq.size,
                                            N.ptr(d_uptr), N.ptr(d_node), N.ptr(d_out),
-                                           N.ptr(logits), N.ptr(err), N.stream_ptr()),
+                                           N.ptr(logits), numerics.mode(), N.ptr(err),
+                                           N.stream_ptr()),
             "spx_tree_merged_logits")
     N.raise_device_error(err.item())
     return list(torch.split(logits, sizes))
