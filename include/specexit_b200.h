@@ -65,6 +65,7 @@ typedef struct {
   const float *norm_b;       /* (d) final_norm.b                               */
   const void *head;          /* (V, d) LM head, vocab-row major                */
   int32_t head_dtype;        /* SPX_DTYPE_*                                    */
+  const float *head_bw;      /* (V) spx_head_bias output (FAST mode; NULL = 0) */
   const int32_t *ids;        /* (B, K) speculative token ids                   */
   float *prev;               /* (B, K) in: previous local probs, out: new ones */
   const float *w1;           /* (3K, H) predictor W1 (row-major, as reference) */
@@ -113,6 +114,7 @@ typedef struct {
   const float *norm_g, *norm_b;
   const void *head;                             /* (V, d) */
   int32_t head_dtype;                           /* SPX_DTYPE_* */
+  const float *head_bw;                         /* (V) spx_head_bias (FAST); NULL = 0 */
   const uint8_t *gate;        /* (B) optional: row computed iff gate[r] != 0  */
   const uint8_t *row_done;    /* (B) optional: row skipped if nonzero         */
   const int32_t *spec_ptr;    /* (B+1) optional CSR offsets of verify sets    */
@@ -152,15 +154,27 @@ int spx_sched_active(spx_online_state st, uint64_t offline_mask, int64_t B, int3
                      int32_t mode, uint64_t *active_out, void *stream);
 
 /* K6 -- context-aware merged mapping (src/specexit/tree.py:92-113): logits of
- * node n for ids[ptr[n]..ptr[n+1]) with each UNIQUE id's LM-head row read
- * once.  uniq (U) are the distinct ids (grouped: pairs of unique id u are
- * uniq_ptr[u]..uniq_ptr[u+1]), pair_uid / pair_node / pair_out (P)
- * map every (node, id) pair to its unique row; hn (N, d) are the final-normed
- * node rows (spx_final_norm).  Bit-identical to K1's logits (FAST order). */
-int spx_tree_merged_logits(const float *hn, int64_t N, const void *head, int32_t head_dtype,
-                           int64_t V, int64_t d, const int32_t *uniq, int64_t U, const int32_t *uniq_ptr,
+ * the (node, id) pairs with each UNIQUE id's LM-head row read once.  uniq (U)
+ * are the distinct ids; the pairs of unique id u are uniq_ptr[u]..uniq_ptr[u+1]
+ * with pair_node (row of xg) and pair_out (index into logits).  xg / r are the
+ * spx_head_prep outputs of the N node rows.  FAST: logit = r*CDOT(xg,W)+bw,
+ * bit-identical to K1's logits; STRICT: xg holds the reference LayerNorm rows
+ * and each logit is the reference's sequential dot. */
+int spx_tree_merged_logits(const float *xg, const float *r, int64_t N, const void *head,
+                           int32_t head_dtype, const float *head_bw, int64_t V, int64_t d,
+                           const int32_t *uniq, int64_t U, const int32_t *uniq_ptr,
                            const int32_t *pair_node, const int32_t *pair_out, float *logits,
                            int32_t mode, int32_t *err, void *stream);
+/* Head-side normalisation of N rows for K6: FAST -> xg = (x-mean)*g and
+ * r = 1/sqrt(var+eps) per row (canonical order); STRICT -> xg = the
+ * reference LayerNorm (model.py:140-146), r = 1. */
+int spx_head_prep(const float *hidden, int64_t hidden_stride, const float *g, const float *b,
+                  float *xg, float *r, int64_t N, int64_t d, int32_t mode, int32_t *err,
+                  void *stream);
+/* bw[v] = CDOT(b, head_v): the final-norm bias folded through the head, once
+ * per model (FAST path; all-zero b gives bw = 0). */
+int spx_head_bias(const void *head, int32_t head_dtype, const float *b, int64_t V, int64_t d,
+                  float *bw, void *stream);
 /* final LayerNorm of N rows into hn (model.py:140-146), FAST or STRICT. */
 int spx_final_norm(const float *hidden, int64_t hidden_stride, const float *g, const float *b,
                    float *hn, int64_t N, int64_t d, int32_t mode, int32_t *err, void *stream);

@@ -32,7 +32,8 @@ _i32, _i64, _f32, _f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.
 
 class PredictorArgs(ctypes.Structure):
     _fields_ = [("hidden", _vp), ("hidden_stride", _i64), ("norm_g", _vp), ("norm_b", _vp),
-                ("head", _vp), ("head_dtype", _i32), ("ids", _vp), ("prev", _vp),
+                ("head", _vp), ("head_dtype", _i32), ("head_bw", _vp), ("ids", _vp),
+                ("prev", _vp),
                 ("w1", _vp), ("b1", _vp), ("w2", _vp), ("b2", _f32), ("z_cut", _f32),
                 ("policy", _i32), ("const_prob", _f64), ("threshold", _f64),
                 ("logits_out", _vp), ("feat_out", _vp), ("z_out", _vp), ("prob_out", _vp),
@@ -43,7 +44,8 @@ class PredictorArgs(ctypes.Structure):
 
 class VerifyArgs(ctypes.Structure):
     _fields_ = [("hidden", _vp), ("hidden_stride", _i64), ("norm_g", _vp), ("norm_b", _vp),
-                ("head", _vp), ("head_dtype", _i32), ("gate", _vp), ("row_done", _vp),
+                ("head", _vp), ("head_dtype", _i32), ("head_bw", _vp), ("gate", _vp),
+                ("row_done", _vp),
                 ("spec_ptr", _vp), ("spec_ids", _vp), ("token_out", _vp),
                 ("verified_out", _vp), ("maxlogit_out", _vp), ("logits_out", _vp),
                 ("done_out", _vp), ("exit_layer_out", _vp), ("full_heads", _vp),
@@ -71,8 +73,10 @@ def lib():
     L.spx_verify.argtypes = [ctypes.POINTER(VerifyArgs), _vp]
     L.spx_sched_update.argtypes = [OnlineStateC, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]
     L.spx_sched_active.argtypes = [OnlineStateC, ctypes.c_uint64, _i64, _i32, _i32, _vp, _vp]
-    L.spx_tree_merged_logits.argtypes = [_vp, _i64, _vp, _i32, _i64, _i64, _vp, _i64, _vp, _vp,
-                                         _vp, _vp, _i32, _vp, _vp]
+    L.spx_tree_merged_logits.argtypes = [_vp, _vp, _i64, _vp, _i32, _vp, _i64, _i64, _vp, _i64,
+                                         _vp, _vp, _vp, _vp, _i32, _vp, _vp]
+    L.spx_head_prep.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _vp, _vp]
+    L.spx_head_bias.argtypes = [_vp, _i32, _vp, _i64, _i64, _vp, _vp]
     L.spx_final_norm.argtypes = [_vp, _i64, _vp, _vp, _vp, _i64, _i64, _i32, _vp, _vp]
     L.spx_path_and.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _vp]
     L.spx_init_uniform.argtypes = [_vp, _i32, _i64, _i64, _i32, ctypes.c_uint64, _f64, _f64, _vp]

@@ -38,12 +38,12 @@ namespace spx {
 constexpr int MAXK = 64;
 constexpr int MAXH = 1024;
 constexpr int GROUP = 4;              // LM-head rows per TMA stage
-constexpr int MAXW = 8;               // warps (row slots) per CTA
 
 struct PredParams {
   const float *hidden; int64_t hidden_stride;
   const float *norm_g, *norm_b;
   const void *head;            // (V, d) bf16 or f32
+  const float *head_bw;        // (V) CDOT(final_norm.b, head_v) (FAST path), may be null
   const int32_t *ids;          // (B, K)
   float *prev;                 // (B, K) in: previous local probs; out: new
   const float *w1, *b1, *w2;   // (3K, H), (H), (H)
@@ -139,18 +139,19 @@ __device__ __forceinline__ float z1_unit(const float *feats, const float *w1, in
   return acc;
 }
 
-// MLP of one row, whole warp.  w1/b1/w2 may point to shared or global
-// memory; hs: per-warp scratch of H floats.  Returns z2 in every lane.
-__device__ float warp_mlp(const float *feats, const float *w1, const float *b1, const float *w2,
-                          float b2, int K, int H, float *hs, int lane) {
-  const int n = 3 * K;
-  // z1 / ReLU.  Lane owns units j = jb + 4*lane + 128*u + e (u, e < 4): 16
-  // independent FMA chains per lane, 16-byte conflict-free W1 reads.
+// z1 = feats @ W1 + b1 and ReLU into hs, for the units owned by this warp:
+// j = jb + 4*lane + 128*(u0 + u) + e (jb over 512-blocks, u < NU, e < 4),
+// i.e. NU*4 independent FMA chains per lane with 16-byte conflict-free W1
+// reads.  NU = 4, u0 = 0: one warp does all units; NU = 1, u0 = w: warp w of
+// a 4-warp team does a quarter.  Per-unit arithmetic is identical.
+template <int NU>
+__device__ void mlp_z1(const float *feats, const float *w1, const float *b1, int n, int H,
+                       float *hs, int lane, int u0) {
   if ((H % 4) == 0) {
     for (int jb = 0; jb < H; jb += 512) {
-      float y[4][4];
+      float y[NU][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < NU; ++u)
 #pragma unroll
         for (int e = 0; e < 4; ++e) y[u][e] = 0.f;
       if (n <= 48) {
@@ -158,8 +159,8 @@ __device__ float warp_mlp(const float *feats, const float *w1, const float *b1, 
         for (int i = 0; i < n; ++i) {
           const float f = feats[i];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int j0 = jb + 4 * lane + 128 * u;
+          for (int u = 0; u < NU; ++u) {
+            const int j0 = jb + 4 * lane + 128 * (u0 + u);
             if (j0 < H) {
               const float4 w = *reinterpret_cast<const float4 *>(w1 + (size_t)i * H + j0);
               y[u][0] = __fmaf_rn(f, w.x, y[u][0]); y[u][1] = __fmaf_rn(f, w.y, y[u][1]);
@@ -173,16 +174,16 @@ __device__ float warp_mlp(const float *feats, const float *w1, const float *b1, 
         for (int bi = 0; bi < 4; ++bi) {
           const int bs = blocks[bi];
           while (n - i >= bs) {
-            float t[4][4];
+            float t[NU][4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < NU; ++u)
 #pragma unroll
               for (int e = 0; e < 4; ++e) t[u][e] = 0.f;
             for (int q = 0; q < bs; ++q) {
               const float f = feats[i + q];
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int j0 = jb + 4 * lane + 128 * u;
+              for (int u = 0; u < NU; ++u) {
+                const int j0 = jb + 4 * lane + 128 * (u0 + u);
                 if (j0 < H) {
                   const float4 w = *reinterpret_cast<const float4 *>(w1 + (size_t)(i + q) * H + j0);
                   t[u][0] = __fmaf_rn(f, w.x, t[u][0]); t[u][1] = __fmaf_rn(f, w.y, t[u][1]);
@@ -191,7 +192,7 @@ __device__ float warp_mlp(const float *feats, const float *w1, const float *b1, 
               }
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < NU; ++u)
 #pragma unroll
               for (int e = 0; e < 4; ++e) y[u][e] = __fadd_rn(y[u][e], t[u][e]);
             i += bs;
@@ -200,8 +201,8 @@ __device__ float warp_mlp(const float *feats, const float *w1, const float *b1, 
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j0 = jb + 4 * lane + 128 * u;
+      for (int u = 0; u < NU; ++u) {
+        const int j0 = jb + 4 * lane + 128 * (u0 + u);
         if (j0 < H) {
           const float4 bb = *reinterpret_cast<const float4 *>(b1 + j0);
           float4 r;
@@ -212,22 +213,29 @@ __device__ float warp_mlp(const float *feats, const float *w1, const float *b1, 
       }
     }
   } else {
-    for (int j = lane; j < H; j += 32) {
+    // ragged H: scalar units, split over the same NU/u0 ownership by lanes
+    for (int j = lane + 32 * u0; j < H; j += 32 * (NU == 4 ? 1 : 4)) {
       const float z1 = __fadd_rn(z1_unit(feats, w1, n, H, j), b1[j]);
       hs[j] = z1 > 0.f ? z1 : 0.f;
     }
   }
-  __syncwarp();
-  // z2: OpenBLAS SkylakeX sdot order (sdot.c + sdot_microk_skylakex-2.c):
-  // 4 x 16-lane FMA accumulators over 64-element blocks, fold 16->8, optional
-  // 32-element AVX2 step, lane-wise ((a0+a1)+a2)+a3, 8->4, ((q0+q1)+(q2+q3)),
-  // scalar tail, + b2.
+}
+
+// sdot partial A[c] (c < 64) = FMA chain over the 64-element blocks.
+__device__ __forceinline__ float z2_partial(const float *hs, const float *w2, int H, int c) {
+  const int n64 = (H & ~31) & ~63;
+  float a = 0.f;
+  for (int b = 0; b < n64; b += 64) a = __fmaf_rn(hs[b + c], w2[b + c], a);
+  return a;
+}
+
+// z2: OpenBLAS SkylakeX sdot order (sdot.c + sdot_microk_skylakex-2.c):
+// 4 x 16-lane FMA accumulators over 64-element blocks (alo = A[lane], ahi =
+// A[lane+32]), fold 16->8, optional 32-element AVX2 step, lane-wise
+// ((a0+a1)+a2)+a3, 8->4, ((q0+q1)+(q2+q3)), scalar tail, + b2.  Whole warp.
+__device__ float z2_tree(float alo, float ahi, const float *hs, const float *w2, int H, float b2,
+                         int lane) {
   const int n1 = H & ~31, n64 = n1 & ~63;
-  float alo = 0.f, ahi = 0.f;              // A[lane], A[lane + 32]
-  for (int b = 0; b < n64; b += 64) {
-    alo = __fmaf_rn(hs[b + lane], w2[b + lane], alo);
-    ahi = __fmaf_rn(hs[b + lane + 32], w2[b + lane + 32], ahi);
-  }
   float blo = __fadd_rn(alo, __shfl_down_sync(0xffffffffu, alo, 8));
   float bhi = __fadd_rn(ahi, __shfl_down_sync(0xffffffffu, ahi, 8));
   const int m = lane & 15;
@@ -246,6 +254,16 @@ __device__ float warp_mlp(const float *feats, const float *w1, const float *b1, 
   for (int i = n1; i < H; ++i) dot = __fadd_rn(dot, __fmul_rn(hs[i], w2[i]));
   __syncwarp();
   return __fadd_rn(dot, b2);
+}
+
+// MLP of one row by one warp.  w1/b1/w2 may point to shared or global memory;
+// hs: scratch of H floats.  Returns z2 in every lane.
+__device__ float warp_mlp(const float *feats, const float *w1, const float *b1, const float *w2,
+                          float b2, int K, int H, float *hs, int lane) {
+  mlp_z1<4>(feats, w1, b1, 3 * K, H, hs, lane, 0);
+  __syncwarp();
+  return z2_tree(z2_partial(hs, w2, H, lane), z2_partial(hs, w2, H, lane + 32), hs, w2, H, b2,
+                 lane);
 }
 
 __device__ __forceinline__ double sigmoid64(float z2) {   // predictor.py:87-94
@@ -288,77 +306,98 @@ __device__ void warp_row_tail(const PredParams &p, int row, float *feats, const 
 }
 
 // ------------------------------------------------------------ FAST (TMA)
+// One 4-warp TEAM per row: warp w of the team owns canonical partial group
+// g = w (partials 32w..32w+31), so every per-row reduction is split four
+// ways; teams synchronise with their own named barrier.  Each team owns a
+// shared-memory stage (hidden row + GROUP LM-head rows) filled by 1-D TMA
+// bulk copies; the next row's copies are issued as soon as the current row's
+// dot products are done.  Fast-path algebra (canonical, shared with K4/K6):
+//   mean = CSUM(x)/d ; xc = x - mean ; var = CSUM(xc*xc)/d ; r = 1/sqrt(var+eps)
+//   logit_v = r * CDOT(xc*g, W_v) + bw_v      (bw_v = CDOT(b, W_v), per model)
+// i.e. the LayerNorm is folded into the head dot (one pass over the row for
+// the variance and all K dots).
+constexpr int TEAM = 4;
+constexpr int MAXT = 4;
+constexpr int RED_FLOATS = 32;    // (GROUP + 2) * 4 used
+
 struct SmemPlan {
-  int nw;          // warps (= row stages) per CTA
-  int w1_smem;     // stage W1 in shared memory?
+  int nt;          // teams (= row stages) per CTA
+  int w1_smem;     // W1 staged in shared memory?
   size_t bytes;
-  size_t off_g, off_b, off_w2, off_b1, off_w1, off_warp, warp_bytes, scratch_bytes, off_bar;
+  size_t off_g, off_w2, off_b1, off_w1, off_team, team_bytes, scratch_bytes, off_bar;
 };
 
 template <typename TW>
-inline SmemPlan plan_smem(int d, int K, int H, int max_bytes, int nw_cap) {
-  SmemPlan s{};
+inline SmemPlan plan_smem(int d, int K, int H, int max_bytes) {
+  SmemPlan best{};
   const size_t stage = (size_t)d * 4 + (size_t)GROUP * d * sizeof(TW);
-  const size_t scratch = ((size_t)(3 * MAXK + (H > 0 ? H : 1)) * 4 + 127) / 128 * 128;
-  const size_t per_warp = scratch + (stage + 127) / 128 * 128;
-  const size_t w1b = (size_t)3 * K * H * 4;
-  const size_t fixed0 = (((size_t)2 * d + 2 * H) * 4 + 127) / 128 * 128 + 256;
-  for (int w1 = (H > 0 ? 1 : 0); w1 >= 0; --w1) {
-    const size_t fixed = fixed0 + (w1 ? (w1b + 127) / 128 * 128 : 0);
-    int nw = 0;
-    for (int t = nw_cap; t >= 1; --t)
-      if (fixed + (size_t)t * per_warp + 64 <= (size_t)max_bytes) { nw = t; break; }
-    if (nw >= (w1 ? 3 : 1)) {
-      s.nw = nw; s.w1_smem = w1;
+  const size_t scratch = ((size_t)(RED_FLOATS + 4 + 3 * MAXK + (H > 0 ? H : 4) + 64) * 4 + 127) /
+                         128 * 128;
+  const size_t per_team = scratch + (stage + 127) / 128 * 128;
+  const size_t w1b = ((size_t)3 * K * H * 4 + 127) / 128 * 128;
+  const size_t fixed0 = (((size_t)d + 2 * H) * 4 + 127) / 128 * 128;
+  for (int w1 = 0; w1 <= (H > 0 ? 1 : 0); ++w1) {
+    const size_t fixed = fixed0 + (w1 ? w1b : 0);
+    int nt = 0;
+    for (int t = MAXT; t >= 1; --t)
+      if (fixed + (size_t)t * per_team + (MAXT + 1) * 8 <= (size_t)max_bytes) { nt = t; break; }
+    if (nt > best.nt || (nt == best.nt && nt > 0 && w1)) {
+      SmemPlan s{};
+      s.nt = nt; s.w1_smem = w1;
       size_t o = 0;
       s.off_g = o; o += (size_t)d * 4;
-      s.off_b = o; o += (size_t)d * 4;
       s.off_w2 = o; o += (size_t)H * 4;
       s.off_b1 = o; o += (size_t)H * 4;
       o = (o + 127) / 128 * 128;
-      s.off_w1 = o; if (w1) o += (w1b + 127) / 128 * 128;
-      s.off_warp = o; s.warp_bytes = per_warp; s.scratch_bytes = scratch;
-      o += (size_t)nw * per_warp;
-      s.off_bar = o; o += (size_t)(nw + 1) * 8;
+      s.off_w1 = o; if (w1) o += w1b;
+      s.off_team = o; s.team_bytes = per_team; s.scratch_bytes = scratch;
+      o += (size_t)nt * per_team;
+      s.off_bar = o; o += (size_t)(nt + 1) * 8;
       s.bytes = o;
-      return s;
+      best = s;
     }
   }
-  return s;   // nw == 0: does not fit
+  return best;
+}
+
+__device__ __forceinline__ void team_sync(int team) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(32 * TEAM) : "memory");
 }
 
 template <typename TW, int CPL>
-__global__ void __launch_bounds__(32 * MAXW)
-predictor_tma_kernel(PredParams p, SmemPlan sp) {
+__global__ void __launch_bounds__(32 * TEAM * MAXT)
+predictor_team_kernel(PredParams p, SmemPlan sp) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = sp.nw;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int team = warp / TEAM, w = warp % TEAM, nt = sp.nt;
   const int d = p.d, K = p.K, H = p.H, nchunk = d / CHUNK;
   float *gs = reinterpret_cast<float *>(smem + sp.off_g);
-  float *bs = reinterpret_cast<float *>(smem + sp.off_b);
   float *w2s = reinterpret_cast<float *>(smem + sp.off_w2);
   float *b1s = reinterpret_cast<float *>(smem + sp.off_b1);
   float *w1s = reinterpret_cast<float *>(smem + sp.off_w1);
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + sp.off_bar) + warp;
-  uint8_t *wbase = smem + sp.off_warp + (size_t)warp * sp.warp_bytes;
-  float *feats = reinterpret_cast<float *>(wbase);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + sp.off_bar) + team;
+  uint64_t *setup_bar = reinterpret_cast<uint64_t *>(smem + sp.off_bar) + nt;
+  uint8_t *tbase = smem + sp.off_team + (size_t)team * sp.team_bytes;
+  float *red = reinterpret_cast<float *>(tbase);            // [GROUP+2][4]
+  int *tflag = reinterpret_cast<int *>(red + RED_FLOATS);   // [4]
+  float *feats = red + RED_FLOATS + 4;
   float *hs = feats + 3 * MAXK;
-  float *sh = reinterpret_cast<float *>(wbase + sp.scratch_bytes);
-  TW *sw = reinterpret_cast<TW *>(wbase + sp.scratch_bytes + (size_t)d * 4);
+  float *as = hs + (H > 0 ? H : 4);
+  float *sh = reinterpret_cast<float *>(tbase + sp.scratch_bytes);
+  TW *sw = reinterpret_cast<TW *>(tbase + sp.scratch_bytes + (size_t)d * 4);
+  const TW *head = reinterpret_cast<const TW *>(p.head);
 
-  uint64_t *setup_bar = reinterpret_cast<uint64_t *>(smem + sp.off_bar) + nw;
   const bool mlp = p.policy == SPX_POLICY_MLP;
   const bool bulk_consts = (H % 4) == 0;
-  if (lane == 0) mbar_init(bar, 1);
+  if (w == 0 && lane == 0 && team < nt) mbar_init(bar, 1);
   if (threadIdx.x == 0) mbar_init(setup_bar, 1);
   fence_mbar_init();
   __syncthreads();
-  // ---- per-CTA constants -> shared memory (TMA bulk; plain loads if ragged)
-  if (threadIdx.x == 0) {
-    uint32_t bytes = 2u * d * 4u;
+  if (threadIdx.x == 0) {            // per-CTA constants by TMA
+    uint32_t bytes = (uint32_t)d * 4u;
     if (mlp && bulk_consts) bytes += 2u * H * 4u + (sp.w1_smem ? 3u * K * H * 4u : 0u);
     mbar_arrive_expect_tx(setup_bar, bytes);
     bulk_g2s(gs, p.norm_g, (uint32_t)d * 4u, setup_bar);
-    bulk_g2s(bs, p.norm_b, (uint32_t)d * 4u, setup_bar);
     if (mlp && bulk_consts) {
       bulk_g2s(w2s, p.w2, (uint32_t)H * 4u, setup_bar);
       bulk_g2s(b1s, p.b1, (uint32_t)H * 4u, setup_bar);
@@ -369,118 +408,182 @@ predictor_tma_kernel(PredParams p, SmemPlan sp) {
     for (int i = threadIdx.x; i < H; i += blockDim.x) { w2s[i] = p.w2[i]; b1s[i] = p.b1[i]; }
     if (sp.w1_smem)
       for (int i = threadIdx.x; i < 3 * K * H; i += blockDim.x) w1s[i] = p.w1[i];
+    __syncthreads();
   }
   const float *w1 = sp.w1_smem ? w1s : p.w1;
-
-  const int stride = gridDim.x * nw;
   const uint32_t wrow_bytes = (uint32_t)((size_t)d * sizeof(TW));
-  uint32_t phase = 0;
-  int id_bad = 0;
+  const bool leader = (w == 0 && lane == 0);
 
-  // lane 0 issues the TMA copies of the W rows of ids [c0, c0+ng) of `row`
-  auto issue_group = [&](int row, int c0, int ng, bool with_hidden) {
+  // leader: TMA copies for `row` (hidden row when with_hidden, W rows of ids
+  // [c0, c0+ng)); returns nonzero if an id was out of range (clamped to 0).
+  auto issue_group = [&](int row, int c0, int ng, bool with_hidden) -> int {
+    int bad = 0;
     fence_proxy_async();
     mbar_arrive_expect_tx(bar, (with_hidden ? (uint32_t)d * 4u : 0u) + (uint32_t)ng * wrow_bytes);
     if (with_hidden)
       bulk_g2s(sh, p.hidden + (size_t)row * p.hidden_stride, (uint32_t)d * 4u, bar);
     for (int q = 0; q < ng; ++q) {
       int id = p.ids[(size_t)row * K + c0 + q];
-      if (id < 0 || id >= p.V) { id_bad = 1; id = 0; }
-      bulk_g2s(sw + (size_t)q * d, reinterpret_cast<const TW *>(p.head) + (size_t)id * d,
-               wrow_bytes, bar);
+      if (id < 0 || id >= p.V) { bad = 1; id = 0; }
+      bulk_g2s(sw + (size_t)q * d, head + (size_t)id * d, wrow_bytes, bar);
     }
-  };
-  // issue (hidden row + first id group) for `row`; returns 1 if skipped.
-  auto issue = [&](int row) -> int {
-    int skip = 1;
-    if (lane == 0 && row < p.B) {
-      skip = row_skipped(p, row) ? 1 : 0;
-      if (!skip) issue_group(row, 0, K < GROUP ? K : GROUP, true);
-    }
-    return __shfl_sync(0xffffffffu, skip, 0);
+    return bad;
   };
 
-  int row = blockIdx.x * nw + warp;
-  int skip = issue(row);                // first row's copies overlap the setup copies
+  const int stride = gridDim.x * nt;
+  int row = blockIdx.x * nt + team;
+  if (team >= nt) return;
+  uint32_t phase = 0;
+  int id_bad = 0;
+  bool skip = row >= p.B || row_skipped(p, row);
+  if (leader && !skip) id_bad = issue_group(row, 0, K < GROUP ? K : GROUP, true);
   mbar_wait(setup_bar, 0);
-  if (mlp && !bulk_consts) __syncthreads();
+
   while (row < p.B) {
     const int next = row + stride;
     if (skip) {
-      if (lane == 0 && p.fired) p.fired[row] = 0;
+      if (leader && p.fired) p.fired[row] = 0;
       row = next;
-      skip = issue(row);
+      skip = row >= p.B || row_skipped(p, row);
+      if (leader && !skip) id_bad = issue_group(row, 0, K < GROUP ? K : GROUP, true);
       continue;
     }
     mbar_wait(bar, phase);
     phase ^= 1u;
-    float mean, denom;
-    bool bad;
-    warp_ln_stats<CPL>(sh, d, lane, mean, denom, bad);
-    const float rinv = __frcp_rn(denom);
+    // ---- pass 1: mean (this warp = canonical group w)
+    float part = 0.f;
+    bool fin = true;
+#pragma unroll
+    for (int s = 0; s < CPL; ++s) {
+      const int c = 32 * w + lane + NPART * s;
+      if (c < nchunk) {
+        const float4 v = *reinterpret_cast<const float4 *>(sh + CHUNK * c);
+        part = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(part, v.x), v.y), v.z), v.w);
+        fin &= is_finite(v.x) & is_finite(v.y) & is_finite(v.z) & is_finite(v.w);
+      }
+    }
+    part = warp_butterfly_sum(part);
+    const bool wbad = __any_sync(0xffffffffu, !fin);
+    if (lane == 0) { red[GROUP * 4 + w] = part; tflag[w] = wbad ? 1 : 0; }
+    team_sync(team);
+    const float mean = __fdiv_rn(canon_combine(red[GROUP * 4 + 0], red[GROUP * 4 + 1],
+                                               red[GROUP * 4 + 2], red[GROUP * 4 + 3]),
+                                 (float)d);
+    const bool hbad = (tflag[0] | tflag[1] | tflag[2] | tflag[3]) != 0;
+    float r = 0.f;
+    // ---- pass 2 (per id group): variance (first group) + the K dots
     for (int c0 = 0; c0 < K; c0 += GROUP) {
       const int ng = (K - c0) < GROUP ? (K - c0) : GROUP;
-      if (c0 > 0) {                       // next id group into the W stage
-        __syncwarp();
-        if (lane == 0) issue_group(row, c0, ng, false);
+      if (c0 > 0) {
+        team_sync(team);                       // everyone done with the W stage / red
+        if (leader) id_bad |= issue_group(row, c0, ng, false);
         mbar_wait(bar, phase);
         phase ^= 1u;
       }
-      float acc[GROUP][4];
+      float acc[GROUP] = {0.f, 0.f, 0.f, 0.f};
+      float sq = 0.f;
 #pragma unroll
-      for (int q = 0; q < GROUP; ++q)
-#pragma unroll
-        for (int g = 0; g < 4; ++g) acc[q][g] = 0.f;
-#pragma unroll
-      for (int s = 0; s < CPL; ++s)
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-          const int c = 32 * g + lane + NPART * s;
-          if (c >= nchunk) continue;
+      for (int s = 0; s < CPL; ++s) {
+        const int c = 32 * w + lane + NPART * s;
+        if (c < nchunk) {
           const float4 xv = *reinterpret_cast<const float4 *>(sh + CHUNK * c);
           const float4 gv = *reinterpret_cast<const float4 *>(gs + CHUNK * c);
-          const float4 bv = *reinterpret_cast<const float4 *>(bs + CHUNK * c);
-          const float hn[4] = {
-              __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv.x, mean), rinv), gv.x), bv.x),
-              __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv.y, mean), rinv), gv.y), bv.y),
-              __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv.z, mean), rinv), gv.z), bv.z),
-              __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(xv.w, mean), rinv), gv.w), bv.w)};
+          const float xc[4] = {__fsub_rn(xv.x, mean), __fsub_rn(xv.y, mean),
+                               __fsub_rn(xv.z, mean), __fsub_rn(xv.w, mean)};
+          sq = __fmaf_rn(xc[3], xc[3], __fmaf_rn(xc[2], xc[2],
+                         __fmaf_rn(xc[1], xc[1], __fmaf_rn(xc[0], xc[0], sq))));
+          const float xg[4] = {__fmul_rn(xc[0], gv.x), __fmul_rn(xc[1], gv.y),
+                               __fmul_rn(xc[2], gv.z), __fmul_rn(xc[3], gv.w)};
 #pragma unroll
           for (int q = 0; q < GROUP; ++q) {
             if (q < ng) {
               Chunk<TW> ch;
               ch.lds(sw + (size_t)q * d + CHUNK * c);
-              float w[4];
-              ch.to_f32(w);
+              float wf[4];
+              ch.to_f32(wf);
 #pragma unroll
-              for (int e = 0; e < CHUNK; ++e) acc[q][g] = __fmaf_rn(hn[e], w[e], acc[q][g]);
+              for (int e = 0; e < CHUNK; ++e) acc[q] = __fmaf_rn(xg[e], wf[e], acc[q]);
             }
           }
         }
-#pragma unroll
-      for (int q = 0; q < GROUP; ++q) {
-        if (q < ng) {
-          float gsum[4];
-#pragma unroll
-          for (int g = 0; g < 4; ++g) gsum[g] = warp_butterfly_sum(acc[q][g]);
-          if (lane == 0) feats[c0 + q] = canon_combine(gsum[0], gsum[1], gsum[2], gsum[3]);
-        }
       }
-    }
-    __syncwarp();
-    const int ibad = __shfl_sync(0xffffffffu, id_bad, 0);
-    id_bad = 0;
-    // the stage is free: prefetch the next row while this row's tail runs
-    const int nskip = issue(next);
-    if (ibad || bad) {
+#pragma unroll
+      for (int q = 0; q < GROUP; ++q)
+        if (q < ng) acc[q] = warp_butterfly_sum(acc[q]);
+      if (c0 == 0) sq = warp_butterfly_sum(sq);
       if (lane == 0) {
-        atomicOr(p.err, (ibad ? ERR_ID_RANGE : 0) | (bad ? ERR_HIDDEN_NONFINITE : 0));
-        if (p.fired) p.fired[row] = 0;
+#pragma unroll
+        for (int q = 0; q < GROUP; ++q) red[q * 4 + w] = acc[q];
+        if (c0 == 0) red[(GROUP + 1) * 4 + w] = sq;
       }
-    } else {
-      warp_row_tail(p, row, feats, w1, b1s, w2s, hs, lane);
+      team_sync(team);
+      if (c0 == 0) {
+        const float var = __fdiv_rn(canon_combine(red[(GROUP + 1) * 4 + 0], red[(GROUP + 1) * 4 + 1],
+                                                  red[(GROUP + 1) * 4 + 2], red[(GROUP + 1) * 4 + 3]),
+                                    (float)d);
+        r = __frcp_rn(__fsqrt_rn(__fadd_rn(var, 1e-5f)));
+      }
+      if (w == 0 && lane < ng) {
+        const int q = lane;
+        int id = p.ids[(size_t)row * K + c0 + q];
+        id = (id < 0 || id >= p.V) ? 0 : id;
+        const float dot = canon_combine(red[q * 4 + 0], red[q * 4 + 1], red[q * 4 + 2], red[q * 4 + 3]);
+        feats[c0 + q] = __fadd_rn(__fmul_rn(r, dot), p.head_bw ? p.head_bw[id] : 0.f);
+      }
     }
-    row = next;
+    const int ibad = __shfl_sync(0xffffffffu, id_bad, 0);   // leader's lane is lane 0 of w0
+    team_sync(team);                                       // stage free, feats complete
+    // ---- prefetch the next row while this row's tail runs
+    const int nrow = next;
+    const bool nskip = nrow >= p.B || row_skipped(p, nrow);
+    if (leader) id_bad = nskip ? 0 : issue_group(nrow, 0, K < GROUP ? K : GROUP, true);
+    // ---- softmax / features (warp 0), error handling
+    if (w == 0) {
+      int ok = 0;
+      if (ibad || hbad) {
+        if (lane == 0) atomicOr(p.err, (ibad ? ERR_ID_RANGE : 0) | (hbad ? ERR_HIDDEN_NONFINITE : 0));
+      } else {
+        ok = warp_softmax_features(p, row, feats, lane) ? 1 : 0;
+      }
+      if (p.logits_out && !ibad && !hbad) {
+        if (lane < K) p.logits_out[(size_t)row * K + lane] = feats[lane];
+        if (lane + 32 < K) p.logits_out[(size_t)row * K + lane + 32] = feats[lane + 32];
+      }
+      if (ok) {
+        if (p.feat_out)
+          for (int i = lane; i < 3 * K; i += 32) p.feat_out[(size_t)row * 3 * K + i] = feats[i];
+        if (lane < K) p.prev[(size_t)row * K + lane] = feats[K + lane];          // engine.py:196
+        if (lane + 32 < K) p.prev[(size_t)row * K + lane + 32] = feats[K + lane + 32];
+        if (lane == 0 && p.evals) p.evals[row] += 1;
+      } else if (lane == 0 && p.fired) {
+        p.fired[row] = 0;
+      }
+      if (lane == 0) tflag[0] = ok;
+    }
+    team_sync(team);
+    const int ok = tflag[0];
+    if (ok) {
+      if (mlp) {
+        mlp_z1<1>(feats, w1, b1s, 3 * K, H, hs, lane, w);
+        team_sync(team);
+        if (w < 2) as[32 * w + lane] = z2_partial(hs, w2s, H, 32 * w + lane);
+        team_sync(team);
+        if (w == 0) {
+          const float z2 = z2_tree(as[lane], as[lane + 32], hs, w2s, H, p.b2, lane);
+          if (lane == 0) {
+            if (p.z_out) p.z_out[row] = z2;
+            if (p.prob_out) p.prob_out[row] = sigmoid64(z2);
+            if (p.fired) p.fired[row] = (z2 >= p.z_cut) ? 1 : 0;
+          }
+        }
+      } else if (leader) {
+        if (p.prob_out) p.prob_out[row] = p.const_prob;
+        if (p.z_out) p.z_out[row] = 0.0f;
+        if (p.fired) p.fired[row] = (p.const_prob > p.threshold) ? 1 : 0;
+      }
+    }
+    team_sync(team);                      // feats/hs/as/tflag reused by the next row
+    row = nrow;
     skip = nskip;
   }
 }
@@ -606,16 +709,17 @@ static void device_limits() {
 }
 
 template <typename TW>
-struct TmaLaunch {
+struct TeamLaunch {
   const PredParams &p; const SmemPlan &sp; int grid; cudaStream_t stream;
   template <int CPL> void operator()() const {
     static bool configured = false;
     if (!configured) {
-      cudaFuncSetAttribute(predictor_tma_kernel<TW, CPL>,
+      cudaFuncSetAttribute(predictor_team_kernel<TW, CPL>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_optin);
       configured = true;
     }
-    predictor_tma_kernel<TW, CPL><<<grid > 0 ? grid : 1, 32 * sp.nw, sp.bytes, stream>>>(p, sp);
+    predictor_team_kernel<TW, CPL><<<grid > 0 ? grid : 1, 32 * TEAM * sp.nt, sp.bytes, stream>>>(
+        p, sp);
   }
 };
 
@@ -630,11 +734,11 @@ static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cu
     predictor_strict_kernel<TW><<<(unsigned)a->B, STRICT_THREADS, smem, stream>>>(p);
   } else {
     if (((size_t)p.d * sizeof(TW)) % 16) return SPX_EINVAL;   // TMA bulk: 16-byte rows
-    SmemPlan sp = plan_smem<TW>(p.d, p.K, p.H, g_smem_optin, MAXW);
-    if (sp.nw == 0) return SPX_EINVAL;
-    const long long need = (a->B + sp.nw - 1) / sp.nw;
+    SmemPlan sp = plan_smem<TW>(p.d, p.K, p.H, g_smem_optin);
+    if (sp.nt == 0) return SPX_EINVAL;
+    const long long need = (a->B + sp.nt - 1) / sp.nt;
     const int grid = (int)(need < g_sms ? need : g_sms);
-    if (!dispatch_cpl(p.d, TmaLaunch<TW>{p, sp, grid, stream})) return SPX_EINVAL;
+    if (!dispatch_cpl(p.d, TeamLaunch<TW>{p, sp, grid, stream})) return SPX_EINVAL;
   }
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
 }
@@ -653,7 +757,7 @@ extern "C" int spx_predictor_eval(const spx_predictor_args *a, void *stream_) {
   PredParams p;
   p.hidden = a->hidden; p.hidden_stride = a->hidden_stride ? a->hidden_stride : a->d;
   p.norm_g = a->norm_g; p.norm_b = a->norm_b;
-  p.head = a->head;
+  p.head = a->head; p.head_bw = a->head_bw;
   p.ids = a->ids; p.prev = a->prev;
   p.w1 = a->w1; p.b1 = a->b1; p.w2 = a->w2; p.b2 = a->b2; p.z_cut = a->z_cut;
   p.policy = a->policy; p.const_prob = a->const_prob; p.threshold = a->threshold;

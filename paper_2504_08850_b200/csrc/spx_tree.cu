@@ -20,9 +20,10 @@ constexpr int TREE_THREADS = 128;
 
 template <typename TW, int CPL>
 __global__ void __launch_bounds__(TREE_THREADS)
-tree_merged_kernel(const float *hn, int N, const TW *head, int V, int d,
-                   const int32_t *uniq, int U, const int32_t *uniq_ptr, const int32_t *pair_node,
-                   const int32_t *pair_out, float *logits, int strict, int *err) {
+tree_merged_kernel(const float *hn, const float *rr, int N, const TW *head, const float *bwv,
+                   int V, int d, const int32_t *uniq, int U, const int32_t *uniq_ptr,
+                   const int32_t *pair_node, const int32_t *pair_out, float *logits, int strict,
+                   int *err) {
   const int lane = threadIdx.x & 31;
   const int u = blockIdx.x * (TREE_THREADS / 32) + (threadIdx.x >> 5);
   if (u >= U) return;
@@ -56,6 +57,7 @@ tree_merged_kernel(const float *hn, int N, const TW *head, int V, int d,
       if (c < nchunk) w[g][s].load(wrow + CHUNK * c);
       else w[g][s].zero();
     }
+  const float bw = bwv ? bwv[id] : 0.f;
   for (int q = uniq_ptr[u]; q < uniq_ptr[u + 1]; ++q) {
     const float *h = hn + (size_t)pair_node[q] * d;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -78,18 +80,18 @@ tree_merged_kernel(const float *hn, int N, const TW *head, int V, int d,
 #pragma unroll
     for (int g = 0; g < 4; ++g) gs[g] = warp_butterfly_sum(acc[g]);
     const float lg = canon_combine(gs[0], gs[1], gs[2], gs[3]);
-    if (lane == 0) logits[pair_out[q]] = lg;
+    if (lane == 0) logits[pair_out[q]] = __fadd_rn(__fmul_rn(rr[pair_node[q]], lg), bw);
   }
 }
 
 template <typename TW>
 struct TreeLaunch {
-  const float *hn; int N; const TW *head; int V, d;
+  const float *hn, *rr; int N; const TW *head; const float *bw; int V, d;
   const int32_t *uniq; int U; const int32_t *uniq_ptr, *pair_node, *pair_out;
   float *logits; int strict; int *err; unsigned grid; cudaStream_t stream;
   template <int CPL> void operator()() const {
     tree_merged_kernel<TW, CPL><<<grid, TREE_THREADS, 0, stream>>>(
-        hn, N, head, V, d, uniq, U, uniq_ptr, pair_node, pair_out, logits, strict, err);
+        hn, rr, N, head, bw, V, d, uniq, U, uniq_ptr, pair_node, pair_out, logits, strict, err);
   }
 };
 
@@ -97,13 +99,14 @@ struct TreeLaunch {
 
 using namespace spx;
 
-extern "C" int spx_tree_merged_logits(const float *hn, int64_t N, const void *head,
-                                      int32_t head_dtype, int64_t V, int64_t d,
-                                      const int32_t *uniq, int64_t U, const int32_t *uniq_ptr,
-                                      const int32_t *pair_node, const int32_t *pair_out,
-                                      float *logits, int32_t mode, int32_t *err, void *stream_) {
+extern "C" int spx_tree_merged_logits(const float *xg, const float *r, int64_t N, const void *head,
+                                      int32_t head_dtype, const float *head_bw, int64_t V,
+                                      int64_t d, const int32_t *uniq, int64_t U,
+                                      const int32_t *uniq_ptr, const int32_t *pair_node,
+                                      const int32_t *pair_out, float *logits, int32_t mode,
+                                      int32_t *err, void *stream_) {
   cudaStream_t stream = (cudaStream_t)stream_;
-  if (!hn || !head || !uniq || !uniq_ptr || !pair_node || !pair_out || !logits || !err ||
+  if (!xg || !r || !head || !uniq || !uniq_ptr || !pair_node || !pair_out || !logits || !err ||
       N < 0 || U < 0 || d <= 0 || d % CHUNK || V <= 0)
     return SPX_EINVAL;
   if (U == 0) return 0;
@@ -112,14 +115,14 @@ extern "C" int spx_tree_merged_logits(const float *hn, int64_t N, const void *he
   const int strict = mode == SPX_MODE_STRICT;
   bool ok;
   if (head_dtype == SPX_DTYPE_F32)
-    ok = dispatch_cpl((int)d, TreeLaunch<float>{hn, (int)N, (const float *)head, (int)V, (int)d,
-                                                uniq, (int)U, uniq_ptr, pair_node, pair_out,
-                                                logits, strict, err, grid, stream});
+    ok = dispatch_cpl((int)d, TreeLaunch<float>{xg, r, (int)N, (const float *)head, head_bw,
+                                                (int)V, (int)d, uniq, (int)U, uniq_ptr, pair_node,
+                                                pair_out, logits, strict, err, grid, stream});
   else if (head_dtype == SPX_DTYPE_BF16)
     ok = dispatch_cpl((int)d, TreeLaunch<__nv_bfloat16>{
-                                  hn, (int)N, (const __nv_bfloat16 *)head, (int)V, (int)d, uniq,
-                                  (int)U, uniq_ptr, pair_node, pair_out, logits, strict, err,
-                                  grid, stream});
+                                  xg, r, (int)N, (const __nv_bfloat16 *)head, head_bw, (int)V,
+                                  (int)d, uniq, (int)U, uniq_ptr, pair_node, pair_out, logits,
+                                  strict, err, grid, stream});
   else
     return SPX_EINVAL;
   if (!ok) return SPX_EINVAL;

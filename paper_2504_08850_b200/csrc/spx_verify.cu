@@ -25,6 +25,7 @@ struct VerParams {
   const float *hidden; int64_t hidden_stride;
   const float *g, *b;
   const void *head;
+  const float *head_bw;
   const uint8_t *gate, *row_done;
   const int32_t *spec_ptr, *spec_ids;
   int32_t *token_out; uint8_t *verified_out; float *maxlogit_out, *logits_out;
@@ -41,25 +42,31 @@ __device__ __forceinline__ bool ver_row_on(const VerParams &p, int r) {
   return true;
 }
 
-// Canonical LayerNorm of one row into smem `hn` by one warp (FAST: the CDOT
-// statistics + reciprocal scaling, identical bits to the predictor kernel) or
-// one thread (STRICT: the reference's sequential sums and division).
+// Head-side normalisation of one row into `hn` (shared or global) by one warp.
+// FAST: hn = xg = (x - mean) * g with the canonical statistics and *r_out =
+// 1/sqrt(var + eps) -- the folded form logit = r * CDOT(xg, W) + bw used by
+// every fast head kernel (identical bits to the predictor kernel).  STRICT:
+// the reference LayerNorm (sequential sums, division; model.py:140-146),
+// *r_out = 1.  `layer_norm_out` (FAST only) writes the plain LayerNorm value
+// (xg * r + b) instead, for the function-level layer_norm.
 template <int CPL>
-__device__ void warp_layernorm(const VerParams &p, int r, float *hn, int lane, bool strict,
-                               int *bad) {
-  const float *x = p.hidden + (size_t)r * p.hidden_stride;
-  const int d = p.d;
+__device__ void warp_head_prep(const float *x, const float *g, const float *b, int d, float *hn,
+                               int lane, bool strict, float *r_out, int *bad,
+                               bool layer_norm_out = false) {
   const float df = (float)d;
   for (int j = lane; j < d; j += 32) hn[j] = x[j];
   __syncwarp();
   if (!strict) {
     float mean, denom;
-    bool b;
-    warp_ln_stats<CPL>(hn, d, lane, mean, denom, b);
-    if (b) *bad = 1;
-    const float rinv = __frcp_rn(denom);
-    for (int j = lane; j < d; j += 32)
-      hn[j] = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(hn[j], mean), rinv), p.g[j]), p.b[j]);
+    bool bb;
+    warp_ln_stats<CPL>(hn, d, lane, mean, denom, bb);
+    if (bb) *bad = 1;
+    const float r = __frcp_rn(denom);
+    for (int j = lane; j < d; j += 32) {
+      const float xg = __fmul_rn(__fsub_rn(hn[j], mean), g[j]);
+      hn[j] = layer_norm_out ? __fadd_rn(__fmul_rn(xg, r), b[j]) : xg;
+    }
+    *r_out = r;
   } else {
     float m = 0.f, v = 0.f;
     bool fin = true;
@@ -76,7 +83,8 @@ __device__ void warp_layernorm(const VerParams &p, int r, float *hn, int lane, b
     const float mean = __shfl_sync(0xffffffffu, m, 0);
     const float denom = __shfl_sync(0xffffffffu, v, 0);
     __syncwarp();
-    for (int j = lane; j < d; j += 32) hn[j] = ln_elem(__fsub_rn(hn[j], mean), denom, p.g[j], p.b[j]);
+    for (int j = lane; j < d; j += 32) hn[j] = ln_elem(__fsub_rn(hn[j], mean), denom, g[j], b[j]);
+    *r_out = 1.0f;
   }
   __syncwarp();
 }
@@ -137,6 +145,7 @@ verify_kernel(VerParams p) {
   extern __shared__ float hn[];           // VER_ROWS * d
   __shared__ int s_rows[VER_ROWS];
   __shared__ int s_nr, s_bad;
+  __shared__ float s_r[VER_ROWS];
   __shared__ unsigned long long s_best[VER_THREADS / 32][VER_ROWS];
   __shared__ bool s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = VER_THREADS / 32;
@@ -160,7 +169,10 @@ verify_kernel(VerParams p) {
     if (nr == 0) break;
     if (warp < nr) {
       int bad = 0;
-      warp_layernorm<CPL>(p, s_rows[warp], hn + (size_t)warp * p.d, lane, strict, &bad);
+      float rr = 1.f;
+      warp_head_prep<CPL>(p.hidden + (size_t)s_rows[warp] * p.hidden_stride, p.g, p.b, p.d,
+                          hn + (size_t)warp * p.d, lane, strict, &rr, &bad);
+      if (lane == 0) s_r[warp] = rr;
       if (bad && lane == 0) { atomicOr(p.err, ERR_HIDDEN_NONFINITE); s_bad = 1; }
     }
     __syncthreads();
@@ -169,11 +181,16 @@ verify_kernel(VerParams p) {
     for (int r = 0; r < VER_ROWS; ++r) best[r] = 0ull;
     const int gw = blockIdx.x * nwarps + warp, tw = gridDim.x * nwarps;
     if (!strict) {
+      float rs[VER_ROWS];
+#pragma unroll
+      for (int r = 0; r < VER_ROWS; ++r) rs[r] = s_r[r];
       for (int v = gw; v < p.V; v += tw) {
         float lg[VER_ROWS];
         warp_cdot<TW, VER_ROWS, CPL>(head + (size_t)v * p.d, hn, p.d, nr, lane, lg);
+        const float bw = p.head_bw ? p.head_bw[v] : 0.f;
 #pragma unroll
         for (int r = 0; r < VER_ROWS; ++r) {
+          lg[r] = __fadd_rn(__fmul_rn(rs[r], lg[r]), bw);
           if (r < nr) {
             const unsigned long long k = argmax_key(lg[r], (uint32_t)v);
             best[r] = k > best[r] ? k : best[r];
@@ -254,16 +271,49 @@ verify_kernel(VerParams p) {
 // Final LayerNorm of N rows into hn (FAST: canonical, STRICT: sequential).
 template <int CPL>
 __global__ void final_norm_kernel(const float *x, int64_t stride, const float *g, const float *b,
-                                  float *hn, int N, int d, int mode, int *err) {
+                                  float *hn, float *r_out, int N, int d, int mode,
+                                  int layer_norm_out, int *err) {
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (row >= N) return;
-  VerParams p;
-  p.hidden = x; p.hidden_stride = stride; p.g = g; p.b = b; p.d = d;
   int bad = 0;
-  warp_layernorm<CPL>(p, row, hn + (size_t)row * d, lane, mode == SPX_MODE_STRICT, &bad);
+  float r = 1.f;
+  warp_head_prep<CPL>(x + (size_t)row * stride, g, b, d, hn + (size_t)row * d, lane,
+                      mode == SPX_MODE_STRICT, &r, &bad, layer_norm_out != 0);
+  if (lane == 0 && r_out) r_out[row] = r;
   if (bad && lane == 0) atomicOr(err, ERR_HIDDEN_NONFINITE);
 }
+
+// bw[v] = CDOT(b, head_v), one warp per vocab row.
+template <typename TW, int CPL>
+__global__ void head_bias_kernel(const TW *head, const float *b, int V, int d, float *bw) {
+  extern __shared__ float bs[];
+  for (int j = threadIdx.x; j < d; j += blockDim.x) bs[j] = b[j];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int nw = blockDim.x / 32;
+  for (int v = blockIdx.x * nw + (threadIdx.x >> 5); v < V; v += gridDim.x * nw) {
+    float out[1];
+    warp_cdot<TW, 1, CPL>(head + (size_t)v * d, bs, d, 1, lane, out);
+    if (lane == 0) bw[v] = out[0];
+  }
+}
+
+struct NormLaunch {
+  const float *x; int64_t st; const float *g, *b; float *hn, *r; int N, d, mode, lno; int *err;
+  unsigned grid; int threads; cudaStream_t stream;
+  template <int CPL> void operator()() const {
+    final_norm_kernel<CPL><<<grid, threads, 0, stream>>>(x, st, g, b, hn, r, N, d, mode, lno, err);
+  }
+};
+
+template <typename TW>
+struct BiasLaunch {
+  const TW *head; const float *b; int V, d; float *bw; cudaStream_t stream;
+  template <int CPL> void operator()() const {
+    head_bias_kernel<TW, CPL><<<592, 256, (size_t)d * 4, stream>>>(head, b, V, d, bw);
+  }
+};
 
 }  // namespace spx
 
@@ -309,7 +359,7 @@ extern "C" int spx_verify(const spx_verify_args *a, void *stream_) {
   VerParams p;
   p.hidden = a->hidden; p.hidden_stride = a->hidden_stride ? a->hidden_stride : a->d;
   p.g = a->norm_g; p.b = a->norm_b;
-  p.head = a->head;
+  p.head = a->head; p.head_bw = a->head_bw;
   p.gate = a->gate; p.row_done = a->row_done; p.spec_ptr = a->spec_ptr; p.spec_ids = a->spec_ids;
   p.token_out = a->token_out; p.verified_out = a->verified_out; p.maxlogit_out = a->maxlogit_out;
   p.logits_out = a->logits_out; p.done_out = a->done_out; p.exit_layer_out = a->exit_layer_out;
@@ -337,18 +387,40 @@ extern "C" int spx_final_norm(const float *hidden, int64_t hidden_stride, const 
   const int wpc = 4;
   const unsigned grid = (unsigned)((N + wpc - 1) / wpc);
   const int64_t st = hidden_stride ? hidden_stride : d;
+  if (!dispatch_cpl((int)d, NormLaunch{hidden, st, g, b, hn, nullptr, (int)N, (int)d, mode, 1,
+                                       err, grid, wpc * 32, stream}))
+    return SPX_EINVAL;
+  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+}
+
+extern "C" int spx_head_prep(const float *hidden, int64_t hidden_stride, const float *g,
+                             const float *b, float *xg, float *r, int64_t N, int64_t d,
+                             int32_t mode, int32_t *err, void *stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!hidden || !g || !b || !xg || !r || !err || N < 0 || d <= 0 || d % CHUNK) return SPX_EINVAL;
+  if (N == 0) return 0;
+  const int wpc = 4;
+  const unsigned grid = (unsigned)((N + wpc - 1) / wpc);
+  const int64_t st = hidden_stride ? hidden_stride : d;
+  if (!dispatch_cpl((int)d, NormLaunch{hidden, st, g, b, xg, r, (int)N, (int)d, mode, 0, err,
+                                       grid, wpc * 32, stream}))
+    return SPX_EINVAL;
+  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+}
+
+extern "C" int spx_head_bias(const void *head, int32_t head_dtype, const float *b, int64_t V,
+                             int64_t d, float *bw, void *stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (!head || !b || !bw || V <= 0 || d <= 0 || d % CHUNK) return SPX_EINVAL;
+  if ((size_t)d * 4 > 48 * 1024) return SPX_EINVAL;
   bool ok;
-  switch (((int)d / CHUNK + NPART - 1) / NPART) {
-    case 1: final_norm_kernel<1><<<grid, wpc * 32, 0, stream>>>(hidden, st, g, b, hn, (int)N, (int)d, mode, err); ok = true; break;
-    case 2: final_norm_kernel<2><<<grid, wpc * 32, 0, stream>>>(hidden, st, g, b, hn, (int)N, (int)d, mode, err); ok = true; break;
-    case 3: case 4: final_norm_kernel<4><<<grid, wpc * 32, 0, stream>>>(hidden, st, g, b, hn, (int)N, (int)d, mode, err); ok = true; break;
-    case 5: case 6: case 7: case 8: final_norm_kernel<8><<<grid, wpc * 32, 0, stream>>>(hidden, st, g, b, hn, (int)N, (int)d, mode, err); ok = true; break;
-    default:
-      if (d / CHUNK <= 16 * NPART) {
-        final_norm_kernel<16><<<grid, wpc * 32, 0, stream>>>(hidden, st, g, b, hn, (int)N, (int)d, mode, err);
-        ok = true;
-      } else ok = false;
-  }
+  if (head_dtype == SPX_DTYPE_BF16)
+    ok = dispatch_cpl((int)d, BiasLaunch<__nv_bfloat16>{(const __nv_bfloat16 *)head, b, (int)V,
+                                                        (int)d, bw, stream});
+  else if (head_dtype == SPX_DTYPE_F32)
+    ok = dispatch_cpl((int)d, BiasLaunch<float>{(const float *)head, b, (int)V, (int)d, bw, stream});
+  else
+    return SPX_EINVAL;
   if (!ok) return SPX_EINVAL;
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
 }

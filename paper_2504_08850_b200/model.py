@@ -153,6 +153,16 @@ class TransformerModel:
             t = t[part * d:(part + 1) * d]
         return t, True
 
+    def finalize(self):
+        """Derived per-model constants once the weights are in place: the
+        final-norm bias folded through the head, bw[v] = CDOT(b, head_v), used
+        by the fast head kernels (logit = r * CDOT(xg, head_v) + bw[v])."""
+        self.head_bw = torch.empty(self.config.vocab_size, dtype=torch.float32, device="cuda")
+        N.check(N.lib().spx_head_bias(N.ptr(self.lm_head), self.spx_dtype, N.ptr(self.final_b),
+                                      self.config.vocab_size, self.config.hidden_dim,
+                                      N.ptr(self.head_bw), N.stream_ptr()), "spx_head_bias")
+        return self
+
     def numel(self):
         n = self.lm_head.numel() + 2 * self.config.hidden_dim
         if not self.head_only:
@@ -184,6 +194,7 @@ def init_model(config: ModelConfig, dtype: str = "bf16", head_only: bool = False
         N.check(L.spx_init_uniform(N.ptr(t), int(is_f32), shape[0], shape[1], int(transpose),
                                    rng.derive(config.seed, idx), -b, b, N.stream_ptr()),
                 "spx_init_uniform")
+    m.finalize()
     return m
 
 
@@ -211,6 +222,7 @@ def from_tensors(config: ModelConfig, tensors: dict, dtype: str = "f32",
         if transpose:
             src = src.t()
         dst.copy_(src.to(dst.dtype))
+    m.finalize()
     return m
 
 
@@ -280,8 +292,24 @@ def final_norm(model: TransformerModel, hidden) -> torch.Tensor:
     return out
 
 
-def merged_logits(model: TransformerModel, hn: torch.Tensor, id_lists) -> list:
-    """K6: logits of node j for id_lists[j], one HBM read per unique id."""
+def head_prep(model: TransformerModel, hidden):
+    """(xg, r) of (N, d) rows for the fast head kernels (spx_head_prep); in
+    strict mode xg is the reference LayerNorm and r = 1."""
+    h = _rows(hidden, model.config.hidden_dim)
+    xg = torch.empty_like(h)
+    r = torch.empty(h.shape[0], dtype=torch.float32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.check(N.lib().spx_head_prep(N.ptr(h), h.shape[1], N.ptr(model.final_g), N.ptr(model.final_b),
+                                  N.ptr(xg), N.ptr(r), h.shape[0], h.shape[1], numerics.mode(),
+                                  N.ptr(err), N.stream_ptr()), "spx_head_prep")
+    N.raise_device_error(err.item())
+    return xg, r
+
+
+def merged_logits(model: TransformerModel, prep, id_lists) -> list:
+    """K6: logits of node j for id_lists[j], one HBM read per unique id.
+    prep = head_prep(model, rows)."""
+    xg, rr = prep
     flat = np.concatenate([np.asarray(ids, np.int64).reshape(-1) for ids in id_lists])
     sizes = [len(ids) for ids in id_lists]
     node = np.repeat(np.arange(len(id_lists), dtype=np.int64), sizes)
@@ -297,8 +325,9 @@ def merged_logits(model: TransformerModel, hn: torch.Tensor, id_lists) -> list:
     d_node, d_out = dev(node[order]), dev(out_idx[order])
     logits = torch.empty(flat.size, dtype=torch.float32, device="cuda")
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
-    N.check(N.lib().spx_tree_merged_logits(N.ptr(hn), hn.shape[0], N.ptr(model.lm_head),
-                                           model.spx_dtype, model.config.vocab_size,
+    N.check(N.lib().spx_tree_merged_logits(N.ptr(xg), N.ptr(rr), xg.shape[0], N.ptr(model.lm_head),
+                                           model.spx_dtype, N.ptr(model.head_bw),
+                                           model.config.vocab_size,
                                            model.config.hidden_dim, N.ptr(d_uniq), uniq.size,
                                            N.ptr(d_uptr), N.ptr(d_node), N.ptr(d_out),
                                            N.ptr(logits), numerics.mode(), N.ptr(err),
@@ -316,8 +345,7 @@ def sliced_head_logits(model: TransformerModel, hidden, token_ids) -> torch.Tens
         raise ValueError("empty token id list")
     if ids.min() < 0 or ids.max() >= model.config.vocab_size:
         raise ValueError("token id out of range")
-    hn = final_norm(model, hidden)
-    return merged_logits(model, hn, [ids])[0]
+    return merged_logits(model, head_prep(model, hidden), [ids])[0]
 
 
 class _VerifyScratch:
@@ -347,7 +375,7 @@ def head_argmax(model: TransformerModel, hidden, spec_lists=None, want_logits=Fa
     a = N.VerifyArgs()
     a.hidden, a.hidden_stride = N.ptr(h), h.shape[1]
     a.norm_g, a.norm_b = N.ptr(model.final_g), N.ptr(model.final_b)
-    a.head, a.head_dtype = N.ptr(model.lm_head), model.spx_dtype
+    a.head, a.head_dtype, a.head_bw = N.ptr(model.lm_head), model.spx_dtype, N.ptr(model.head_bw)
     keep = []
     if spec_lists is not None:
         ptr_ = np.concatenate([[0], np.cumsum([len(s) for s in spec_lists])]).astype(np.int32)

@@ -317,7 +317,7 @@ def evaluate_batch(model, weights, hidden, ids, prev, threshold=0.5, layer=0, ou
     a = N.PredictorArgs()
     a.hidden, a.hidden_stride = N.ptr(hidden), hidden.stride(0)
     a.norm_g, a.norm_b = N.ptr(model.final_g), N.ptr(model.final_b)
-    a.head, a.head_dtype = N.ptr(model.lm_head), model.spx_dtype
+    a.head, a.head_dtype, a.head_bw = N.ptr(model.lm_head), model.spx_dtype, N.ptr(model.head_bw)
     a.ids, a.prev = N.ptr(ids), N.ptr(prev)
     if policy is None:
         if isinstance(weights, PredictorBank):

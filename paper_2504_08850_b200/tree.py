@@ -10,7 +10,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .model import TransformerModel, final_norm, merged_logits
+from .model import TransformerModel, head_prep, merged_logits
 from .predictor import decide_exit
 
 
@@ -29,8 +29,7 @@ def grouped_speculative_logits(model: TransformerModel, hiddens, token_id_lists)
             raise ValueError("empty token id list")
         if min(ids) < 0 or max(ids) >= v:
             raise ValueError("token id out of range")
-    hn = final_norm(model, h)
-    return merged_logits(model, hn, token_id_lists)
+    return merged_logits(model, head_prep(model, h), token_id_lists)
 
 
 def hypertoken_exit_decision(per_node_probs, threshold: float) -> bool:
