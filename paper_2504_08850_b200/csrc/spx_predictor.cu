@@ -144,7 +144,13 @@ __device__ __forceinline__ float z1_unit(const float *feats, const float *w1, in
 // i.e. NU*4 independent FMA chains per lane with 16-byte conflict-free W1
 // reads.  NU = 4, u0 = 0: one warp does all units; NU = 1, u0 = w: warp w of
 // a 4-warp team does a quarter.  Per-unit arithmetic is identical.
-template <int NU>
+template <bool G>
+__device__ __forceinline__ float4 ld_w1(const float *p) {
+  if (G) return __ldg(reinterpret_cast<const float4 *>(p));
+  return *reinterpret_cast<const float4 *>(p);
+}
+
+template <int NU, bool W1G = false>
 __device__ void mlp_z1(const float *feats, const float *w1, const float *b1, int n, int H,
                        float *hs, int lane, int u0) {
   if ((H % 4) == 0) {
@@ -162,7 +168,7 @@ __device__ void mlp_z1(const float *feats, const float *w1, const float *b1, int
           for (int u = 0; u < NU; ++u) {
             const int j0 = jb + 4 * lane + 128 * (u0 + u);
             if (j0 < H) {
-              const float4 w = *reinterpret_cast<const float4 *>(w1 + (size_t)i * H + j0);
+              const float4 w = ld_w1<W1G>(w1 + (size_t)i * H + j0);
               y[u][0] = __fmaf_rn(f, w.x, y[u][0]); y[u][1] = __fmaf_rn(f, w.y, y[u][1]);
               y[u][2] = __fmaf_rn(f, w.z, y[u][2]); y[u][3] = __fmaf_rn(f, w.w, y[u][3]);
             }
@@ -185,7 +191,7 @@ __device__ void mlp_z1(const float *feats, const float *w1, const float *b1, int
               for (int u = 0; u < NU; ++u) {
                 const int j0 = jb + 4 * lane + 128 * (u0 + u);
                 if (j0 < H) {
-                  const float4 w = *reinterpret_cast<const float4 *>(w1 + (size_t)(i + q) * H + j0);
+                  const float4 w = ld_w1<W1G>(w1 + (size_t)(i + q) * H + j0);
                   t[u][0] = __fmaf_rn(f, w.x, t[u][0]); t[u][1] = __fmaf_rn(f, w.y, t[u][1]);
                   t[u][2] = __fmaf_rn(f, w.z, t[u][2]); t[u][3] = __fmaf_rn(f, w.w, t[u][3]);
                 }
@@ -364,7 +370,7 @@ __device__ __forceinline__ void team_sync(int team) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(32 * TEAM) : "memory");
 }
 
-template <typename TW, int CPL>
+template <typename TW, int CPL, bool FULL>
 __global__ void __launch_bounds__(32 * TEAM * MAXT)
 predictor_team_kernel(PredParams p, SmemPlan sp) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -452,26 +458,37 @@ predictor_team_kernel(PredParams p, SmemPlan sp) {
     phase ^= 1u;
     // ---- pass 1: mean (this warp = canonical group w)
     float part = 0.f;
-    bool fin = true;
 #pragma unroll
     for (int s = 0; s < CPL; ++s) {
       const int c = 32 * w + lane + NPART * s;
-      if (c < nchunk) {
+      if (FULL || c < nchunk) {
         const float4 v = *reinterpret_cast<const float4 *>(sh + CHUNK * c);
         part = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(part, v.x), v.y), v.z), v.w);
-        fin &= is_finite(v.x) & is_finite(v.y) & is_finite(v.z) & is_finite(v.w);
       }
     }
     part = warp_butterfly_sum(part);
-    const bool wbad = __any_sync(0xffffffffu, !fin);
-    if (lane == 0) { red[GROUP * 4 + w] = part; tflag[w] = wbad ? 1 : 0; }
+    if (lane == 0) red[GROUP * 4 + w] = part;
     team_sync(team);
-    const float mean = __fdiv_rn(canon_combine(red[GROUP * 4 + 0], red[GROUP * 4 + 1],
-                                               red[GROUP * 4 + 2], red[GROUP * 4 + 3]),
-                                 (float)d);
-    const bool hbad = (tflag[0] | tflag[1] | tflag[2] | tflag[3]) != 0;
+    const float total = canon_combine(red[GROUP * 4 + 0], red[GROUP * 4 + 1], red[GROUP * 4 + 2],
+                                      red[GROUP * 4 + 3]);
+    const float mean = __fdiv_rn(total, (float)d);
+    bool hbad = false;
+    if (!is_finite(total)) {            // rare: exact element scan (model.py:310-311)
+      bool fin = true;
+      for (int c = 32 * w + lane; c < nchunk; c += NPART) {
+        const float4 v = *reinterpret_cast<const float4 *>(sh + CHUNK * c);
+        fin &= is_finite(v.x) & is_finite(v.y) & is_finite(v.z) & is_finite(v.w);
+      }
+      const bool wbad = __any_sync(0xffffffffu, !fin);
+      if (lane == 0) tflag[w] = wbad ? 1 : 0;
+      team_sync(team);
+      hbad = (tflag[0] | tflag[1] | tflag[2] | tflag[3]) != 0;
+      team_sync(team);
+    }
     float r = 0.f;
-    // ---- pass 2 (per id group): variance (first group) + the K dots
+    const float2 nmean = make_float2(-mean, -mean);
+    // ---- pass 2 (per id group): variance (first group) + GROUP dots, packed
+    // FP32 (FADD2/FMUL2/FFMA2) with per-chain order identical to CDOT.
     for (int c0 = 0; c0 < K; c0 += GROUP) {
       const int ng = (K - c0) < GROUP ? (K - c0) : GROUP;
       if (c0 > 0) {
@@ -480,36 +497,40 @@ predictor_team_kernel(PredParams p, SmemPlan sp) {
         mbar_wait(bar, phase);
         phase ^= 1u;
       }
-      float acc[GROUP] = {0.f, 0.f, 0.f, 0.f};
+      float2 acc01 = make_float2(0.f, 0.f), acc23 = make_float2(0.f, 0.f);
       float sq = 0.f;
 #pragma unroll
       for (int s = 0; s < CPL; ++s) {
         const int c = 32 * w + lane + NPART * s;
-        if (c < nchunk) {
+        if (FULL || c < nchunk) {
           const float4 xv = *reinterpret_cast<const float4 *>(sh + CHUNK * c);
           const float4 gv = *reinterpret_cast<const float4 *>(gs + CHUNK * c);
-          const float xc[4] = {__fsub_rn(xv.x, mean), __fsub_rn(xv.y, mean),
-                               __fsub_rn(xv.z, mean), __fsub_rn(xv.w, mean)};
-          sq = __fmaf_rn(xc[3], xc[3], __fmaf_rn(xc[2], xc[2],
-                         __fmaf_rn(xc[1], xc[1], __fmaf_rn(xc[0], xc[0], sq))));
-          const float xg[4] = {__fmul_rn(xc[0], gv.x), __fmul_rn(xc[1], gv.y),
-                               __fmul_rn(xc[2], gv.z), __fmul_rn(xc[3], gv.w)};
+          const float2 xc01 = fadd2(make_float2(xv.x, xv.y), nmean);
+          const float2 xc23 = fadd2(make_float2(xv.z, xv.w), nmean);
+          if (c0 == 0)
+            sq = __fmaf_rn(xc23.y, xc23.y, __fmaf_rn(xc23.x, xc23.x,
+                           __fmaf_rn(xc01.y, xc01.y, __fmaf_rn(xc01.x, xc01.x, sq))));
+          const float2 xg01 = fmul2(xc01, make_float2(gv.x, gv.y));
+          const float2 xg23 = fmul2(xc23, make_float2(gv.z, gv.w));
+          float wv[GROUP][4];
 #pragma unroll
           for (int q = 0; q < GROUP; ++q) {
-            if (q < ng) {
-              Chunk<TW> ch;
-              ch.lds(sw + (size_t)q * d + CHUNK * c);
-              float wf[4];
-              ch.to_f32(wf);
+            Chunk<TW> ch;
+            ch.lds(sw + (size_t)q * d + CHUNK * c);
+            ch.to_f32(wv[q]);
+          }
+          const float xe[4] = {xg01.x, xg01.y, xg23.x, xg23.y};
 #pragma unroll
-              for (int e = 0; e < CHUNK; ++e) acc[q] = __fmaf_rn(xg[e], wf[e], acc[q]);
-            }
+          for (int e = 0; e < CHUNK; ++e) {
+            const float2 xx = make_float2(xe[e], xe[e]);
+            acc01 = ffma2(xx, make_float2(wv[0][e], wv[1][e]), acc01);
+            acc23 = ffma2(xx, make_float2(wv[2][e], wv[3][e]), acc23);
           }
         }
       }
+      float acc[GROUP] = {acc01.x, acc01.y, acc23.x, acc23.y};
 #pragma unroll
-      for (int q = 0; q < GROUP; ++q)
-        if (q < ng) acc[q] = warp_butterfly_sum(acc[q]);
+      for (int q = 0; q < GROUP; ++q) acc[q] = warp_butterfly_sum(acc[q]);
       if (c0 == 0) sq = warp_butterfly_sum(sq);
       if (lane == 0) {
 #pragma unroll
@@ -528,7 +549,7 @@ predictor_team_kernel(PredParams p, SmemPlan sp) {
         int id = p.ids[(size_t)row * K + c0 + q];
         id = (id < 0 || id >= p.V) ? 0 : id;
         const float dot = canon_combine(red[q * 4 + 0], red[q * 4 + 1], red[q * 4 + 2], red[q * 4 + 3]);
-        feats[c0 + q] = __fadd_rn(__fmul_rn(r, dot), p.head_bw ? p.head_bw[id] : 0.f);
+        feats[c0 + q] = __fadd_rn(__fmul_rn(r, dot), p.head_bw ? __ldg(p.head_bw + id) : 0.f);
       }
     }
     const int ibad = __shfl_sync(0xffffffffu, id_bad, 0);   // leader's lane is lane 0 of w0
@@ -564,7 +585,8 @@ predictor_team_kernel(PredParams p, SmemPlan sp) {
     const int ok = tflag[0];
     if (ok) {
       if (mlp) {
-        mlp_z1<1>(feats, w1, b1s, 3 * K, H, hs, lane, w);
+        if (sp.w1_smem) mlp_z1<1, false>(feats, w1, b1s, 3 * K, H, hs, lane, w);
+        else mlp_z1<1, true>(feats, w1, b1s, 3 * K, H, hs, lane, w);
         team_sync(team);
         if (w < 2) as[32 * w + lane] = z2_partial(hs, w2s, H, 32 * w + lane);
         team_sync(team);
@@ -712,14 +734,18 @@ template <typename TW>
 struct TeamLaunch {
   const PredParams &p; const SmemPlan &sp; int grid; cudaStream_t stream;
   template <int CPL> void operator()() const {
+    if (p.d == CHUNK * NPART * CPL) launch<CPL, true>();
+    else launch<CPL, false>();
+  }
+  template <int CPL, bool FULL> void launch() const {
     static bool configured = false;
     if (!configured) {
-      cudaFuncSetAttribute(predictor_team_kernel<TW, CPL>,
+      cudaFuncSetAttribute(predictor_team_kernel<TW, CPL, FULL>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_optin);
       configured = true;
     }
-    predictor_team_kernel<TW, CPL><<<grid > 0 ? grid : 1, 32 * TEAM * sp.nt, sp.bytes, stream>>>(
-        p, sp);
+    predictor_team_kernel<TW, CPL, FULL>
+        <<<grid > 0 ? grid : 1, 32 * TEAM * sp.nt, sp.bytes, stream>>>(p, sp);
   }
 };
 
