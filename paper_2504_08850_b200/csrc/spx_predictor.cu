@@ -32,6 +32,7 @@
 // reference's `prob > threshold`.
 #include "spx_common.cuh"
 #include "../../include/specexit_b200.h"
+#include <cstdlib>
 
 namespace spx {
 
@@ -60,6 +61,7 @@ struct PredParams {
   int32_t *evals;                  // (B) optional: += 1 per evaluated row
   int layer;
   int *err;
+  unsigned long long *trace;       // debug: per-row globaltimer stamps (8 per row)
   int B, d, V, K, H;
 };
 
@@ -311,304 +313,8 @@ __device__ void warp_row_tail(const PredParams &p, int row, float *feats, const 
   }
 }
 
-// ------------------------------------------------------------ FAST (TMA)
-// One 4-warp TEAM per row: warp w of the team owns canonical partial group
-// g = w (partials 32w..32w+31), so every per-row reduction is split four
-// ways; teams synchronise with their own named barrier.  Each team owns a
-// shared-memory stage (hidden row + GROUP LM-head rows) filled by 1-D TMA
-// bulk copies; the next row's copies are issued as soon as the current row's
-// dot products are done.  Fast-path algebra (canonical, shared with K4/K6):
-//   mean = CSUM(x)/d ; xc = x - mean ; var = CSUM(xc*xc)/d ; r = 1/sqrt(var+eps)
-//   logit_v = r * CDOT(xc*g, W_v) + bw_v      (bw_v = CDOT(b, W_v), per model)
-// i.e. the LayerNorm is folded into the head dot (one pass over the row for
-// the variance and all K dots).
-constexpr int TEAM = 4;
-constexpr int MAXT = 4;
-constexpr int RED_FLOATS = 32;    // (GROUP + 2) * 4 used
-
-struct SmemPlan {
-  int nt;          // teams (= row stages) per CTA
-  int w1_smem;     // W1 staged in shared memory?
-  size_t bytes;
-  size_t off_g, off_w2, off_b1, off_w1, off_team, team_bytes, scratch_bytes, off_bar;
-};
-
-template <typename TW>
-inline SmemPlan plan_smem(int d, int K, int H, int max_bytes) {
-  SmemPlan best{};
-  const size_t stage = (size_t)d * 4 + (size_t)GROUP * d * sizeof(TW);
-  const size_t scratch = ((size_t)(RED_FLOATS + 4 + 3 * MAXK + (H > 0 ? H : 4) + 64) * 4 + 127) /
-                         128 * 128;
-  const size_t per_team = scratch + (stage + 127) / 128 * 128;
-  const size_t w1b = ((size_t)3 * K * H * 4 + 127) / 128 * 128;
-  const size_t fixed0 = (((size_t)d + 2 * H) * 4 + 127) / 128 * 128;
-  for (int w1 = 0; w1 <= (H > 0 ? 1 : 0); ++w1) {
-    const size_t fixed = fixed0 + (w1 ? w1b : 0);
-    int nt = 0;
-    for (int t = MAXT; t >= 1; --t)
-      if (fixed + (size_t)t * per_team + (MAXT + 1) * 8 <= (size_t)max_bytes) { nt = t; break; }
-    if (nt > best.nt || (nt == best.nt && nt > 0 && w1)) {
-      SmemPlan s{};
-      s.nt = nt; s.w1_smem = w1;
-      size_t o = 0;
-      s.off_g = o; o += (size_t)d * 4;
-      s.off_w2 = o; o += (size_t)H * 4;
-      s.off_b1 = o; o += (size_t)H * 4;
-      o = (o + 127) / 128 * 128;
-      s.off_w1 = o; if (w1) o += w1b;
-      s.off_team = o; s.team_bytes = per_team; s.scratch_bytes = scratch;
-      o += (size_t)nt * per_team;
-      s.off_bar = o; o += (size_t)(nt + 1) * 8;
-      s.bytes = o;
-      best = s;
-    }
-  }
-  return best;
-}
-
-__device__ __forceinline__ void team_sync(int team) {
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(32 * TEAM) : "memory");
-}
-
-template <typename TW, int CPL, bool FULL>
-__global__ void __launch_bounds__(32 * TEAM * MAXT)
-predictor_team_kernel(PredParams p, SmemPlan sp) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int team = warp / TEAM, w = warp % TEAM, nt = sp.nt;
-  const int d = p.d, K = p.K, H = p.H, nchunk = d / CHUNK;
-  float *gs = reinterpret_cast<float *>(smem + sp.off_g);
-  float *w2s = reinterpret_cast<float *>(smem + sp.off_w2);
-  float *b1s = reinterpret_cast<float *>(smem + sp.off_b1);
-  float *w1s = reinterpret_cast<float *>(smem + sp.off_w1);
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem + sp.off_bar) + team;
-  uint64_t *setup_bar = reinterpret_cast<uint64_t *>(smem + sp.off_bar) + nt;
-  uint8_t *tbase = smem + sp.off_team + (size_t)team * sp.team_bytes;
-  float *red = reinterpret_cast<float *>(tbase);            // [GROUP+2][4]
-  int *tflag = reinterpret_cast<int *>(red + RED_FLOATS);   // [4]
-  float *feats = red + RED_FLOATS + 4;
-  float *hs = feats + 3 * MAXK;
-  float *as = hs + (H > 0 ? H : 4);
-  float *sh = reinterpret_cast<float *>(tbase + sp.scratch_bytes);
-  TW *sw = reinterpret_cast<TW *>(tbase + sp.scratch_bytes + (size_t)d * 4);
-  const TW *head = reinterpret_cast<const TW *>(p.head);
-
-  const bool mlp = p.policy == SPX_POLICY_MLP;
-  const bool bulk_consts = (H % 4) == 0;
-  if (w == 0 && lane == 0 && team < nt) mbar_init(bar, 1);
-  if (threadIdx.x == 0) mbar_init(setup_bar, 1);
-  fence_mbar_init();
-  __syncthreads();
-  if (threadIdx.x == 0) {            // per-CTA constants by TMA
-    uint32_t bytes = (uint32_t)d * 4u;
-    if (mlp && bulk_consts) bytes += 2u * H * 4u + (sp.w1_smem ? 3u * K * H * 4u : 0u);
-    mbar_arrive_expect_tx(setup_bar, bytes);
-    bulk_g2s(gs, p.norm_g, (uint32_t)d * 4u, setup_bar);
-    if (mlp && bulk_consts) {
-      bulk_g2s(w2s, p.w2, (uint32_t)H * 4u, setup_bar);
-      bulk_g2s(b1s, p.b1, (uint32_t)H * 4u, setup_bar);
-      if (sp.w1_smem) bulk_g2s(w1s, p.w1, 3u * K * H * 4u, setup_bar);
-    }
-  }
-  if (mlp && !bulk_consts) {
-    for (int i = threadIdx.x; i < H; i += blockDim.x) { w2s[i] = p.w2[i]; b1s[i] = p.b1[i]; }
-    if (sp.w1_smem)
-      for (int i = threadIdx.x; i < 3 * K * H; i += blockDim.x) w1s[i] = p.w1[i];
-    __syncthreads();
-  }
-  const float *w1 = sp.w1_smem ? w1s : p.w1;
-  const uint32_t wrow_bytes = (uint32_t)((size_t)d * sizeof(TW));
-  const bool leader = (w == 0 && lane == 0);
-
-  // leader: TMA copies for `row` (hidden row when with_hidden, W rows of ids
-  // [c0, c0+ng)); returns nonzero if an id was out of range (clamped to 0).
-  auto issue_group = [&](int row, int c0, int ng, bool with_hidden) -> int {
-    int bad = 0;
-    fence_proxy_async();
-    mbar_arrive_expect_tx(bar, (with_hidden ? (uint32_t)d * 4u : 0u) + (uint32_t)ng * wrow_bytes);
-    if (with_hidden)
-      bulk_g2s(sh, p.hidden + (size_t)row * p.hidden_stride, (uint32_t)d * 4u, bar);
-    for (int q = 0; q < ng; ++q) {
-      int id = p.ids[(size_t)row * K + c0 + q];
-      if (id < 0 || id >= p.V) { bad = 1; id = 0; }
-      bulk_g2s(sw + (size_t)q * d, head + (size_t)id * d, wrow_bytes, bar);
-    }
-    return bad;
-  };
-
-  const int stride = gridDim.x * nt;
-  int row = blockIdx.x * nt + team;
-  if (team >= nt) return;
-  uint32_t phase = 0;
-  int id_bad = 0;
-  bool skip = row >= p.B || row_skipped(p, row);
-  if (leader && !skip) id_bad = issue_group(row, 0, K < GROUP ? K : GROUP, true);
-  mbar_wait(setup_bar, 0);
-
-  while (row < p.B) {
-    const int next = row + stride;
-    if (skip) {
-      if (leader && p.fired) p.fired[row] = 0;
-      row = next;
-      skip = row >= p.B || row_skipped(p, row);
-      if (leader && !skip) id_bad = issue_group(row, 0, K < GROUP ? K : GROUP, true);
-      continue;
-    }
-    mbar_wait(bar, phase);
-    phase ^= 1u;
-    // ---- pass 1: mean (this warp = canonical group w)
-    float part = 0.f;
-#pragma unroll
-    for (int s = 0; s < CPL; ++s) {
-      const int c = 32 * w + lane + NPART * s;
-      if (FULL || c < nchunk) {
-        const float4 v = *reinterpret_cast<const float4 *>(sh + CHUNK * c);
-        part = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(part, v.x), v.y), v.z), v.w);
-      }
-    }
-    part = warp_butterfly_sum(part);
-    if (lane == 0) red[GROUP * 4 + w] = part;
-    team_sync(team);
-    const float total = canon_combine(red[GROUP * 4 + 0], red[GROUP * 4 + 1], red[GROUP * 4 + 2],
-                                      red[GROUP * 4 + 3]);
-    const float mean = __fdiv_rn(total, (float)d);
-    bool hbad = false;
-    if (!is_finite(total)) {            // rare: exact element scan (model.py:310-311)
-      bool fin = true;
-      for (int c = 32 * w + lane; c < nchunk; c += NPART) {
-        const float4 v = *reinterpret_cast<const float4 *>(sh + CHUNK * c);
-        fin &= is_finite(v.x) & is_finite(v.y) & is_finite(v.z) & is_finite(v.w);
-      }
-      const bool wbad = __any_sync(0xffffffffu, !fin);
-      if (lane == 0) tflag[w] = wbad ? 1 : 0;
-      team_sync(team);
-      hbad = (tflag[0] | tflag[1] | tflag[2] | tflag[3]) != 0;
-      team_sync(team);
-    }
-    float r = 0.f;
-    const float2 nmean = make_float2(-mean, -mean);
-    // ---- pass 2 (per id group): variance (first group) + GROUP dots, packed
-    // FP32 (FADD2/FMUL2/FFMA2) with per-chain order identical to CDOT.
-    for (int c0 = 0; c0 < K; c0 += GROUP) {
-      const int ng = (K - c0) < GROUP ? (K - c0) : GROUP;
-      if (c0 > 0) {
-        team_sync(team);                       // everyone done with the W stage / red
-        if (leader) id_bad |= issue_group(row, c0, ng, false);
-        mbar_wait(bar, phase);
-        phase ^= 1u;
-      }
-      float2 acc01 = make_float2(0.f, 0.f), acc23 = make_float2(0.f, 0.f);
-      float sq = 0.f;
-#pragma unroll
-      for (int s = 0; s < CPL; ++s) {
-        const int c = 32 * w + lane + NPART * s;
-        if (FULL || c < nchunk) {
-          const float4 xv = *reinterpret_cast<const float4 *>(sh + CHUNK * c);
-          const float4 gv = *reinterpret_cast<const float4 *>(gs + CHUNK * c);
-          const float2 xc01 = fadd2(make_float2(xv.x, xv.y), nmean);
-          const float2 xc23 = fadd2(make_float2(xv.z, xv.w), nmean);
-          if (c0 == 0)
-            sq = __fmaf_rn(xc23.y, xc23.y, __fmaf_rn(xc23.x, xc23.x,
-                           __fmaf_rn(xc01.y, xc01.y, __fmaf_rn(xc01.x, xc01.x, sq))));
-          const float2 xg01 = fmul2(xc01, make_float2(gv.x, gv.y));
-          const float2 xg23 = fmul2(xc23, make_float2(gv.z, gv.w));
-          float wv[GROUP][4];
-#pragma unroll
-          for (int q = 0; q < GROUP; ++q) {
-            Chunk<TW> ch;
-            ch.lds(sw + (size_t)q * d + CHUNK * c);
-            ch.to_f32(wv[q]);
-          }
-          const float xe[4] = {xg01.x, xg01.y, xg23.x, xg23.y};
-#pragma unroll
-          for (int e = 0; e < CHUNK; ++e) {
-            const float2 xx = make_float2(xe[e], xe[e]);
-            acc01 = ffma2(xx, make_float2(wv[0][e], wv[1][e]), acc01);
-            acc23 = ffma2(xx, make_float2(wv[2][e], wv[3][e]), acc23);
-          }
-        }
-      }
-      float acc[GROUP] = {acc01.x, acc01.y, acc23.x, acc23.y};
-#pragma unroll
-      for (int q = 0; q < GROUP; ++q) acc[q] = warp_butterfly_sum(acc[q]);
-      if (c0 == 0) sq = warp_butterfly_sum(sq);
-      if (lane == 0) {
-#pragma unroll
-        for (int q = 0; q < GROUP; ++q) red[q * 4 + w] = acc[q];
-        if (c0 == 0) red[(GROUP + 1) * 4 + w] = sq;
-      }
-      team_sync(team);
-      if (c0 == 0) {
-        const float var = __fdiv_rn(canon_combine(red[(GROUP + 1) * 4 + 0], red[(GROUP + 1) * 4 + 1],
-                                                  red[(GROUP + 1) * 4 + 2], red[(GROUP + 1) * 4 + 3]),
-                                    (float)d);
-        r = __frcp_rn(__fsqrt_rn(__fadd_rn(var, 1e-5f)));
-      }
-      if (w == 0 && lane < ng) {
-        const int q = lane;
-        int id = p.ids[(size_t)row * K + c0 + q];
-        id = (id < 0 || id >= p.V) ? 0 : id;
-        const float dot = canon_combine(red[q * 4 + 0], red[q * 4 + 1], red[q * 4 + 2], red[q * 4 + 3]);
-        feats[c0 + q] = __fadd_rn(__fmul_rn(r, dot), p.head_bw ? __ldg(p.head_bw + id) : 0.f);
-      }
-    }
-    const int ibad = __shfl_sync(0xffffffffu, id_bad, 0);   // leader's lane is lane 0 of w0
-    team_sync(team);                                       // stage free, feats complete
-    // ---- prefetch the next row while this row's tail runs
-    const int nrow = next;
-    const bool nskip = nrow >= p.B || row_skipped(p, nrow);
-    if (leader) id_bad = nskip ? 0 : issue_group(nrow, 0, K < GROUP ? K : GROUP, true);
-    // ---- softmax / features (warp 0), error handling
-    if (w == 0) {
-      int ok = 0;
-      if (ibad || hbad) {
-        if (lane == 0) atomicOr(p.err, (ibad ? ERR_ID_RANGE : 0) | (hbad ? ERR_HIDDEN_NONFINITE : 0));
-      } else {
-        ok = warp_softmax_features(p, row, feats, lane) ? 1 : 0;
-      }
-      if (p.logits_out && !ibad && !hbad) {
-        if (lane < K) p.logits_out[(size_t)row * K + lane] = feats[lane];
-        if (lane + 32 < K) p.logits_out[(size_t)row * K + lane + 32] = feats[lane + 32];
-      }
-      if (ok) {
-        if (p.feat_out)
-          for (int i = lane; i < 3 * K; i += 32) p.feat_out[(size_t)row * 3 * K + i] = feats[i];
-        if (lane < K) p.prev[(size_t)row * K + lane] = feats[K + lane];          // engine.py:196
-        if (lane + 32 < K) p.prev[(size_t)row * K + lane + 32] = feats[K + lane + 32];
-        if (lane == 0 && p.evals) p.evals[row] += 1;
-      } else if (lane == 0 && p.fired) {
-        p.fired[row] = 0;
-      }
-      if (lane == 0) tflag[0] = ok;
-    }
-    team_sync(team);
-    const int ok = tflag[0];
-    if (ok) {
-      if (mlp) {
-        if (sp.w1_smem) mlp_z1<1, false>(feats, w1, b1s, 3 * K, H, hs, lane, w);
-        else mlp_z1<1, true>(feats, w1, b1s, 3 * K, H, hs, lane, w);
-        team_sync(team);
-        if (w < 2) as[32 * w + lane] = z2_partial(hs, w2s, H, 32 * w + lane);
-        team_sync(team);
-        if (w == 0) {
-          const float z2 = z2_tree(as[lane], as[lane + 32], hs, w2s, H, p.b2, lane);
-          if (lane == 0) {
-            if (p.z_out) p.z_out[row] = z2;
-            if (p.prob_out) p.prob_out[row] = sigmoid64(z2);
-            if (p.fired) p.fired[row] = (z2 >= p.z_cut) ? 1 : 0;
-          }
-        }
-      } else if (leader) {
-        if (p.prob_out) p.prob_out[row] = p.const_prob;
-        if (p.z_out) p.z_out[row] = 0.0f;
-        if (p.fired) p.fired[row] = (p.const_prob > p.threshold) ? 1 : 0;
-      }
-    }
-    team_sync(team);                      // feats/hs/as/tflag reused by the next row
-    row = nrow;
-    skip = nskip;
-  }
-}
+// ------------------------------------------------------------ FAST
+#include "spx_pred_fast.cuh"
 
 // ----------------------------------------------------------- STRICT (parity)
 // The reference's own operation sequence: every sum a left-to-right chain of
@@ -719,6 +425,14 @@ __global__ void mlp_kernel(PredParams p, const float *feats_in) {
 using namespace spx;
 
 static int g_sms = 0, g_smem_optin = 0;
+static unsigned long long *g_debug_trace = nullptr;
+
+// Debug hook (not part of the ABI contract): per-row globaltimer stamps of the
+// fast predictor kernel, 8 u64 per row: issue(5) wait-start(0) data(1)
+// pass1(2) dots(3) tail-done(4).  NULL disables.
+extern "C" void spx_debug_trace(void *buf) {
+  g_debug_trace = reinterpret_cast<unsigned long long *>(buf);
+}
 static void device_limits() {
   if (!g_sms) {
     int dev = 0;
@@ -731,25 +445,6 @@ static void device_limits() {
 }
 
 template <typename TW>
-struct TeamLaunch {
-  const PredParams &p; const SmemPlan &sp; int grid; cudaStream_t stream;
-  template <int CPL> void operator()() const {
-    if (p.d == CHUNK * NPART * CPL) launch<CPL, true>();
-    else launch<CPL, false>();
-  }
-  template <int CPL, bool FULL> void launch() const {
-    static bool configured = false;
-    if (!configured) {
-      cudaFuncSetAttribute(predictor_team_kernel<TW, CPL, FULL>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_optin);
-      configured = true;
-    }
-    predictor_team_kernel<TW, CPL, FULL>
-        <<<grid > 0 ? grid : 1, 32 * TEAM * sp.nt, sp.bytes, stream>>>(p, sp);
-  }
-};
-
-template <typename TW>
 static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cudaStream_t stream) {
   device_limits();
   if (a->mode == SPX_MODE_STRICT) {
@@ -760,11 +455,16 @@ static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cu
     predictor_strict_kernel<TW><<<(unsigned)a->B, STRICT_THREADS, smem, stream>>>(p);
   } else {
     if (((size_t)p.d * sizeof(TW)) % 16) return SPX_EINVAL;   // TMA bulk: 16-byte rows
-    SmemPlan sp = plan_smem<TW>(p.d, p.K, p.H, g_smem_optin);
-    if (sp.nt == 0) return SPX_EINVAL;
-    const long long need = (a->B + sp.nt - 1) / sp.nt;
+    // tuning overrides (benchmark sweeps only)
+    static const int env_w1 = getenv("SPX_PRED_W1SMEM") ? atoi(getenv("SPX_PRED_W1SMEM")) : -1;
+    static const int env_ns = getenv("SPX_PRED_STAGES") ? atoi(getenv("SPX_PRED_STAGES")) : NS_MAX;
+    SmemPlan sp = plan_smem<TW>(p.d, p.K, p.H, g_smem_optin, env_w1,
+                                env_ns >= 2 && env_ns <= NS_MAX ? env_ns : NS_MAX);
+    if (sp.ns == 0) return SPX_EINVAL;
+    const long long need = (a->B + NTEAM - 1) / NTEAM;
     const int grid = (int)(need < g_sms ? need : g_sms);
-    if (!dispatch_cpl(p.d, TeamLaunch<TW>{p, sp, grid, stream})) return SPX_EINVAL;
+    if (!dispatch_cpl(p.d, FastLaunch<TW>{p, sp, grid > 0 ? grid : 1, stream, g_smem_optin}))
+      return SPX_EINVAL;
   }
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
 }
@@ -790,7 +490,7 @@ extern "C" int spx_predictor_eval(const spx_predictor_args *a, void *stream_) {
   p.logits_out = a->logits_out; p.feat_out = a->feat_out; p.z_out = a->z_out;
   p.prob_out = a->prob_out; p.fired = a->fired;
   p.row_layer_mask = a->row_layer_mask; p.row_done = a->row_done; p.evals = a->evals;
-  p.layer = a->layer; p.err = a->err;
+  p.layer = a->layer; p.err = a->err; p.trace = g_debug_trace;
   p.B = (int)a->B; p.d = (int)a->d; p.V = (int)a->V; p.K = (int)a->K;
   p.H = a->policy == SPX_POLICY_MLP ? (int)a->H : 0;
   if (a->head_dtype == SPX_DTYPE_F32) return launch_predictor<float>(p, a, stream);
