@@ -43,6 +43,7 @@ V, D, K, H, LAYERS = 32000, 4096, 4, 512, 32
 PRED_LAYERS = LAYERS - 1
 THRESHOLD = 0.7
 SEED = 1234
+PDL = os.environ.get("SPX_PDL", "1") == "1"
 METRIC = "predictor evals/sec + early-exit decode tok/s, Llama2-7B shape, 1/2/4/8 B200"
 
 
@@ -276,7 +277,7 @@ def main():
         prev.copy_(prev0)                                  # token start: uniform prior
         for l in range(PRED_LAYERS):
             spx.evaluate_batch(model, bank, hidden[l], ids, prev, threshold=THRESHOLD, layer=l,
-                               outputs=False, out=outs[l])
+                               outputs=False, out=outs[l], pdl=PDL)
 
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
@@ -346,7 +347,7 @@ def main():
         with torch.cuda.graph(g1, stream=stream):
             for l in range(PRED_LAYERS):
                 spx.evaluate_batch(model, bank, hidden[l, :1], i1, p1, threshold=THRESHOLD,
-                                   layer=l, outputs=False, out=o1)
+                                   layer=l, outputs=False, out=o1, pdl=PDL)
         for _ in range(5):
             g1.replay()
         torch.cuda.synchronize()
@@ -378,7 +379,7 @@ def main():
             prev.copy_(prev0)
             for l in range(PRED_LAYERS):
                 spx.evaluate_batch(model, bank, hid_dev[l], ids_dev, prev, threshold=THRESHOLD,
-                                   layer=l, outputs=False, out=eo[l])
+                                   layer=l, outputs=False, out=eo[l], pdl=PDL)
             for l in range(PRED_LAYERS):
                 fired_host[l].copy_(eo[l].fired, non_blocking=True)
                 prob_host[l].copy_(eo[l].prob, non_blocking=True)

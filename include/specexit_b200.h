@@ -86,6 +86,8 @@ typedef struct {
   int32_t *evals;            /* (B) optional per-row evaluation counter        */
   int32_t layer;
   int32_t mode;              /* SPX_MODE_*                                     */
+  int32_t pdl;               /* 1: programmatic dependent launch (overlap the  */
+                             /*    prologue with the previous kernel)          */
   int32_t *err;              /* device error word                              */
   int64_t B, d, V, K, H;
 } spx_predictor_args;

@@ -38,7 +38,7 @@ class PredictorArgs(ctypes.Structure):
                 ("policy", _i32), ("const_prob", _f64), ("threshold", _f64),
                 ("logits_out", _vp), ("feat_out", _vp), ("z_out", _vp), ("prob_out", _vp),
                 ("fired", _vp), ("row_layer_mask", _vp), ("row_done", _vp), ("evals", _vp),
-                ("layer", _i32), ("mode", _i32), ("err", _vp),
+                ("layer", _i32), ("mode", _i32), ("pdl", _i32), ("err", _vp),
                 ("B", _i64), ("d", _i64), ("V", _i64), ("K", _i64), ("H", _i64)]
 
 

