@@ -195,6 +195,68 @@ int spx_path_and(const uint8_t *node_fired, const int32_t *path_ptr, const int32
 int spx_init_uniform(void *out, int32_t out_f32, int64_t rows, int64_t cols, int32_t transpose,
                      uint64_t seed, double low, double high, void *stream);
 
+/* Flag-guarded decoder layer with lazy KV completion (model.py:220-270): advances
+ * every unfrozen row whose frontier == layer through pre-LN MHA + ReLU FFN and
+ * sets its frontier to layer+1.  All kernels return immediately when *done is
+ * nonzero (the stream exited early this token: engine.py:205-207).  Weights
+ * are out-major: wqkv (3d, d) = [wq^T; wk^T; wv^T], wo (d, d) = wo^T,
+ * w1 (ffn, d) = ffn.w1^T, w2 (d, ffn) = ffn.w2^T. */
+typedef struct {
+  const float *ln1_g, *ln1_b, *ln2_g, *ln2_b;
+  const void *wqkv, *wo, *w1, *w2;
+  const float *b1, *b2;
+  int32_t w_dtype;                 /* SPX_DTYPE_*                               */
+  float *pending;                  /* (max_ctx, d) residual rows                */
+  float *kcache, *vcache;          /* this layer's (max_ctx, d) K/V             */
+  int32_t *frontier;               /* (max_ctx)                                 */
+  const int32_t *n_ctx;            /* device scalar: rows in use                */
+  const int32_t *new_row;          /* device scalar: newest row (cur_hidden)    */
+  const uint8_t *frozen;           /* (max_ctx) optional (tree mode)            */
+  const int32_t *attn_ptr;         /* (max_ctx+1) optional ancestor lists (CSR) */
+  const int32_t *attn_idx;
+  const uint8_t *done;             /* device exit flag (skip when nonzero)      */
+  float *cur_hidden;               /* (d) optional copy of the newest row       */
+  int32_t *rows, *nrows;           /* scratch: row set (max_ctx), count         */
+  float *s_q, *s_att, *s_f;        /* scratch (max_ctx, d), (max_ctx, d), (max_ctx, ffn) */
+  int32_t layer, mode;
+  int32_t *err;
+  int64_t max_ctx, d, n_heads, ffn;
+} spx_layer_args;
+int spx_layer_forward(const spx_layer_args *args, void *stream);
+/* begin() (model.py:181-212): append T rows, pending = emb[tok] + pe[pos],
+ * frontier 0; *n_ctx += T; *new_row = last appended row. */
+int spx_embed(const void *embedding, int32_t w_dtype, const float *pos_encoding,
+              const int32_t *tokens, const int32_t *pos_ids, int64_t T, int64_t d, int64_t V,
+              int64_t max_ctx, float *pending, int32_t *frontier, int32_t *n_ctx,
+              int32_t *new_row, int32_t *err, void *stream);
+
+/* Device-resident per-token state of a single-stream engine (engine.py:176-217)
+ * and its trace record arrays (ExitRecord, engine.py:26-48). */
+typedef struct {
+  float *prev;                                  /* (K) local probs carried    */
+  uint8_t *done, *fired, *fired_any;            /* exit flag, per-layer fire  */
+  int32_t *exit_layer, *exit_token, *final_token, *evals, *full_heads;
+  int32_t *next_in, *step;
+  uint64_t *active;                             /* scheduled-layer bitmask    */
+  int32_t *rec_token, *rec_exit_layer, *rec_evals, *rec_full_heads;
+  uint8_t *rec_fired, *rec_verified;
+  uint64_t *rec_active;
+} spx_token_state;
+/* stable top-K (value desc, lower id on ties) of n logits
+ * (speculation.py:57-60 topk_from_logits). K <= 64. */
+int spx_topk(const float *logits, int64_t n, int32_t K, int32_t *ids_out, void *stream);
+/* token start: prev = inv_k (= float32(1/K)), clear flags, exit_layer = L-1 */
+int spx_token_begin(spx_token_state st, int32_t K, int32_t L, float inv_k, void *stream);
+/* token end: pick verified exit token or the final argmax, record, next_in,
+ * update_online (scheduler.py:65-79) of stream row 0 */
+int spx_token_end(spx_token_state st, spx_online_state os, int32_t L, int32_t queue_len,
+                  int32_t radius, int64_t max_steps, void *stream);
+/* *dst |= *src (byte flags) */
+int spx_or_flag(const uint8_t *src, uint8_t *dst, void *stream);
+/* generate_forced (engine.py:227-246): *next_in = forced[*step - 1] */
+int spx_force_next(const int32_t *forced, const int32_t *step, int32_t *next_in,
+                   int64_t n_forced, void *stream);
+
 /* numpy float32 exp restated on device (the exp of softmax_1d, model.py:151),
  * elementwise -- test hook for the bit-exactness of the softmax. */
 int spx_np_expf(const float *x, float *y, int64_t n, void *stream);

@@ -16,5 +16,12 @@ from .scheduler import (OfflineProfile, OnlineState, ScheduleConfig, active_laye
                         load_profile, online_hot_layers, profile_offline, recompute_counts,
                         save_profile, update_online, weight_fingerprint)
 from .tree import grouped_speculative_logits, hypertoken_exit_decision  # noqa: F401
+from .decode import DecodeState, forward_to_layer, prefill  # noqa: F401
+from .speculation import (SpeculativeSet, TokenTree, TreeNode, build_token_tree,  # noqa: F401
+                          enumerate_paths, propose_topk, speculative_set_from_logits,
+                          topk_from_logits)
+from .engine import (AlwaysExitPolicy, EngineConfig, ExitEngine, ExitRecord,  # noqa: F401
+                     NeverExitPolicy, OraclePolicy, PredictorPolicy, generate, greedy_generate,
+                     oracle_exit_layer, read_trace, verify_exit, write_trace)
 
 __version__ = "0.1.0"

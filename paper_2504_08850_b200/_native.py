@@ -57,6 +57,28 @@ class OnlineStateC(ctypes.Structure):
     _fields_ = [("queue", _vp), ("head", _vp), ("len", _vp), ("counts", _vp)]
 
 
+class LayerArgs(ctypes.Structure):
+    """spx_layer_args (include/specexit_b200.h)."""
+    _fields_ = [("ln1_g", _vp), ("ln1_b", _vp), ("ln2_g", _vp), ("ln2_b", _vp),
+                ("wqkv", _vp), ("wo", _vp), ("w1", _vp), ("w2", _vp), ("b1", _vp), ("b2", _vp),
+                ("w_dtype", _i32), ("pending", _vp), ("kcache", _vp), ("vcache", _vp),
+                ("frontier", _vp), ("n_ctx", _vp), ("new_row", _vp), ("frozen", _vp),
+                ("attn_ptr", _vp), ("attn_idx", _vp), ("done", _vp), ("cur_hidden", _vp),
+                ("rows", _vp), ("nrows", _vp), ("s_q", _vp), ("s_att", _vp), ("s_f", _vp),
+                ("layer", _i32), ("mode", _i32), ("err", _vp),
+                ("max_ctx", _i64), ("d", _i64), ("n_heads", _i64), ("ffn", _i64)]
+
+
+class TokenStateC(ctypes.Structure):
+    """spx_token_state (include/specexit_b200.h)."""
+    _fields_ = [("prev", _vp), ("done", _vp), ("fired", _vp), ("fired_any", _vp),
+                ("exit_layer", _vp), ("exit_token", _vp), ("final_token", _vp), ("evals", _vp),
+                ("full_heads", _vp), ("next_in", _vp), ("step", _vp), ("active", _vp),
+                ("rec_token", _vp), ("rec_exit_layer", _vp), ("rec_evals", _vp),
+                ("rec_full_heads", _vp), ("rec_fired", _vp), ("rec_verified", _vp),
+                ("rec_active", _vp)]
+
+
 _LIB = None
 
 
@@ -85,6 +107,16 @@ def lib():
                                     _i64, _vp]
     L.spx_extract_features.argtypes = [_vp, _vp, _vp, _vp, _i64, _i64, _vp]
     L.spx_np_expf.argtypes = [_vp, _vp, _i64, _vp]
+    L.spx_layer_forward.argtypes = [ctypes.POINTER(LayerArgs), _vp]
+    L.spx_embed.argtypes = [_vp, _i32, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
+                            _vp, _vp, _vp]
+    L.spx_topk.argtypes = [_vp, _i64, _i32, _vp, _vp]
+    L.spx_token_begin.argtypes = [TokenStateC, _i32, _i32, _f32, _vp]
+    L.spx_token_end.argtypes = [TokenStateC, OnlineStateC, _i32, _i32, _i32, _i64, _vp]
+    L.spx_or_flag.argtypes = [_vp, _vp, _vp]
+    L.spx_force_next.argtypes = [_vp, _vp, _vp, _i64, _vp]
+    L.spx_debug_trace.argtypes = [_vp]
+    L.spx_debug_trace.restype = None
     _LIB = L
     return L
 

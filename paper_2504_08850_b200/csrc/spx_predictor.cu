@@ -423,6 +423,63 @@ __global__ void features_kernel(const float *logits, float *prev, float *feats_o
   for (int i = threadIdx.x; i < 3 * K; i += 32) feats_out[(size_t)row * 3 * K + i] = feats[i];
 }
 
+// extract_features for wide speculative sets (K > MAXK: the spec_full_vocab
+// ablation, engine.py:166-168).  One CTA per row, working in feats_out; the
+// two sums stay the reference's strict left-to-right chains (thread 0).
+__global__ void features_wide_kernel(const float *logits, const float *prev, float *feats_out,
+                                     int *err, int K) {
+  const int row = blockIdx.x, tid = threadIdx.x;
+  const float *x = logits + (size_t)row * K, *pv = prev + (size_t)row * K;
+  float *f = feats_out + (size_t)row * 3 * K;
+  __shared__ float s_red[32];
+  __shared__ int s_bad;
+  __shared__ float s_esum;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  float m = -INFINITY;
+  for (int i = tid; i < K; i += blockDim.x) {
+    const float v = x[i];
+    if (!is_finite(v)) s_bad = 1;
+    m = fmaxf(m, v);
+  }
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, s));
+  if ((tid & 31) == 0) s_red[tid >> 5] = m;
+  __syncthreads();
+  if (tid == 0) {
+    float mm = s_red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mm = fmaxf(mm, s_red[w]);
+    s_red[0] = mm;
+  }
+  __syncthreads();
+  m = s_red[0];
+  for (int i = tid; i < K; i += blockDim.x) {
+    f[i] = x[i];
+    f[K + i] = np_expf(__fsub_rn(x[i], m));
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float esum = 0.f, psum = 0.f;
+    for (int c = 0; c < K; ++c) {
+      esum = __fadd_rn(esum, f[K + c]);
+      psum = __fadd_rn(psum, pv[c]);
+    }
+    int e = 0;
+    if (s_bad) e |= ERR_LOGIT_NONFINITE;
+    if (fabs((double)psum - 1.0) > 1e-5) e |= ERR_PREV_SUM;
+    if (e) atomicOr(err, e);
+    s_bad = e;
+    s_esum = esum;
+  }
+  __syncthreads();
+  if (s_bad) return;
+  for (int i = tid; i < K; i += blockDim.x) {
+    const float pr = __fdiv_rn(f[K + i], s_esum);
+    f[K + i] = pr;
+    f[2 * K + i] = __fsub_rn(pr, pv[i]);
+  }
+}
+
 __global__ void mlp_kernel(PredParams p, const float *feats_in) {
   const int row = blockIdx.x;
   if (row >= p.B) return;
@@ -518,8 +575,13 @@ extern "C" int spx_predictor_eval(const spx_predictor_args *a, void *stream_) {
 
 extern "C" int spx_extract_features(const float *logits, const float *prev, float *feats_out,
                                     int32_t *err, int64_t B, int64_t K, void *stream) {
-  if (!logits || !prev || !feats_out || !err || B < 0 || K < 1 || K > MAXK) return SPX_EINVAL;
+  if (!logits || !prev || !feats_out || !err || B < 0 || K < 1 || K > (1 << 24)) return SPX_EINVAL;
   if (B == 0) return 0;
+  if (K > MAXK) {
+    features_wide_kernel<<<(unsigned)B, 256, 0, (cudaStream_t)stream>>>(logits, prev, feats_out,
+                                                                       err, (int)K);
+    return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  }
   features_kernel<<<(unsigned)B, 32, 0, (cudaStream_t)stream>>>(
       logits, const_cast<float *>(prev), feats_out, err, (int)B, (int)K);
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;

@@ -362,6 +362,37 @@ class _VerifyScratch:
         return s
 
 
+def verify_args(model: TransformerModel, hidden: torch.Tensor, B: int, token_out, scratch,
+                counter, err, **kw) -> N.VerifyArgs:
+    """spx_verify_args for B rows of `hidden` (row stride hidden.stride(0), or
+    a (d) vector for B == 1); keyword arguments name the optional device
+    pointers of the struct (gate, row_done, spec_ptr, spec_ids, verified_out,
+    maxlogit_out, logits_out, done_out, exit_layer_out, full_heads) plus
+    `layer` and `mode`.  Nothing is launched."""
+    a = N.VerifyArgs()
+    a.hidden = N.ptr(hidden)
+    a.hidden_stride = hidden.stride(0) if hidden.dim() == 2 else model.config.hidden_dim
+    a.norm_g, a.norm_b = N.ptr(model.final_g), N.ptr(model.final_b)
+    a.head, a.head_dtype, a.head_bw = N.ptr(model.lm_head), model.spx_dtype, N.ptr(model.head_bw)
+    for name in ("gate", "row_done", "spec_ptr", "spec_ids", "verified_out", "maxlogit_out",
+                 "logits_out", "done_out", "exit_layer_out", "full_heads"):
+        setattr(a, name, N.ptr(kw.get(name)))
+    a.token_out = N.ptr(token_out)
+    a.layer = int(kw.get("layer", 0))
+    a.scratch, a.counter = N.ptr(scratch), N.ptr(counter)
+    mode = kw.get("mode")
+    a.mode, a.err = numerics.mode() if mode is None else mode, N.ptr(err)
+    a.B, a.d, a.V = B, model.config.hidden_dim, model.config.vocab_size
+    return a
+
+
+def launch_verify(args: N.VerifyArgs, mode: int = None):
+    """Enqueue one spx_verify on the current stream (no sync)."""
+    if mode is not None:
+        args.mode = mode
+    N.check(N.lib().spx_verify(args, N.stream_ptr()), "spx_verify")
+
+
 def head_argmax(model: TransformerModel, hidden, spec_lists=None, want_logits=False):
     """K4 on N rows: (tokens, verified, logits|None).  spec_lists: per-row
     verify sets (or None)."""
@@ -372,25 +403,17 @@ def head_argmax(model: TransformerModel, hidden, spec_lists=None, want_logits=Fa
     logits = torch.empty((B, V), dtype=torch.float32, device="cuda") if want_logits else None
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
     scratch, counter = _VerifyScratch.get(B)
-    a = N.VerifyArgs()
-    a.hidden, a.hidden_stride = N.ptr(h), h.shape[1]
-    a.norm_g, a.norm_b = N.ptr(model.final_g), N.ptr(model.final_b)
-    a.head, a.head_dtype, a.head_bw = N.ptr(model.lm_head), model.spx_dtype, N.ptr(model.head_bw)
-    keep = []
+    d_ptr = d_ids = None
     if spec_lists is not None:
         ptr_ = np.concatenate([[0], np.cumsum([len(s) for s in spec_lists])]).astype(np.int32)
         ids = np.concatenate([np.asarray(s, np.int32).reshape(-1) for s in spec_lists]
                              ) if len(spec_lists) else np.zeros(0, np.int32)
         d_ptr = torch.as_tensor(ptr_, device="cuda")
-        d_ids = torch.as_tensor(np.ascontiguousarray(ids, np.int32), device="cuda")
-        keep += [d_ptr, d_ids]
-        a.spec_ptr, a.spec_ids = N.ptr(d_ptr), N.ptr(d_ids) if ids.size else N.ptr(d_ptr)
-    a.token_out, a.verified_out = N.ptr(tok), N.ptr(ver)
-    a.logits_out = N.ptr(logits)
-    a.scratch, a.counter = N.ptr(scratch), N.ptr(counter)
-    a.mode, a.err = numerics.mode(), N.ptr(err)
-    a.B, a.d, a.V = B, model.config.hidden_dim, V
-    N.check(N.lib().spx_verify(a, N.stream_ptr()), "spx_verify")
+        d_ids = torch.as_tensor(np.ascontiguousarray(ids, np.int32), device="cuda") \
+            if ids.size else d_ptr
+    a = verify_args(model, h, B, tok, scratch, counter, err, spec_ptr=d_ptr, spec_ids=d_ids,
+                    verified_out=ver, logits_out=logits)
+    launch_verify(a)
     N.raise_device_error(err.item())
     return tok, ver, logits
 

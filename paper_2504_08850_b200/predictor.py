@@ -57,8 +57,6 @@ def extract_features(spec_logits, prev_local_probs) -> FeatureVector:
     if lg.numel() < 1 or tuple(np.shape(spec_logits)) != tuple(np.shape(prev_local_probs)):
         raise ValueError("bad feature input shapes")
     k = lg.numel()
-    if k > 64:
-        raise ValueError("speculative set larger than 64 is not supported on device")
     out = torch.empty(3 * k, dtype=torch.float32, device="cuda")
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
     N.check(N.lib().spx_extract_features(N.ptr(lg), N.ptr(pv), N.ptr(out), N.ptr(err), 1, k,

@@ -1,0 +1,227 @@
+"""GPU parity of the device-resident early-exit engine (flag-guarded decoder
+layers + the graph-captured token step) against the oracle and the
+reference's golden traces.
+
+STRICT mode (reference reduction order) must reproduce the reference's
+hidden states bit-for-bit and every ExitRecord field exactly.  FAST mode is
+held to hidden states within 1e-4 relative (tolerance stated here) and to
+self-consistency (Never policy == greedy decoding).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2504_08850_b200 as spx
+from paper_2504_08850_b200 import engine as E
+from paper_2504_08850_b200 import numerics
+from paper_2504_08850_b200.decode import DecodeState
+
+pytestmark = pytest.mark.gpu
+
+HIDDEN_RTOL_FAST = 1e-4
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+PROMPT = [84, 104, 101, 32]
+
+
+def _ref_rows(oracle, seed, layers, tokens):
+    cfg = oracle.ModelConfig(num_layers=layers, seed=seed)
+    t = oracle.init_model(cfg, bf16=True)
+    st = oracle.DecodeState(cfg, t, oracle.sinusoidal_encoding(cfg.max_context, cfg.hidden_dim))
+    return cfg, t, st
+
+
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_decode_state_lazy_completion(oracle, mode):
+    """Layer kernels vs the oracle DecodeState, including the lazy
+    completion of rows left behind by an early exit (model.py:220-270)."""
+    m = spx.init_model(spx.ModelConfig(num_layers=4, seed=3), dtype="bf16")
+    cfg, t, ref = _ref_rows(oracle, 3, 4, None)
+    with numerics.using(mode):
+        st = DecodeState(m)
+        # prompt through all layers, then token A exits after layer 1,
+        # token B runs all layers (dragging A's rows 2..3 along)
+        plan = [(PROMPT, 4), ([65], 2), ([66], 4), ([67], 1), ([68], 4)]
+        for toks, depth in plan:
+            st.begin(toks)
+            ref.begin(toks)
+            for l in range(depth):
+                got = st.run_layer(l).cpu().numpy()
+                want = ref.run_layer(l)
+                if mode == "strict":
+                    assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (toks, l)
+                else:
+                    np.testing.assert_allclose(got, want, rtol=HIDDEN_RTOL_FAST,
+                                               atol=HIDDEN_RTOL_FAST * np.abs(want).max())
+        st.check()
+        fr = st.frontier[:st.n].cpu().numpy()
+        assert list(fr) == list(ref.frontier[:ref.n])
+
+
+def _engine_models(eg):
+    tc = spx.ModelConfig(num_layers=6, seed=eg["target_seed"])
+    dc = spx.ModelConfig(num_layers=2, seed=eg["draft_seed"])
+    return spx.init_model(tc, dtype="bf16"), spx.init_model(dc, dtype="bf16")
+
+
+def _rec_tuple(r):
+    return (r.token, r.exit_layer, r.predictor_fired, r.verified, list(r.active),
+            r.full_head_count, r.predictor_evals)
+
+
+def test_engine_golden_traces_strict(golden, oracle):
+    """Every policy / schedule of engine_tiny.json reproduced record for
+    record by the graph-captured device engine."""
+    eg = golden.json("engine_tiny.json")
+    t, d = _engine_models(eg)
+    bank = {l: spx.init_predictor(4, 512, oracle.derive(eg["bank_seed"], l)) for l in range(5)}
+    prof = spx.OfflineProfile(6, np.asarray(eg["exit_counts"]), 0)
+    with numerics.using("strict"):
+        for tr in eg["traces"]:
+            pol = {"never": E.NeverExitPolicy(), "always": E.AlwaysExitPolicy()}.get(
+                tr["policy"]) or E.PredictorPolicy(bank)
+            cfg = E.EngineConfig(k=4, threshold=tr["threshold"], schedule_mode=tr["mode"])
+            eng = E.ExitEngine(t, d, pol, cfg, prof,
+                               spx.ScheduleConfig(tr["queue_len"], tr["radius"], tr["top_k"]))
+            assert eng.device_resident()
+            toks, trace = eng.generate(tr["prompt"], len(tr["tokens"]))
+            assert toks == tr["tokens"], tr["policy"]
+            for rec, ref in zip(trace, tr["records"]):
+                assert _rec_tuple(rec) == (ref["token"], ref["exit_layer"], ref["predictor_fired"],
+                                           ref["verified"], ref["active"], ref["full_head_count"],
+                                           ref["predictor_evals"]), tr["policy"]
+
+
+def test_engine_host_path_matches_device_path(golden, oracle):
+    """The host-decision loop (used for custom policies) and the device graph
+    agree record for record."""
+    eg = golden.json("engine_tiny.json")
+    t, d = _engine_models(eg)
+    bank = {l: spx.init_predictor(4, 512, oracle.derive(eg["bank_seed"], l)) for l in range(5)}
+    prof = spx.OfflineProfile(6, np.asarray(eg["exit_counts"]), 0)
+
+    class Wrapped(E.PredictorPolicy):       # a user subclass -> host path
+        pass
+
+    with numerics.using("strict"):
+        cfg = E.EngineConfig(k=4, threshold=0.5, schedule_mode="two-level")
+        dev = E.ExitEngine(t, d, E.PredictorPolicy(bank), cfg, prof, spx.ScheduleConfig(5, 1, 2))
+        host = E.ExitEngine(t, d, Wrapped(bank), cfg, prof, spx.ScheduleConfig(5, 1, 2))
+        assert dev.device_resident() and not host.device_resident()
+        a = dev.generate(PROMPT, 12)
+        b = host.generate(PROMPT, 12)
+        assert a[0] == b[0]
+        assert [_rec_tuple(r) for r in a[1]] == [_rec_tuple(r) for r in b[1]]
+
+
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_never_exit_equals_greedy(golden, mode):
+    """engine tests: test_never_exit_equals_greedy (tests/test_engine.py:14-20)."""
+    eg = golden.json("engine_tiny.json")
+    t, d = _engine_models(eg)
+    with numerics.using(mode):
+        base, _ = E.greedy_generate(t, PROMPT, 24)
+        toks, trace = E.ExitEngine(t, d, E.NeverExitPolicy()).generate(PROMPT, 24)
+    assert toks == base
+    assert all(r.exit_layer == 5 for r in trace)
+    assert not any(r.predictor_fired for r in trace)
+
+
+def test_oracle_policy_lossless(golden):
+    """tests/test_engine.py:23-38: the oracle policy with the full-vocabulary
+    speculative set reproduces greedy output and the oracle exit layers."""
+    eg = golden.json("engine_tiny.json")
+    t, d = _engine_models(eg)
+    base, layers = E.greedy_generate(t, PROMPT, 12)
+    eng = E.ExitEngine(t, d, E.OraclePolicy(t), E.EngineConfig(spec_full_vocab=True))
+    assert not eng.device_resident()
+    toks, trace = eng.generate(PROMPT, 12)
+    assert toks == base
+    assert [r.exit_layer for r in trace] == layers
+
+
+def test_always_exit_soundness(golden):
+    """tests/test_engine.py:53-68: a verified exit token equals the full-head
+    argmax at the exit layer (replayed from scratch)."""
+    eg = golden.json("engine_tiny.json")
+    t, d = _engine_models(eg)
+    toks, trace = E.ExitEngine(t, d, E.AlwaysExitPolicy()).generate(PROMPT, 16)
+    ctx = list(PROMPT)
+    for rec in trace:
+        st = DecodeState(t)
+        st.begin(ctx)
+        for l in range(rec.exit_layer + 1):
+            st.launch_layer(l)
+        tok, _, _ = spx.head_argmax(t, st.cur_hidden)
+        if rec.verified or rec.exit_layer == 5:
+            assert rec.token == int(tok[0].item())
+        ctx.append(rec.token)
+
+
+def test_predictor_policy_requires_layer_coverage(golden):
+    """tests/test_engine.py:71-75."""
+    eg = golden.json("engine_tiny.json")
+    t, d = _engine_models(eg)
+    bank = {0: spx.init_predictor(4, 8, seed=0)}
+    eng = E.ExitEngine(t, d, E.PredictorPolicy(bank))
+    with pytest.raises(KeyError):
+        eng.generate(PROMPT, 2)
+
+
+def test_context_overflow_raises(golden):
+    eg = golden.json("engine_tiny.json")
+    t, d = _engine_models(eg)
+    eng = E.ExitEngine(t, d, E.NeverExitPolicy())
+    with pytest.raises(ValueError):
+        eng.generate(PROMPT, t.config.max_context)
+
+
+def _corpus_prompts(corpus, n, plen, seed, oracle):
+    data = np.frombuffer(corpus, dtype=np.uint8)
+    starts = oracle.splitmix64(seed, n) % np.uint64(data.size - plen + 1)
+    return [[int(b) for b in data[int(s):int(s) + plen]] for s in starts]
+
+
+def test_tiny_pipeline_trace_on_device(oracle):
+    """The reference pipeline's bench stage (pipeline.py:193-242) on the
+    device engine: greedy stream, then generate_forced with the trained
+    predictors, two-level scheduling (thr 0.7, ScheduleConfig(5, 1, 4)) --
+    the shipped trace.jsonl reproduced record for record (f32 weights)."""
+    d = os.path.join(GOLDEN, "tiny_pipeline")
+    t = spx.load_weights(os.path.join(d, "target.spxw"))
+    dm = spx.load_weights(os.path.join(d, "draft.spxw"))
+    bank = spx.load_predictors(os.path.join(d, "predictors.spxp"))
+    prof = spx.load_profile(os.path.join(d, "profile.spxs"))
+    with open(os.path.join(d, "fixture_corpus.txt"), "rb") as fh:
+        prompts = _corpus_prompts(fh.read(), 16, 16, 606, oracle)
+    with open(os.path.join(d, "trace.jsonl")) as fh:
+        golden = [json.loads(line) for line in fh if line.strip()]
+    out = []
+    with numerics.using("strict"):
+        eng = E.ExitEngine(t, dm, E.PredictorPolicy(bank),
+                           E.EngineConfig(k=4, threshold=0.7, schedule_mode="two-level"), prof,
+                           spx.ScheduleConfig(5, 1, 4))
+        assert eng.device_resident()
+        for prompt in prompts:
+            base, _ = E.greedy_generate(t, prompt, 48)
+            out.extend(eng.generate_forced(prompt, base))
+    assert len(out) == len(golden) == 768
+    for i, (rec, ref) in enumerate(zip(out, golden)):
+        assert (rec.token, rec.exit_layer, rec.predictor_fired, rec.verified, rec.active) == (
+            ref["token"], ref["exit_layer"], ref["predictor_fired"], ref["verified"],
+            ref["active"]), i
+
+
+def test_device_step_graph_replays_without_host_sync(golden):
+    """generate() of N tokens replays the captured token graph N times; the
+    graph is captured once per (mode, forced) and reused across calls."""
+    eg = golden.json("engine_tiny.json")
+    t, d = _engine_models(eg)
+    eng = E.ExitEngine(t, d, E.AlwaysExitPolicy())
+    a, _ = eng.generate(PROMPT, 8)
+    g = dict(eng._dev.graphs)
+    b, _ = eng.generate(PROMPT, 8)
+    assert a == b
+    assert eng._dev.graphs == g and len(g) == 1
