@@ -262,7 +262,7 @@ class _DeviceStep:
         for l in range(self.L):
             ts.launch_layer(l)
             if l <= self.L - 2:
-                pa = self._pred_args(l, mode)
+                pa = self._pargs[l]
                 N.check(lib.spx_predictor_eval(pa, s()), "spx_predictor_eval")
                 N.check(lib.spx_or_flag(N.ptr(self.fired), N.ptr(self.fired_any), s()),
                         "spx_or_flag")
@@ -287,6 +287,8 @@ class _DeviceStep:
         key = (mode, forced)
         g = self.graphs.get(key)
         if g is None:
+            # host-side preparation (weight packing, z_cut) before capture
+            self._pargs = [self._pred_args(l, mode) for l in range(self.L - 1)]
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 self.enqueue(mode, forced)

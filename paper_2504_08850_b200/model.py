@@ -218,7 +218,7 @@ def from_tensors(config: ModelConfig, tensors: dict, dtype: str = "f32",
         dst, transpose = m._target(name)
         if dst is None:
             continue
-        src = torch.as_tensor(np.ascontiguousarray(tensors[name], dtype=np.float32))
+        src = torch.from_numpy(np.array(tensors[name], dtype=np.float32, order="C"))
         if transpose:
             src = src.t()
         dst.copy_(src.to(dst.dtype))
