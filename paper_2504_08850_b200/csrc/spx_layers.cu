@@ -380,6 +380,8 @@ __global__ void finish_kernel(LayerParams p) {
 
 }  // namespace spx
 
+#include "spx_layers_fast.cuh"
+
 using namespace spx;
 
 static int sm_count() {
@@ -396,6 +398,10 @@ static int sm_count() {
 template <typename TW>
 static void launch_layer(const LayerParams &p, cudaStream_t s) {
   const int sms = sm_count();
+  if (!p.strict && fast_layer_supported(p, sizeof(TW))) {
+    launch_layer_fast<TW>(p, sms, s);
+    return;
+  }
   const size_t ln_smem = (size_t)RMAX * p.d * sizeof(float);
   const size_t f_smem = (size_t)RMAX * (p.ffn > p.d ? p.ffn : p.d) * sizeof(float);
   static bool configured = false;
