@@ -218,11 +218,16 @@ typedef struct {
   float *cur_hidden;               /* (d) optional copy of the newest row       */
   int32_t *rows, *nrows;           /* scratch: row set (max_ctx), count         */
   float *s_q, *s_att, *s_f;        /* scratch (max_ctx, d), (max_ctx, d), (max_ctx, ffn) */
+  float *s_part;                   /* scratch: split-K partials (FAST), see spx_layer_part_floats */
+  int32_t *s_flag;                 /* scratch: split-K arrival counters, zeroed once, self-reset */
   int32_t layer, mode;
   int32_t *err;
   int64_t max_ctx, d, n_heads, ffn;
 } spx_layer_args;
 int spx_layer_forward(const spx_layer_args *args, void *stream);
+/* floats needed for s_part and int32s for s_flag at these dimensions */
+int64_t spx_layer_part_floats(int64_t d, int64_t ffn);
+int64_t spx_layer_flag_ints(int64_t d, int64_t ffn);
 /* begin() (model.py:181-212): append T rows, pending = emb[tok] + pe[pos],
  * frontier 0; *n_ctx += T; *new_row = last appended row. */
 int spx_embed(const void *embedding, int32_t w_dtype, const float *pos_encoding,

@@ -65,6 +65,7 @@ class LayerArgs(ctypes.Structure):
                 ("frontier", _vp), ("n_ctx", _vp), ("new_row", _vp), ("frozen", _vp),
                 ("attn_ptr", _vp), ("attn_idx", _vp), ("done", _vp), ("cur_hidden", _vp),
                 ("rows", _vp), ("nrows", _vp), ("s_q", _vp), ("s_att", _vp), ("s_f", _vp),
+                ("s_part", _vp), ("s_flag", _vp),
                 ("layer", _i32), ("mode", _i32), ("err", _vp),
                 ("max_ctx", _i64), ("d", _i64), ("n_heads", _i64), ("ffn", _i64)]
 
@@ -108,6 +109,10 @@ def lib():
     L.spx_extract_features.argtypes = [_vp, _vp, _vp, _vp, _i64, _i64, _vp]
     L.spx_np_expf.argtypes = [_vp, _vp, _i64, _vp]
     L.spx_layer_forward.argtypes = [ctypes.POINTER(LayerArgs), _vp]
+    L.spx_layer_part_floats.argtypes = [_i64, _i64]
+    L.spx_layer_part_floats.restype = _i64
+    L.spx_layer_flag_ints.argtypes = [_i64, _i64]
+    L.spx_layer_flag_ints.restype = _i64
     L.spx_embed.argtypes = [_vp, _i32, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
                             _vp, _vp, _vp]
     L.spx_topk.argtypes = [_vp, _i64, _i32, _vp, _vp]

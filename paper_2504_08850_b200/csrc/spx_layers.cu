@@ -35,6 +35,8 @@ struct LayerParams {
   float *cur_hidden;
   int32_t *rows, *nrows;
   float *s_q, *s_att, *s_f;
+  float *s_part;
+  int32_t *s_flag;
   int layer, strict;
   int *err;
   int max_ctx, d, nh, ffn;
@@ -447,6 +449,7 @@ extern "C" int spx_layer_forward(const spx_layer_args *a, void *stream) {
   p.attn_ptr = a->attn_ptr; p.attn_idx = a->attn_idx; p.done = a->done;
   p.cur_hidden = a->cur_hidden; p.rows = a->rows; p.nrows = a->nrows;
   p.s_q = a->s_q; p.s_att = a->s_att; p.s_f = a->s_f;
+  p.s_part = a->s_part; p.s_flag = a->s_flag;
   p.layer = a->layer; p.strict = a->mode == SPX_MODE_STRICT; p.err = a->err;
   p.max_ctx = (int)a->max_ctx; p.d = (int)a->d; p.nh = (int)a->n_heads; p.ffn = (int)a->ffn;
   cudaStream_t s = (cudaStream_t)stream;
@@ -454,6 +457,20 @@ extern "C" int spx_layer_forward(const spx_layer_args *a, void *stream) {
   else if (a->w_dtype == SPX_DTYPE_F32) launch_layer<float>(p, s);
   else return SPX_EINVAL;
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+}
+
+static int64_t mma_items(int64_t nout, int64_t kin) {
+  return ((nout + MRG - 1) / MRG) * ((kin + MKC - 1) / MKC);
+}
+extern "C" int64_t spx_layer_part_floats(int64_t d, int64_t ffn) {
+  int64_t m = mma_items(3 * d, d);
+  m = mma_items(ffn, d) > m ? mma_items(ffn, d) : m;
+  m = mma_items(d, ffn) > m ? mma_items(d, ffn) : m;
+  return m * 128;
+}
+extern "C" int64_t spx_layer_flag_ints(int64_t d, int64_t ffn) {
+  const int64_t n = 3 * d > ffn ? 3 * d : ffn;
+  return (n + MRG - 1) / MRG;
 }
 
 // ---- begin(): append T rows (model.py:181-212): pending = emb[tok] + pe[pos]

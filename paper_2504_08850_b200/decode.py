@@ -40,6 +40,11 @@ class DecodeState:
         self.s_att = torch.zeros((C, d), dtype=torch.float32, device=dev)
         self.s_f = torch.zeros((C, f), dtype=torch.float32, device=dev)
         self.cur_hidden = torch.zeros(d, dtype=torch.float32, device=dev)
+        lib = N.lib()
+        self.s_part = torch.zeros(max(1, lib.spx_layer_part_floats(d, f)), dtype=torch.float32,
+                                  device=dev)
+        self.s_flag = torch.zeros(max(1, lib.spx_layer_flag_ints(d, f)), dtype=torch.int32,
+                                  device=dev)
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
         self.attn_ptr = None
         self.attn_idx = None
@@ -132,6 +137,7 @@ class DecodeState:
         a.cur_hidden = N.ptr(self.cur_hidden)
         a.rows, a.nrows = N.ptr(self.rows), N.ptr(self.nrows)
         a.s_q, a.s_att, a.s_f = N.ptr(self.s_q), N.ptr(self.s_att), N.ptr(self.s_f)
+        a.s_part, a.s_flag = N.ptr(self.s_part), N.ptr(self.s_flag)
         a.layer = l
         a.err = N.ptr(self.err)
         a.max_ctx, a.d, a.n_heads, a.ffn = cfg.max_context, cfg.hidden_dim, cfg.num_heads, cfg.ffn_dim

@@ -1,0 +1,54 @@
+"""Decode-step decoder layers at Llama2-7B dims for ncu / timing: a short
+prompt is prefilled, then `--steps` single-token steps run all layers.
+Prints the device time per layer (CUDA events, PDL chained launches)."""
+import argparse
+import json
+
+import torch
+
+import paper_2504_08850_b200 as spx
+from paper_2504_08850_b200 import numerics
+from paper_2504_08850_b200.decode import DecodeState
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layers", type=int, default=4)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--d", type=int, default=4096)
+    ap.add_argument("--ffn", type=int, default=11008)
+    ap.add_argument("--heads", type=int, default=32)
+    args = ap.parse_args()
+    numerics.set_mode("fast")
+    cfg = spx.ModelConfig(32000, args.d, args.layers, args.heads, args.ffn, 512, 5)
+    m = spx.init_model(cfg, dtype="bf16")
+    st = DecodeState(m)
+    st.begin(list(range(1, 17)))
+    for l in range(args.layers):
+        st.launch_layer(l)
+    g = torch.cuda.CUDAGraph()
+    tok = torch.tensor([42], dtype=torch.int32, device="cuda")
+    # one captured decode step (embed + all layers), replayed
+    with torch.cuda.graph(g):
+        st.embed_device(tok, 1)
+        for l in range(args.layers):
+            st.launch_layer(l)
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    st.check()
+    ms = e0.elapsed_time(e1) / args.steps
+    lay_bytes = (4 * args.d * args.d + 2 * args.d * args.ffn) * 2
+    us_layer = ms * 1e3 / args.layers
+    print(json.dumps({"us_per_layer": us_layer, "GBps": lay_bytes / (us_layer * 1e-6) / 1e9,
+                      "layer_MB": lay_bytes / 1e6}))
+
+
+if __name__ == "__main__":
+    main()
