@@ -459,18 +459,18 @@ extern "C" int spx_layer_forward(const spx_layer_args *a, void *stream) {
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
 }
 
-static int64_t mma_items(int64_t nout, int64_t kin) {
-  return ((nout + MRG - 1) / MRG) * ((kin + MKC - 1) / MKC);
+static int64_t tc_units(int64_t nout, int64_t kin) {
+  return ((nout + 7) / 8) * ((kin + TUC - 1) / TUC);
 }
 extern "C" int64_t spx_layer_part_floats(int64_t d, int64_t ffn) {
-  int64_t m = mma_items(3 * d, d);
-  m = mma_items(ffn, d) > m ? mma_items(ffn, d) : m;
-  m = mma_items(d, ffn) > m ? mma_items(d, ffn) : m;
-  return m * 128;
+  int64_t m = tc_units(3 * d, d);
+  m = tc_units(ffn, d) > m ? tc_units(ffn, d) : m;
+  m = tc_units(d, ffn) > m ? tc_units(d, ffn) : m;
+  return m * 64;
 }
 extern "C" int64_t spx_layer_flag_ints(int64_t d, int64_t ffn) {
   const int64_t n = 3 * d > ffn ? 3 * d : ffn;
-  return (n + MRG - 1) / MRG;
+  return (n + 7) / 8;
 }
 
 // ---- begin(): append T rows (model.py:181-212): pending = emb[tok] + pe[pos]

@@ -466,419 +466,9 @@ static void launch_pdl(K kern, int grid, int block, size_t smem, cudaStream_t s,
   cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-// ------------------------------------------------- tensor-core GEMV (bf16 weights)
-//
-// The CUDA-core kernel above is issue-bound (≈1.4K warp-instructions per 8 KB
-// weight row: conversions, FFMA2, reductions).  For bf16 weights the product is
-// instead formed on the tensor cores with mma.sync m16n8k16 (bf16 in, f32
-// accumulate): D[a][n] = sum_k A[a][k] W[n][k] where the A rows are the input
-// rows split into a bf16 head and a bf16 tail (x = hi + lo + O(2^-17 |x|)),
-// so the result keeps fp32-level accuracy while the weights stay exact bf16.
-// One m16n8k16 covers 8 weight rows x 16 columns for up to 4 input rows: ~3
-// instructions per 256 bytes of weights, so the kernel is HBM-bound.
-//
-// Work: weight rows in groups of 32 (four n8 blocks) x contraction chunks of
-// 512 columns ("items", 32 KB of weights each); CTA c takes a contiguous item
-// range, so a group's chunks may straddle CTAs (split-K).  Straddling groups
-// write their partial sums to s_part; the last arriving CTA (s_flag counter)
-// adds the parts in part order -- deterministic.  Within a CTA the 8 warps
-// split each chunk's k-steps and are summed in warp order through smem.
-// Input rows: QKV/FFN1 LayerNorm'd and WO's attention rows are resident in
-// smem as hi/lo bf16; FFN2's input (FFN1's ReLU output, written by FFN1 as
-// hi/lo bf16 in the s_f row) is streamed chunk by chunk with the weights.
-constexpr int MT = 256, MW = MT / 32;  // threads / warps per CTA
-constexpr int MRG = 32;                // weight rows per group
-constexpr int MKC = 512;               // contraction columns per chunk
-constexpr int MRP = 4;                 // input rows per pass (A rows: 4 hi + 4 lo)
-constexpr int MPITCH = MKC * 2 + 16;   // smem bytes per weight / x row segment
-constexpr int MMA_SMEM = 225 * 1024;   // dynamic shared memory budget
-
-struct MmaGeom {
-  int nout, kin, ngroups, nkc, items, stages, slot_bytes;
-};
-
-__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1,
-                                               uint32_t a2, uint32_t a3, uint32_t b0,
-                                               uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void split_hilo(float x, __nv_bfloat16 &hi, __nv_bfloat16 &lo) {
-  hi = __float2bfloat16_rn(x);
-  lo = __float2bfloat16_rn(x - __bfloat162float(hi));
-}
-
-template <int EPI>
-__device__ __forceinline__ void mma_epilogue(const LayerParams &p, int row, int o, float v) {
-  if (EPI == EPI_FFN1) {
-    // ReLU output stored as hi/lo bf16 in the row's s_f slot (FFN2's A operand)
-    const float z = __fadd_rn(v, p.b1[o]);
-    __nv_bfloat16 hi, lo;
-    split_hilo(z > 0.f ? z : 0.f, hi, lo);
-    __nv_bfloat16 *sf = reinterpret_cast<__nv_bfloat16 *>(p.s_f) + (size_t)row * 2 * p.ffn;
-    sf[o] = hi;
-    sf[p.ffn + o] = lo;
-  } else {
-    gemv_epilogue<EPI>(p, row, o, v);
-  }
-}
-
-// CTA that owns item i (inverse of i0(c) = floor(c * items / G)).
-__device__ __forceinline__ int mma_cta_of(long long i, int G, int items) {
-  return (int)(((i + 1) * G - 1) / items);
-}
-
-template <int EPI>
-__global__ void __launch_bounds__(MT, 1) gemv_mma_kernel(LayerParams p, MmaGeom g) {
-  constexpr bool XS = EPI == EPI_FFN2;      // streamed input rows
-  extern __shared__ __align__(1024) unsigned char smem[];
-  unsigned char *ring = smem;
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)g.stages * g.slot_bytes);
-  const int xres_pitch = (g.kin + 8) * 2;   // bytes per resident hi/lo row
-  unsigned char *xres = reinterpret_cast<unsigned char *>(full + g.stages);
-  float *red = reinterpret_cast<float *>(xres + (XS ? 0 : (size_t)MRP * 2 * xres_pitch));
-  float *scr = red + MW * 4 * 32;           // [MRP][MW]
-  int *rows = reinterpret_cast<int *>(scr + MRP * MW);
-  __shared__ int s_last;
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = gridDim.x, c = blockIdx.x;
-  const unsigned char *W = reinterpret_cast<const unsigned char *>(gemv_weights<EPI>(p));
-  const size_t wrow = (size_t)g.kin * 2;
-
-  // item range: even split (single pass, split-K allowed) or whole groups
-  int i0 = (int)((long long)c * g.items / G), i1 = (int)((long long)(c + 1) * g.items / G);
-  int q_issue = 0, q_cons = 0, job_base = 0;    // ring sequence counters
-  int nr_cur = 0;
-
-  auto issue = [&](int job, int nj) {       // warp 0
-    const int it = i0 + job % nj;
-    const int grp = it / g.nkc, kc = it % g.nkc;
-    const int rw0 = grp * MRG;
-    const int nrw = g.nout - rw0 < MRG ? g.nout - rw0 : MRG;
-    const int len = g.kin - kc * MKC < MKC ? g.kin - kc * MKC : MKC;
-    const uint32_t bytes = (uint32_t)len * 2;
-    const int slot = q_issue % g.stages;
-    unsigned char *dst = ring + (size_t)slot * g.slot_bytes;
-    if (lane == 0) mbar_arrive_expect_tx(&full[slot], bytes * nrw);
-    __syncwarp();
-    if (lane < nrw)
-      bulk_g2s(dst + lane * MPITCH, W + (size_t)(rw0 + lane) * wrow + (size_t)kc * MKC * 2, bytes,
-               &full[slot]);
-    ++q_issue;
-  };
-  auto issue_x = [&](int job, int nj, int slot, int r0, int nr) {   // warp 0, XS only
-    const int it = i0 + job % nj, kc = it % g.nkc;
-    const int len = g.kin - kc * MKC < MKC ? g.kin - kc * MKC : MKC;
-    const uint32_t bytes = (uint32_t)len * 2;
-    unsigned char *dst = ring + (size_t)slot * g.slot_bytes + MRG * MPITCH;
-    if (lane == 0) mbar_arrive_expect_tx(&full[slot], bytes * 2 * nr);
-    __syncwarp();
-    if (lane < 2 * nr) {
-      const int r = lane >> 1, h = lane & 1;
-      const __nv_bfloat16 *src = reinterpret_cast<const __nv_bfloat16 *>(p.s_f) +
-                                 (size_t)rows[r0 + r] * 2 * g.kin + (size_t)h * g.kin +
-                                 (size_t)kc * MKC;
-      bulk_g2s(dst + lane * MPITCH, src, bytes, &full[slot]);
-    }
-  };
-
-  if (tid == 0) {
-    for (int s = 0; s < g.stages; ++s) mbar_init(&full[s], XS ? 2 : 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  int nj = i1 - i0;
-  int pre = 0;
-  if (EPI != EPI_QKV && nj > 0 && !flag_set(p.done) && warp == 0)
-    for (; pre < (nj < g.stages ? nj : g.stages); ++pre) issue(pre, nj);
-  pdl_wait();
-  const bool skip = flag_set(p.done);
-  pdl_trigger();
-  int nrows = skip ? 0 : cta_row_set(p, rows);
-  const int npass = (nrows + MRP - 1) / MRP;
-  if (npass > 1) {
-    // several passes: whole groups per CTA so passes never share partials
-    const int g0 = (int)((long long)c * g.ngroups / G), g1 = (int)((long long)(c + 1) * g.ngroups / G);
-    i0 = g0 * g.nkc;
-    i1 = g1 * g.nkc;
-  }
-  const int njn = i1 - i0;
-  const int total = npass * njn;
-  // drain prefetched stages that turned out useless (exit, no rows, or the
-  // item split changed); completes their phases so the ring stays in sync
-  if (warp == 0) {
-    if (pre > 0 && (skip || total == 0 || npass > 1)) {
-      for (int j = 0; j < pre; ++j) {
-        const int slot = j % g.stages;
-        if (XS && lane == 0) mbar_arrive(&full[slot]);
-        mbar_wait(&full[slot], (j / g.stages) & 1);
-      }
-      q_cons = pre;                          // warp 0's view; broadcast below
-    } else if (pre > 0 && XS) {
-      nr_cur = nrows < MRP ? nrows : MRP;
-      for (int j = 0; j < pre; ++j) issue_x(j, nj, j % g.stages, 0, nr_cur);
-    }
-  }
-  // every thread learns the drained count
-  __shared__ int s_drained;
-  if (tid == 0) s_drained = (pre > 0 && (skip || total == 0 || npass > 1)) ? pre : 0;
-  __syncthreads();
-  q_cons = s_drained;
-  job_base = q_cons;
-  if (warp == 0 && s_drained) q_issue = s_drained;
-  if (skip) return;
-  nj = njn;
-  if (warp == 0) {
-    // top the ring up (jobs counted from job_base)
-    const int have = s_drained ? 0 : pre;
-    for (int job = have; job < (total < g.stages ? total : g.stages); ++job) {
-      const int slot = q_issue % g.stages;
-      issue(job, nj);
-      if (XS) {
-        const int pass = job / nj, r0 = pass * MRP;
-        issue_x(job, nj, slot, r0, nrows - r0 < MRP ? nrows - r0 : MRP);
-      }
-    }
-  }
-
-  const int g8 = lane >> 2, cq = lane & 3;
-  for (int pass = 0; pass < npass; ++pass) {
-    const int r0 = pass * MRP;
-    const int nr = nrows - r0 < MRP ? nrows - r0 : MRP;
-    if (!XS) {
-      // resident input rows as hi/lo bf16 (LayerNorm first for QKV / FFN1)
-      const bool ln = EPI == EPI_QKV || EPI == EPI_FFN1;
-      const float *src = ln ? p.pending : p.s_att;
-      const float *gg = EPI == EPI_QKV ? p.ln1_g : p.ln2_g;
-      const float *bb = EPI == EPI_QKV ? p.ln1_b : p.ln2_b;
-      float mean[MRP], den[MRP];
-      if (ln) {
-        float s[MRP];
-#pragma unroll
-        for (int r = 0; r < MRP; ++r) {
-          s[r] = 0.f;
-          if (r < nr)
-            for (int j = tid; j < g.kin; j += MT) s[r] += __ldcg(src + (size_t)rows[r0 + r] * g.kin + j);
-        }
-#pragma unroll
-        for (int r = 0; r < MRP; ++r) {
-#pragma unroll
-          for (int m = 16; m; m >>= 1) s[r] += __shfl_xor_sync(0xffffffffu, s[r], m);
-          if (lane == 0) scr[r * MW + warp] = s[r];
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < MRP; ++r) {
-          float t = 0.f;
-#pragma unroll
-          for (int w = 0; w < MW; ++w) t += scr[r * MW + w];
-          mean[r] = t / (float)g.kin;
-          s[r] = 0.f;
-          if (r < nr)
-            for (int j = tid; j < g.kin; j += MT) {
-              const float cc = __ldcg(src + (size_t)rows[r0 + r] * g.kin + j) - mean[r];
-              s[r] = fmaf(cc, cc, s[r]);
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < MRP; ++r) {
-#pragma unroll
-          for (int m = 16; m; m >>= 1) s[r] += __shfl_xor_sync(0xffffffffu, s[r], m);
-          if (lane == 0) scr[r * MW + warp] = s[r];
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < MRP; ++r) {
-          float t = 0.f;
-#pragma unroll
-          for (int w = 0; w < MW; ++w) t += scr[r * MW + w];
-          den[r] = sqrtf(t / (float)g.kin + 1e-5f);
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < MRP; ++r) {
-        __nv_bfloat16 *hrow = reinterpret_cast<__nv_bfloat16 *>(xres + (size_t)(r * 2) * xres_pitch);
-        __nv_bfloat16 *lrow = reinterpret_cast<__nv_bfloat16 *>(xres + (size_t)(r * 2 + 1) * xres_pitch);
-        for (int j = tid; j < g.kin; j += MT) {
-          float v = 0.f;
-          if (r < nr) {
-            v = __ldcg(src + (size_t)rows[r0 + r] * g.kin + j);
-            if (ln) v = ln_elem(v - mean[r], den[r], gg[j], bb[j]);
-          }
-          __nv_bfloat16 hi, lo;
-          split_hilo(v, hi, lo);
-          hrow[j] = hi;
-          lrow[j] = lo;
-        }
-      }
-      __syncthreads();
-    }
-    float D[4][4];
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) D[b][e] = 0.f;
-    for (int j = 0; j < nj; ++j) {
-      const int job = pass * nj + j;
-      const int seq = job_base + job, slot = seq % g.stages;
-      const int it = i0 + j, grp = it / g.nkc, kc = it % g.nkc;
-      const int len = g.kin - kc * MKC < MKC ? g.kin - kc * MKC : MKC;
-      const int nrw = g.nout - grp * MRG < MRG ? g.nout - grp * MRG : MRG;
-      const int nblk = (nrw + 7) >> 3;
-      mbar_wait(&full[slot], (seq / g.stages) & 1);
-      const unsigned char *wb = ring + (size_t)slot * g.slot_bytes;
-      const unsigned char *xb;
-      int xp, xc0;
-      if (XS) { xb = wb + MRG * MPITCH; xp = MPITCH; xc0 = 0; }
-      else { xb = xres; xp = xres_pitch; xc0 = kc * MKC; }
-      const int ks = len >> 4;
-      const int s0 = warp * ks / MW, s1 = (warp + 1) * ks / MW;
-      // A-row g8: input row (g8 & 3), head (g8 < 4) or tail (g8 >= 4)
-      const bool arow = (g8 & 3) < nr;
-      const unsigned char *xa = xb + (size_t)((g8 & 3) * 2 + (g8 >> 2)) * xp + (size_t)(xc0 + 2 * cq) * 2;
-      const unsigned char *wa = wb + (size_t)g8 * MPITCH + 4 * cq;
-      for (int s = s0; s < s1; ++s) {
-        const int k = s * 16;
-        uint32_t a0 = 0u, a2 = 0u;
-        if (arow) {
-          a0 = *reinterpret_cast<const uint32_t *>(xa + k * 2);
-          a2 = *reinterpret_cast<const uint32_t *>(xa + k * 2 + 16);
-        }
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          if (b < nblk) {
-            const unsigned char *wr = wa + (size_t)b * 8 * MPITCH + k * 2;
-            const uint32_t b0 = *reinterpret_cast<const uint32_t *>(wr);
-            const uint32_t b1 = *reinterpret_cast<const uint32_t *>(wr + 16);
-            mma_bf16_16816(D[b], a0, 0u, a2, 0u, b0, b1);
-          }
-        }
-      }
-      __syncthreads();                         // slot consumed by every warp
-      if (warp == 0 && q_issue - job_base < total) {
-        const int nxt = q_issue - job_base;
-        const int nslot = q_issue % g.stages;
-        issue(nxt, nj);
-        if (XS) {
-          const int npas = nxt / nj, nr0 = npas * MRP;
-          issue_x(nxt, nj, nslot, nr0, nrows - nr0 < MRP ? nrows - nr0 : MRP);
-        }
-      }
-      if (kc == g.nkc - 1 || j == nj - 1) {
-        // group finished in this CTA: combine head + tail, then the warps
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const float v0 = D[b][0] + __shfl_xor_sync(0xffffffffu, D[b][0], 16);
-          const float v1 = D[b][1] + __shfl_xor_sync(0xffffffffu, D[b][1], 16);
-          if (lane < 16) {
-            red[(warp * 4 + b) * 32 + lane * 2] = v0;
-            red[(warp * 4 + b) * 32 + lane * 2 + 1] = v1;
-          }
-#pragma unroll
-          for (int e = 0; e < 4; ++e) D[b][e] = 0.f;
-        }
-        __syncthreads();
-        const long long gi0 = (long long)grp * g.nkc;
-        const int first = npass > 1 ? c : mma_cta_of(gi0, G, g.items);
-        const int last = npass > 1 ? c : mma_cta_of(gi0 + g.nkc - 1, G, g.items);
-        const int nparts = last - first + 1;
-        float v = 0.f;
-        int idx = tid, row = -1, o = -1;
-        if (idx < 128) {
-          const int b = idx >> 5, l = (idx & 31) >> 1, e = idx & 1;
-#pragma unroll
-          for (int w = 0; w < MW; ++w) v += red[(w * 4 + b) * 32 + l * 2 + e];
-          const int r = l >> 2, n = b * 8 + (l & 3) * 2 + e;
-          if (r < nr && n < nrw) { row = rows[r0 + r]; o = grp * MRG + n; }
-        }
-        if (nparts == 1) {
-          if (row >= 0) mma_epilogue<EPI>(p, row, o, v);
-        } else {
-          float *part = p.s_part + (size_t)gi0 * 128;
-          if (idx < 128) part[(c - first) * 128 + idx] = v;
-          __threadfence();
-          __syncthreads();
-          if (tid == 0) s_last = atomicAdd(p.s_flag + grp, 1) == nparts - 1;
-          __syncthreads();
-          if (s_last) {
-            __threadfence();
-            if (idx < 128) {
-              float t = 0.f;
-              for (int q = 0; q < nparts; ++q) t += __ldcg(part + q * 128 + idx);
-              if (row >= 0) mma_epilogue<EPI>(p, row, o, t);
-            }
-            if (tid == 0) p.s_flag[grp] = 0;
-          }
-        }
-      }
-    }
-  }
-
-  if (EPI == EPI_FFN2) {
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      s_last = atomicAdd(p.nrows, 1) == G - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      for (int i = tid; i < nrows; i += MT) p.frontier[rows[i]] = p.layer + 1;
-      if (p.cur_hidden && p.new_row) {
-        const int nw = *reinterpret_cast<const volatile int32_t *>(p.new_row);
-        if (nw >= 0)
-          for (int j = tid; j < p.d; j += MT) p.cur_hidden[j] = __ldcg(p.pending + (size_t)nw * p.d + j);
-      }
-      if (tid == 0) *p.nrows = 0;
-    }
-  }
-}
+#include "spx_gemv_tc.cuh"
 
 // ------------------------------------------------------------------ host side
-
-static MmaGeom mma_geom(int nout, int kin, int sms, int max_ctx, bool xs, int &grid,
-                        size_t &smem) {
-  MmaGeom g;
-  g.nout = nout;
-  g.kin = kin;
-  g.ngroups = (nout + MRG - 1) / MRG;
-  g.nkc = (kin + MKC - 1) / MKC;
-  g.items = g.ngroups * g.nkc;
-  g.slot_bytes = (MRG * MPITCH + (xs ? 2 * MRP * MPITCH : 0) + 127) / 128 * 128;
-  const size_t fixed = (xs ? 0 : (size_t)MRP * 2 * (kin + 8) * 2) + MW * 4 * 32 * 4 +
-                       MRP * MW * 4 + (size_t)max_ctx * 4 + 16 * 8 + 1024;
-  int st = (int)((MMA_SMEM - fixed) / g.slot_bytes);
-  g.stages = st > 8 ? 8 : st;
-  grid = g.items < sms ? g.items : sms;
-  smem = (size_t)g.stages * g.slot_bytes + g.stages * 8 + fixed - 1024;
-  return g;
-}
-
-static bool mma_layer_supported(const LayerParams &p) {
-  if (p.d % 16 || p.ffn % 16 || !p.s_part || !p.s_flag) return false;
-  int grid;
-  size_t smem;
-  const MmaGeom g = mma_geom(3 * p.d, p.d, 148, p.max_ctx, false, grid, smem);
-  return g.stages >= 2;
-}
-
-template <int EPI>
-static void launch_mma(const LayerParams &p, int nout, int kin, int sms, cudaStream_t s) {
-  int grid;
-  size_t smem;
-  const MmaGeom g = mma_geom(nout, kin, sms, p.max_ctx, EPI == EPI_FFN2, grid, smem);
-  cudaFuncSetAttribute(gemv_mma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
-  launch_pdl(gemv_mma_kernel<EPI>, grid, MT, smem, s, p, g);
-}
 
 template <typename TW>
 static GemvGeom gemv_geom(int nout, int kin, int sms, int max_ctx, int &grid, size_t &smem) {
@@ -934,14 +524,14 @@ static void launch_gemv(const LayerParams &p, int nout, int kin, int sms, cudaSt
 
 template <typename TW>
 static void launch_layer_fast(const LayerParams &p, int sms, cudaStream_t s) {
-  if (std::is_same<TW, __nv_bfloat16>::value && mma_layer_supported(p)) {
-    launch_mma<EPI_QKV>(p, 3 * p.d, p.d, sms, s);
+  if (std::is_same<TW, __nv_bfloat16>::value && tc_layer_supported(p)) {
+    launch_tc<EPI_QKV>(p, 3 * p.d, p.d, sms, s);
     const size_t ab = (size_t)p.max_ctx * 8 + (size_t)(p.d / p.nh) * 4;
     cudaFuncSetAttribute(attn_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);
     launch_pdl(attn_fast_kernel, 2 * sms, AT, ab, s, p);
-    launch_mma<EPI_WO>(p, p.d, p.d, sms, s);
-    launch_mma<EPI_FFN1>(p, p.ffn, p.d, sms, s);
-    launch_mma<EPI_FFN2>(p, p.d, p.ffn, sms, s);
+    launch_tc<EPI_WO>(p, p.d, p.d, sms, s);
+    launch_tc<EPI_FFN1>(p, p.ffn, p.d, sms, s);
+    launch_tc<EPI_FFN2>(p, p.d, p.ffn, sms, s);
     return;
   }
   launch_gemv<TW, EPI_QKV>(p, 3 * p.d, p.d, sms, s);

@@ -74,7 +74,8 @@ def test_fast_layers_match_strict(dims):
         with numerics.using(mode):
             st = DecodeState(m)
             res = []
-            for toks, depth in [([1, 2, 3, 4, 5], 3), ([6], 1), ([7], 3), ([8], 3)]:
+            for toks, depth in [(list(range(1, 13)), 3), ([6], 1), ([7], 3), ([8], 3), ([9], 1),
+                                ([10], 1), ([11], 3)]:
                 st.begin(toks)
                 for l in range(depth):
                     res.append(st.run_layer(l).cpu().numpy())
