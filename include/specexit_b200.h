@@ -187,6 +187,26 @@ int spx_final_norm(const float *hidden, int64_t hidden_stride, const float *g, c
 int spx_path_and(const uint8_t *node_fired, const int32_t *path_ptr, const int32_t *path_nodes,
                  const uint8_t *live, int64_t P, uint8_t *path_fire, void *stream);
 
+/* K7b -- rows that need the full-head check after the path AND
+ * (src/specexit/tree.py:221-227, _verify_path :274-283): node_gate[j] = 1 for
+ * every node j on a path with path_fire[p] != 0, node_gate[0] (the root) = 1
+ * when any path fires, else 0.  n_nodes includes the root. */
+int spx_tree_gate(const uint8_t *path_fire, const int32_t *path_ptr, const int32_t *path_nodes,
+                  int64_t P, int64_t n_nodes, uint8_t *node_gate, void *stream);
+
+/* Tree-node evaluation (src/specexit/tree.py:213-220; extract_features
+ * src/specexit/predictor.py:42-52, predictor_forward :97-103): for each live
+ * node i (node = live_idx[i]) take its K logits (row i of `logits`, the K6
+ * output), build features against prev[node] (updated in place), evaluate
+ * the MLP (policy SPX_POLICY_MLP: w1/b1/w2/b2, fire iff z2 >= z_cut) or the
+ * constant policy (SPX_POLICY_CONST: fire iff const_prob > threshold), write
+ * fired[node] and prob_out[node] (optional).  prev (n_nodes, K), fired and
+ * prob_out (n_nodes) are indexed by node. */
+int spx_tree_node_eval(const float *logits, const int32_t *live_idx, int64_t n_live, float *prev,
+                       const float *w1, const float *b1, const float *w2, float b2, float z_cut,
+                       int32_t policy, double const_prob, double threshold, double *prob_out,
+                       uint8_t *fired, int32_t *err, int64_t K, int64_t H, void *stream);
+
 /* Synthetic weights on device: reference rng.uniform (src/specexit/rng.py:24-27)
  * of stream `seed` over a (rows, cols) row-major tensor, written as bf16 (or
  * f32 when out_f32 != 0).  transpose != 0 stores element (r, c) at

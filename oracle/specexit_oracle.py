@@ -417,8 +417,8 @@ def topk_from_logits(logits, k):
 
 
 class DecodeState:
-    """model.py:155-286 restated (causal rows only: the autoregressive
-    engine path).  Lazy KV completion through per-position frontiers."""
+    """model.py:155-286 restated: lazy KV completion through per-position
+    frontiers; tree rows with explicit ancestor lists, freezing, compaction."""
 
     def __init__(self, cfg, t, pos_encoding):
         self.cfg, self.t, self.pe = cfg, t, pos_encoding
@@ -429,22 +429,54 @@ class DecodeState:
         self.frontier = np.zeros(C, np.int64)
         self.n = 0
         self.new_rows = []
+        self.attn_index = {}
+        self.frozen = set()
 
-    def begin(self, tokens):
-        """model.py:181-212."""
+    def begin(self, tokens, pos_ids=None, attn_lists=None):
+        """model.py:181-212 (pos_ids / attn_lists: tree rows, :201-211)."""
         rows = list(range(self.n, self.n + len(tokens)))
-        self.pending[rows] = self.t["embedding"][np.asarray(tokens)] + self.pe[rows]
+        if self.n + len(tokens) > self.cfg.max_context:
+            raise ValueError("context overflow")
+        pos = rows if pos_ids is None else list(pos_ids)
+        self.pending[rows] = self.t["embedding"][np.asarray(tokens)] + self.pe[pos]
         self.frontier[rows] = 0
+        for j, p in enumerate(rows):
+            if attn_lists is not None and attn_lists[j] is not None:
+                idx = np.asarray(sorted(set(attn_lists[j]) | {p}), dtype=np.int64)
+                if idx.max() > p:
+                    raise ValueError("attention index must not look ahead")
+                self.attn_index[p] = idx
         self.n += len(tokens)
         self.new_rows = rows
         return rows
 
+    def freeze(self, positions):
+        """model.py:214-215."""
+        self.frozen.update(positions)
+
+    def unfreeze_all(self):
+        """model.py:217-218."""
+        self.frozen.clear()
+
     def run_layer(self, l):
         """model.py:220-233."""
-        rows = [p for p in range(self.n) if self.frontier[p] == l]
+        rows = [p for p in range(self.n) if self.frontier[p] == l and p not in self.frozen]
         if rows:
             self._advance(l, rows)
         return self.pending[self.new_rows].copy()
+
+    def compact(self, keep_new_rows, n_committed):
+        """model.py:272-286."""
+        keep = list(keep_new_rows)
+        dest = list(range(n_committed, n_committed + len(keep)))
+        self.k[:, dest] = self.k[:, keep]
+        self.v[:, dest] = self.v[:, keep]
+        self.pending[dest] = self.pending[keep]
+        self.frontier[dest] = self.frontier[keep]
+        self.attn_index = {}
+        self.n = n_committed + len(keep)
+        self.new_rows = []
+        self.frozen.clear()
 
     def _advance(self, l, rows):
         """model.py:235-270."""
@@ -459,7 +491,10 @@ class DecodeState:
         scale = np.float32(1.0 / math.sqrt(dh))
         attn = np.empty_like(x)
         for j, p in enumerate(rows):
-            kc, vc = self.k[l, : p + 1], self.v[l, : p + 1]
+            ctx = self.attn_index.get(p)
+            if ctx is None:
+                ctx = np.arange(p + 1)
+            kc, vc = self.k[l, ctx], self.v[l, ctx]
             out = np.empty(cfg.hidden_dim, np.float32)
             for hh in range(nh):
                 s = slice(hh * dh, (hh + 1) * dh)
@@ -594,6 +629,220 @@ class ExitEngineOracle:
             self.context[-1] = int(tok)
             self.next_in = int(tok)
         return trace
+
+
+# ---------------------------------------------------------------- tree mode
+
+
+def propose_topk(cfg, t, pe, context, k):
+    """speculation.py:62-84: a FRESH full draft forward over ``context``
+    (:63-68), top-k with lower-id ties, probs = softmax_1d(logits)[ids]."""
+    st = DecodeState(cfg, t, pe)
+    st.begin(list(context))
+    out = None
+    for l in range(cfg.num_layers):
+        out = st.run_layer(l)
+    logits = full_head_logits(t, out[-1])
+    ids = topk_from_logits(logits, k)
+    probs = softmax_1d(logits)[ids]
+    return tuple(int(i) for i in ids), tuple(float(p) for p in probs)
+
+
+@dataclass
+class TreeNodeO:
+    """speculation.py:28-33."""
+    token: int
+    parent: int
+    depth: int
+    prob: float = 0.0
+
+
+def build_token_tree(cfg, t, pe, context, branching):
+    """speculation.py:87-125: depth-first expansion, then (depth, creation)
+    order; node 0 is the root (last context token)."""
+    nodes = [TreeNodeO(int(context[-1]), -1, 0)]
+    context = list(context)
+
+    def expand(idx, path_tokens, depth):
+        if depth == len(branching):
+            return
+        toks, probs = propose_topk(cfg, t, pe, context + path_tokens, branching[depth])
+        kids = []
+        for tok, pr in zip(toks, probs):
+            nodes.append(TreeNodeO(tok, idx, depth + 1, pr))
+            kids.append(len(nodes) - 1)
+        for cid, tok in zip(kids, toks):
+            expand(cid, path_tokens + [tok], depth + 1)
+
+    expand(0, [], 0)
+    order = sorted(range(len(nodes)), key=lambda i: (nodes[i].depth, i))
+    remap = {old: new for new, old in enumerate(order)}
+    return [TreeNodeO(nodes[o].token, remap[nodes[o].parent] if nodes[o].parent >= 0 else -1,
+                      nodes[o].depth, nodes[o].prob) for o in order]
+
+
+def enumerate_paths(nodes):
+    """speculation.py:36-54, :127-130: root-to-leaf paths (root excluded)."""
+    parents = {n.parent for n in nodes}
+    paths = []
+    for leaf in (i for i in range(len(nodes)) if i not in parents):
+        path, idx = [], leaf
+        while idx != 0:
+            path.append(idx)
+            idx = nodes[idx].parent
+        paths.append(path[::-1])
+    return paths
+
+
+def merge_paths(nodes, dcfg, draft, dpe, context, k):
+    """tree.py:49-89 -> (paths, per-path verify specs, per-node feature ids).
+    Feature ids = draft top-k at the node's own context (cached per node);
+    verify spec = children for internal nodes, the feature ids for leaves."""
+    paths = enumerate_paths(nodes)
+    child_map = {}
+    for j, n in enumerate(nodes):
+        child_map.setdefault(n.parent, []).append(j)
+    feat = {}
+    specs = []
+    for path in paths:
+        ps = []
+        for idx in path:
+            if idx not in feat:
+                upto = path[: path.index(idx) + 1]
+                feat[idx] = propose_topk(dcfg, draft, dpe,
+                                         list(context) + [nodes[i].token for i in upto], k)[0]
+            kids = child_map.get(idx)
+            ps.append(tuple(nodes[c].token for c in kids) if kids else feat[idx])
+        specs.append(ps)
+    return paths, specs, feat
+
+
+@dataclass
+class TreeStepO:
+    """tree.py:37-46 (+ the per-call probability log of the golden)."""
+    accepted_tokens: list
+    correction_token: int
+    path_exit_layers: list
+    accepted_path: int
+    predictor_evals: int
+    num_paths: int
+    max_path_len: int
+    scheduled_layer_count: int
+    probs: list = field(default_factory=list)
+
+
+class TreeEngineOracle:
+    """tree.py:133-302 restated; ``policy``: dict layer->PredictorWeights,
+    "never" or "always" (engine.py:67-92)."""
+
+    def __init__(self, target_cfg, target, draft_cfg, draft, policy, branching=(3, 2), k=4,
+                 threshold=0.5, schedule_mode="all", exit_counts=None,
+                 schedule_config=ScheduleConfig()):
+        self.tc, self.t, self.dc, self.d = target_cfg, target, draft_cfg, draft
+        self.policy, self.branching, self.k, self.thr = policy, tuple(branching), k, threshold
+        self.mode, self.counts, self.sc = schedule_mode, exit_counts, schedule_config
+        self.tpe = sinusoidal_encoding(target_cfg.max_context, target_cfg.hidden_dim)
+        self.dpe = sinusoidal_encoding(draft_cfg.max_context, draft_cfg.hidden_dim)
+        self.online = OnlineState(target_cfg.num_layers, schedule_config)
+
+    def start(self, prompt):
+        """tree.py:153-163."""
+        prompt = list(prompt)
+        self.ts = DecodeState(self.tc, self.t, self.tpe)
+        if len(prompt) > 1:
+            self.ts.begin(prompt[:-1])
+            for l in range(self.tc.num_layers):
+                self.ts.run_layer(l)
+        self.context = prompt
+
+    def _prob(self, l, fv):
+        if self.policy == "never":
+            return 0.0
+        if self.policy == "always":
+            return 1.0
+        if l not in self.policy:
+            raise KeyError(f"no predictor for active layer {l}")
+        return predictor_forward(self.policy[l], fv)
+
+    def _argmax(self, h):
+        return int(np.argmax(full_head_logits(self.t, h)))
+
+    def step(self):
+        """tree.py:171-266."""
+        L = self.tc.num_layers
+        nodes = build_token_tree(self.dc, self.d, self.dpe, self.context, self.branching)
+        paths, specs, feat = merge_paths(nodes, self.dc, self.d, self.dpe, self.context, self.k)
+        n_nodes = len(nodes)
+        m = len(self.context) - 1
+        tokens = [n.token for n in nodes]
+        pos_ids = [m + n.depth for n in nodes]
+        attn, anc = [None], {0: [0]}
+        for j in range(1, n_nodes):
+            anc[j] = anc[nodes[j].parent] + [j]
+            attn.append(list(range(m)) + [m + a for a in anc[j]])
+        rows = self.ts.begin(tokens, pos_ids=pos_ids, attn_lists=attn)
+        active = (list(range(L - 1)) if self.mode == "all"
+                  else active_layers(self.counts, self.online, self.sc))
+        aset = set(active)
+        prev = {j: None for j in range(1, n_nodes)}
+        live = set(range(len(paths)))
+        exit_layer = [L - 1] * len(paths)
+        preds = [None] * len(paths)
+        evals, log, hidden = 0, [], None
+        for l in range(L):
+            hidden = self.ts.run_layer(l)
+            if not live:
+                break
+            if l in aset and l <= L - 2:
+                live_nodes = sorted({j for p in live for j in paths[p]})
+                probs = {}
+                for j in live_nodes:
+                    lg = sliced_head_logits(self.t, hidden[j], feat[j])
+                    pv = prev[j] if prev[j] is not None else uniform_probs(len(feat[j]))
+                    fv = extract_features(lg, pv)
+                    prev[j] = fv.local_probs
+                    probs[j] = self._prob(l, fv)
+                    log.append([l, probs[j]])
+                    evals += 1
+                for p in sorted(live):
+                    if hypertoken_exit_decision([probs[j] for j in paths[p]], self.thr):
+                        chain = [self._argmax(hidden[0])]
+                        ok = True
+                        for idx, spec in zip(paths[p], specs[p]):
+                            am = self._argmax(hidden[idx])
+                            if am not in spec:
+                                ok = False
+                                break
+                            chain.append(am)
+                        if ok:
+                            exit_layer[p], preds[p] = l, chain
+                            live.discard(p)
+                keep = {j for p in live for j in paths[p]} | ({0} if live else set())
+                self.ts.freeze(rows[j] for j in range(n_nodes) if j not in keep)
+            if not live:
+                break
+        for p in list(live):
+            preds[p] = [self._argmax(hidden[0])] + [self._argmax(hidden[j]) for j in paths[p]]
+        self.ts.unfreeze_all()
+        best_p, best_len = 0, -1
+        for p, path in enumerate(paths):
+            n_ok = 0
+            for t_, idx in enumerate(path):
+                if nodes[idx].token == preds[p][t_]:
+                    n_ok += 1
+                else:
+                    break
+            if n_ok > best_len:
+                best_p, best_len = p, n_ok
+        acc_nodes = paths[best_p][:best_len]
+        acc = [nodes[j].token for j in acc_nodes]
+        corr = preds[best_p][best_len]
+        self.ts.compact([rows[0]] + [rows[j] for j in acc_nodes], m)
+        self.context.extend(acc + [corr])
+        for _ in range(len(acc) + 1):
+            update_online(self.online, exit_layer[best_p])
+        return TreeStepO(acc, corr, exit_layer, best_p, evals, len(paths),
+                         max(len(p) for p in paths), max(len(aset), 1), log)
 
 
 # ---------------------------------------------------------------- weight files

@@ -102,6 +102,9 @@ def lib():
     L.spx_head_bias.argtypes = [_vp, _i32, _vp, _i64, _i64, _vp, _vp]
     L.spx_final_norm.argtypes = [_vp, _i64, _vp, _vp, _vp, _i64, _i64, _i32, _vp, _vp]
     L.spx_path_and.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _vp]
+    L.spx_tree_gate.argtypes = [_vp, _vp, _vp, _i64, _i64, _vp, _vp]
+    L.spx_tree_node_eval.argtypes = [_vp, _vp, _i64, _vp, _vp, _vp, _vp, _f32, _f32, _i32, _f64,
+                                     _f64, _vp, _vp, _vp, _i64, _i64, _vp]
     L.spx_init_uniform.argtypes = [_vp, _i32, _i64, _i64, _i32, ctypes.c_uint64, _f64, _f64, _vp]
     L.spx_version.restype = ctypes.c_char_p
     L.spx_predictor_mlp.argtypes = [_vp, _vp, _vp, _vp, _f32, _f32, _vp, _vp, _vp, _i64, _i64,

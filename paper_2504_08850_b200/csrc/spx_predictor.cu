@@ -601,3 +601,42 @@ extern "C" int spx_predictor_mlp(const float *feats, const float *w1, const floa
   mlp_kernel<<<(unsigned)B, 32, 0, (cudaStream_t)stream>>>(p, feats);
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
 }
+
+// Tree-node evaluation (tree.py:213-220): live node i's K merged logits (K6
+// output, live order) -> features against that node's carried probabilities
+// prev[node] (updated in place) -> MLP / constant policy -> fired[node],
+// prob[node].  One warp per live node; the per-node gather/scatter by
+// live_idx is fused so the tree engine needs no index kernels.
+namespace spx {
+__global__ void tree_node_eval_kernel(PredParams p, const float *logits, const int32_t *live_idx,
+                                      int n_live) {
+  const int i = blockIdx.x;
+  if (i >= n_live) return;
+  __shared__ float feats[3 * MAXK];
+  __shared__ float hs[MAXH];
+  const int lane = threadIdx.x, node = live_idx[i];
+  for (int c = lane; c < p.K; c += 32) feats[c] = logits[(size_t)i * p.K + c];
+  __syncwarp();
+  warp_row_tail(p, node, feats, p.w1, p.b1, p.w2, hs, lane);
+}
+}  // namespace spx
+
+extern "C" int spx_tree_node_eval(const float *logits, const int32_t *live_idx, int64_t n_live,
+                                  float *prev, const float *w1, const float *b1, const float *w2,
+                                  float b2, float z_cut, int32_t policy, double const_prob,
+                                  double threshold, double *prob_out, uint8_t *fired,
+                                  int32_t *err, int64_t K, int64_t H, void *stream) {
+  if (!logits || !live_idx || !prev || !fired || !err || n_live < 0 || K < 1 || K > MAXK)
+    return SPX_EINVAL;
+  if (policy == SPX_POLICY_MLP && (!w1 || !b1 || !w2 || H < 1 || H > MAXH)) return SPX_EINVAL;
+  if (policy != SPX_POLICY_MLP && policy != SPX_POLICY_CONST) return SPX_EINVAL;
+  if (n_live == 0) return 0;
+  PredParams p{};
+  p.prev = prev; p.w1 = w1; p.b1 = b1; p.w2 = w2; p.b2 = b2; p.z_cut = z_cut;
+  p.policy = policy; p.const_prob = const_prob; p.threshold = threshold;
+  p.prob_out = prob_out; p.fired = fired; p.err = err;
+  p.K = (int)K; p.H = policy == SPX_POLICY_MLP ? (int)H : 0;
+  tree_node_eval_kernel<<<(unsigned)n_live, 32, 0, (cudaStream_t)stream>>>(p, logits, live_idx,
+                                                                          (int)n_live);
+  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+}

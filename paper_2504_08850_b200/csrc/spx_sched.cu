@@ -97,6 +97,34 @@ extern "C" int spx_path_and(const uint8_t *node_fired, const int32_t *path_ptr,
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
 }
 
+// K7b: which rows need the full-head check after the path AND
+// (tree.py:221-227): every node on a firing live path, plus the root (its
+// argmax opens every path's chain) when any path fires.  One CTA; the
+// all-or-nothing writes of 1 race benignly.
+namespace spx {
+__global__ void tree_gate_kernel(const uint8_t *path_fire, const int32_t *path_ptr,
+                                 const int32_t *path_nodes, int P, int n_nodes,
+                                 uint8_t *node_gate) {
+  for (int j = threadIdx.x; j < n_nodes; j += blockDim.x) node_gate[j] = 0;
+  __syncthreads();
+  for (int p = threadIdx.x; p < P; p += blockDim.x) {
+    if (!path_fire[p]) continue;
+    node_gate[0] = 1;
+    for (int q = path_ptr[p]; q < path_ptr[p + 1]; ++q) node_gate[path_nodes[q]] = 1;
+  }
+}
+}  // namespace spx
+
+extern "C" int spx_tree_gate(const uint8_t *path_fire, const int32_t *path_ptr,
+                             const int32_t *path_nodes, int64_t P, int64_t n_nodes,
+                             uint8_t *node_gate, void *stream) {
+  if (!path_fire || !path_ptr || !path_nodes || !node_gate || P < 0 || n_nodes < 1)
+    return SPX_EINVAL;
+  spx::tree_gate_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(path_fire, path_ptr, path_nodes,
+                                                             (int)P, (int)n_nodes, node_gate);
+  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+}
+
 // Elementwise numpy-float32 exp (the softmax's exp, model.py:151), exposed so
 // the tests can compare the device restatement with the host's np.exp over
 // large input sweeps.

@@ -181,6 +181,19 @@ class DecodeState:
         self.frozen.zero_()
         self._largs = [self._layer_args(l) for l in range(self.model.config.num_layers)]
 
+    def reset(self):
+        """Empty the state (buffers kept): n = 0, no rows, nothing frozen."""
+        self.n = 0
+        self.n_ctx.zero_()
+        self.new_row.fill_(-1)
+        self.frontier.zero_()
+        self.frozen.zero_()
+        self.new_rows = []
+        if self.attn_ptr is not None:
+            self.attn_ptr = self.attn_idx = None
+            self._attn_lists = {}
+            self._largs = [self._layer_args(l) for l in range(self.model.config.num_layers)]
+
     def check(self):
         N.raise_device_error(self.err.item())
 

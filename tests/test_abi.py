@@ -18,7 +18,8 @@ def declared_symbols():
 def test_header_declares_the_operator_set():
     syms = declared_symbols()
     for s in ("spx_predictor_eval", "spx_verify", "spx_sched_update", "spx_sched_active",
-              "spx_tree_merged_logits", "spx_path_and", "spx_final_norm", "spx_extract_features",
+              "spx_tree_merged_logits", "spx_path_and", "spx_tree_gate", "spx_tree_node_eval",
+              "spx_final_norm", "spx_extract_features",
               "spx_predictor_mlp", "spx_init_uniform", "spx_version"):
         assert s in syms, s
 

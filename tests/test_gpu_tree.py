@@ -1,0 +1,190 @@
+"""GPU parity of the device TreeEngine (tree.py:133-302) against the
+reference's own TreeEngine runs (tests/golden/tree_tiny.json, made by
+tests/golden/make_tree_golden.py on the trained tiny pipeline artifacts).
+
+STRICT mode must reproduce every TreeStepResult field exactly and every
+predictor probability (in the reference's call order) within 1e-9 abs (the
+decision itself is exact: z2 >= z_cut).  FAST mode is held to the same step
+results on these streams (decisions are exact unless a probability sits
+within ~1e-6 of the threshold, which the golden margins exclude).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2504_08850_b200 as spx
+from paper_2504_08850_b200 import engine as E
+from paper_2504_08850_b200 import numerics
+from paper_2504_08850_b200 import tree as T
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+PIPE = os.path.join(GOLDEN, "tiny_pipeline")
+PROB_ATOL = 1e-9
+PROMPT = [84, 104, 101, 32]
+_MODELS = {}
+
+
+def models():
+    if not _MODELS:
+        _MODELS["t"] = spx.load_weights(os.path.join(PIPE, "target.spxw"))
+        _MODELS["d"] = spx.load_weights(os.path.join(PIPE, "draft.spxw"))
+        _MODELS["bank"] = spx.load_predictors(os.path.join(PIPE, "predictors.spxp"))
+        _MODELS["prof"] = spx.load_profile(os.path.join(PIPE, "profile.spxs"))
+    return _MODELS["t"], _MODELS["d"], _MODELS["bank"], _MODELS["prof"]
+
+
+def engine_for(case):
+    t, d, bank, prof = models()
+    pol = {"never_all": E.NeverExitPolicy(), "always_all": E.AlwaysExitPolicy()}.get(
+        case["case"], E.PredictorPolicy(bank))
+    eng = T.TreeEngine(t, d, pol, tuple(case["branching"]),
+                       E.EngineConfig(k=4, threshold=case["threshold"], schedule_mode=case["mode"]),
+                       profile=prof if case["mode"] == "two-level" else None,
+                       schedule_config=spx.ScheduleConfig(5, 1, 4))
+    eng.record_probs = True
+    return eng
+
+
+def step_fields(r):
+    return dict(accepted_tokens=r.accepted_tokens, correction_token=r.correction_token,
+                path_exit_layers=r.path_exit_layers, accepted_path=r.accepted_path,
+                predictor_evals=r.predictor_evals, num_paths=r.num_paths,
+                max_path_len=r.max_path_len, scheduled_layer_count=r.scheduled_layer_count)
+
+
+def _cases(golden):
+    return golden.json("tree_tiny.json")["cases"]
+
+
+@pytest.mark.parametrize("ci", range(15))
+def test_tree_engine_strict_matches_reference(golden, ci):
+    case = _cases(golden)[ci]
+    eng = engine_for(case)
+    with numerics.using("strict"):
+        eng.start(case["prompt"])
+        for s, ref in enumerate(case["steps"]):
+            n0 = len(eng.prob_log)
+            res = eng.step()
+            exp = {k: ref[k] for k in step_fields(res)}
+            assert step_fields(res) == exp, (case["case"], s)
+            got = eng.prob_log[n0:]
+            assert [l for l, _ in got] == [l for l, _ in ref["probs"]], (case["case"], s)
+            for (_, p), (_, q) in zip(got, ref["probs"]):
+                assert abs(p - q) <= PROB_ATOL, (case["case"], s, p, q)
+    assert eng.context == case["context"]
+    assert eng.online.queue == case["online_queue"]
+
+
+@pytest.mark.parametrize("ci", [0, 4, 9])
+def test_tree_engine_fast_matches_reference(golden, ci):
+    case = _cases(golden)[ci]
+    eng = engine_for(case)
+    with numerics.using("fast"):
+        eng.start(case["prompt"])
+        for s, ref in enumerate(case["steps"]):
+            res = eng.step()
+            assert step_fields(res) == {k: ref[k] for k in step_fields(res)}, (case["case"], s)
+
+
+def test_merge_paths_structure():
+    """tests/test_tree.py:16-26."""
+    _, d, _, _ = models()
+    with numerics.using("strict"):
+        tree = spx.build_token_tree(d, PROMPT, (3, 2))
+        hts = T.merge_paths(tree, d, PROMPT, k=4)
+    assert len(hts) == 6
+    for ht in hts:
+        assert len(ht.path) == 2 == len(ht.per_node_spec)
+        kids = tree.children(ht.path[0])
+        assert ht.per_node_spec[0].tokens == tuple(tree.nodes[c].token for c in kids)
+        assert len(ht.per_node_spec[1].tokens) == 4
+
+
+def test_merge_paths_needs_draft_for_leaves():
+    """tests/test_tree.py:29-32."""
+    _, d, _, _ = models()
+    tree = spx.build_token_tree(d, PROMPT, (2,))
+    with pytest.raises(ValueError):
+        T.merge_paths(tree)
+
+
+def test_tree_no_exit_equals_greedy():
+    """tests/test_tree.py:76-80."""
+    t, d, _, _ = models()
+    with numerics.using("strict"):
+        base, _ = E.greedy_generate(t, PROMPT, 30)
+        toks, _ = T.TreeEngine(t, d, E.NeverExitPolicy(), (3, 2)).generate(PROMPT, 30)
+    assert toks == base
+
+
+def test_tree_self_draft_accepts():
+    """tests/test_tree.py:83-89."""
+    t, _, _, _ = models()
+    with numerics.using("strict"):
+        _, steps = T.TreeEngine(t, t, E.NeverExitPolicy(), (1,)).generate(PROMPT, 12)
+    assert all(len(s.accepted_tokens) >= 1 for s in steps)
+
+
+def test_tree_oracle_policy_lossless():
+    """tests/test_tree.py:92-96 (host-policy path of the engine)."""
+    t, d, _, _ = models()
+    with numerics.using("strict"):
+        base, _ = E.greedy_generate(t, PROMPT, 12)
+        toks, _ = T.TreeEngine(t, d, E.OraclePolicy(t), (2, 2)).generate(PROMPT, 12)
+    assert toks == base
+
+
+def test_mapping_complexity_bound():
+    """tests/test_tree.py:99-104."""
+    t, d, _, _ = models()
+    _, steps = T.TreeEngine(t, d, E.NeverExitPolicy(), (3, 2)).generate(PROMPT, 20)
+    for s in steps:
+        assert s.predictor_evals <= s.num_paths * s.scheduled_layer_count * s.max_path_len
+
+
+def test_merged_mapping_dedups_shared_feature_ids():
+    """K6 reads each unique LM-head row once: sibling nodes share most of their
+    draft top-k, so the unique count is below the pair count."""
+    t, d, bank, _ = models()
+    eng = T.TreeEngine(t, d, E.PredictorPolicy(bank), (3, 2))
+    eng.start(PROMPT)
+    eng.step()
+    assert eng.last_unique_ids <= eng.last_pairs
+
+
+def test_tree_missing_predictor_raises_keyerror():
+    t, d, bank, _ = models()
+    partial = {l: w for l, w in bank.items() if l != 0}
+    eng = T.TreeEngine(t, d, E.PredictorPolicy(partial), (2,))
+    eng.start(PROMPT)
+    with pytest.raises(KeyError):
+        eng.step()
+
+
+def test_two_level_needs_profile():
+    t, d, _, _ = models()
+    with pytest.raises(ValueError):
+        T.TreeEngine(t, d, E.NeverExitPolicy(), (2,), E.EngineConfig(schedule_mode="two-level"))
+
+
+def test_tree_gate_and_node_eval_kernels():
+    """K7b and the node-eval kernel in isolation against numpy."""
+    import torch
+    from paper_2504_08850_b200 import _native as N
+    paths = [[1, 3], [1, 4], [2, 5]]
+    ptr = torch.tensor([0, 2, 4, 6], dtype=torch.int32, device="cuda")
+    nodes = torch.tensor([1, 3, 1, 4, 2, 5], dtype=torch.int32, device="cuda")
+    for fire in ([0, 0, 0], [1, 0, 0], [0, 1, 1]):
+        pf = torch.tensor(fire, dtype=torch.uint8, device="cuda")
+        gate = torch.full((6,), 7, dtype=torch.uint8, device="cuda")
+        N.check(N.lib().spx_tree_gate(N.ptr(pf), N.ptr(ptr), N.ptr(nodes), 3, 6, N.ptr(gate),
+                                      N.stream_ptr()), "spx_tree_gate")
+        exp = np.zeros(6, np.uint8)
+        for p, f in enumerate(fire):
+            if f:
+                exp[0] = 1
+                exp[paths[p]] = 1
+        assert gate.cpu().numpy().tolist() == exp.tolist()

@@ -176,3 +176,38 @@ def test_tiny_pipeline_trace_end_to_end(oracle):
     for rec, ref in zip(out, golden):
         assert (rec.token, rec.exit_layer, rec.predictor_fired, rec.verified, rec.active) == (
             ref["token"], ref["exit_layer"], ref["predictor_fired"], ref["verified"], ref["active"])
+
+
+def _tree_cases(golden):
+    return golden.json("tree_tiny.json")["cases"]
+
+
+def run_tree_oracle(oracle, case, n_steps=None):
+    tc, t, dc, dm, bank, counts, _, _ = tiny_pipeline_inputs(oracle)
+    pol = {"never_all": "never", "always_all": "always"}.get(case["case"], bank)
+    eng = oracle.TreeEngineOracle(tc, t, dc, dm, pol, case["branching"], k=4,
+                                  threshold=case["threshold"], schedule_mode=case["mode"],
+                                  exit_counts=counts, schedule_config=oracle.ScheduleConfig(5, 1, 4))
+    eng.start(case["prompt"])
+    return eng, [eng.step() for _ in range(n_steps or len(case["steps"]))]
+
+
+def assert_tree_step_equal(res, ref, where):
+    got = dict(accepted_tokens=res.accepted_tokens, correction_token=res.correction_token,
+               path_exit_layers=res.path_exit_layers, accepted_path=res.accepted_path,
+               predictor_evals=res.predictor_evals, num_paths=res.num_paths,
+               max_path_len=res.max_path_len, scheduled_layer_count=res.scheduled_layer_count)
+    exp = {k: ref[k] for k in got}
+    assert got == exp, where
+
+
+@pytest.mark.parametrize("ci", range(0, 15, 3))
+def test_tree_engine_oracle_matches_reference(oracle, golden, ci):
+    """The oracle's TreeEngine restatement (tree.py:133-302) reproduces the
+    reference TreeEngine's step results and every predictor probability
+    (bit-exact, in call order) on the trained tiny pipeline models."""
+    case = _tree_cases(golden)[ci]
+    eng, steps = run_tree_oracle(oracle, case)
+    for s, (res, ref) in enumerate(zip(steps, case["steps"])):
+        assert_tree_step_equal(res, ref, (case["case"], s))
+        assert [[l, p] for l, p in res.probs] == ref["probs"], (case["case"], s)
