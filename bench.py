@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mode", default="fast", choices=["fast", "strict"])
+    ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--decode-tokens", type=int, default=32)
     return ap.parse_args()
 
 
@@ -226,6 +228,76 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ ours
+
+
+def decode_bench(args, rank, ws, dev):
+    """Early-exit decode at Llama2-7B shape, one stream per
+    rank through the device-resident ExitEngine (one CUDA graph per token:
+    2-layer draft + top-K, scheduler, 32 flag-guarded decoder layers, fused
+    predictor evals on the active layers, gated verify GEMVs).  Device time of
+    graph replays (max over ranks) and end-to-end ``generate()`` wall time
+    (host prompt in, host tokens out)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_08850_b200 as spx
+    from paper_2504_08850_b200 import engine as E
+    from paper_2504_08850_b200 import rng
+    seed = SEED + 1000 * rank
+    tc = spx.ModelConfig(V, D, LAYERS, 32, 11008, 512, seed)
+    dc = spx.ModelConfig(V, D, 2, 32, 11008, 512, seed + 1)
+    t, d = spx.init_model(tc, dtype="bf16"), spx.init_model(dc, dtype="bf16")
+    bank = {l: spx.init_predictor(K, H, rng.derive(seed, l)) for l in range(LAYERS - 1)}
+    counts = np.asarray([int(x) % 97 for x in rng.splitmix64(seed + 7, LAYERS)], dtype=np.uint64)
+    prof = spx.OfflineProfile(LAYERS, counts, 0)
+    thr = 0.5
+    eng = E.ExitEngine(t, d, E.PredictorPolicy(bank),
+                       E.EngineConfig(k=K, threshold=thr, schedule_mode="two-level"), prof,
+                       spx.ScheduleConfig(5, 2, 4))
+    prompt = [int(x) % V for x in rng.splitmix64(seed, 16)]
+    n = args.decode_tokens
+    eng.generate(prompt, 4)                      # capture + warm
+    eng.start(prompt)
+    g = eng._dev.graph(False)
+    for _ in range(3):
+        g.replay()
+    eng.start(prompt)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(n):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    recs = eng._dev.records(n)
+    t0 = time.perf_counter()
+    toks, trace = eng.generate(prompt, n)
+    e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    layer_bytes = (4 * D * D + 2 * D * 11008) * 2
+    el = float(np.mean([r.exit_layer for r in recs]))
+    heads = float(np.mean([r.full_head_count for r in recs]))
+    ms_tok = float(ms.item()) / n
+    # executed decoder layers = exit layer + 1; plus full-head GEMVs (262 MB)
+    tok_bytes = (el + 1) * layer_bytes + heads * V * D * 2 + 2 * layer_bytes + V * D * 2
+    return {"tok_s": ws * n / (float(ms.item()) / 1e3), "unit": "tokens/s",
+            "ms_per_token": ms_tok, "streams": ws, "tokens_per_stream": n,
+            "e2e_tok_s": ws * n / float(e2e_s.item()),
+            "avg_exit_layer": el, "full_heads_per_token": heads,
+            "fire_token_frac": float(np.mean([r.predictor_fired for r in recs])),
+            "verified_frac": float(np.mean([r.verified for r in recs])),
+            "evals_per_token": float(np.mean([r.predictor_evals for r in recs])),
+            "hbm_bytes_per_token": tok_bytes,
+            "hbm_GBps": tok_bytes / (ms_tok * 1e-3) / 1e9,
+            "config": "Llama2-7B shape (reference architecture) random-init bf16, batch 1 per "
+                      "GPU, 2-layer draft, K=4, H=512, thr 0.5, two-level (top-k 4, N=5, r=2), "
+                      "16-token prompt"}
+
 
 
 def main():
@@ -404,6 +476,11 @@ def main():
                "d2h_bytes_per_step": int(PRED_LAYERS * B * (1 + 8)),
                "path": "paper_2504_08850_b200.evaluate_batch -> spx_predictor_eval (C ABI)"}
 
+    # ---- early-exit decode tok/s (configs[1]: 7B shape, batch 1 per rank) ---
+    decode = None
+    if not args.no_decode:
+        decode = decode_bench(args, rank, ws, dev)
+
     # ---- CPU baseline (rank 0, N=1) ----------------------------------------
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -446,6 +523,7 @@ def main():
             "cpu_baseline": cpu,
             "gpu_launches": launches,
             "clocks": clocks,
+            "decode": decode,
             "fire_rate": fired,
             "batch1_us_per_eval": us_per_eval_b1,
             "lib": N.version(),
