@@ -43,7 +43,11 @@ V, D, K, H, LAYERS = 32000, 4096, 4, 512, 32
 PRED_LAYERS = LAYERS - 1
 THRESHOLD = 0.7
 SEED = 1234
-PDL = os.environ.get("SPX_PDL", "1") == "1"
+# programmatic dependent launch; 2 = also "ids ready": the speculative ids of a
+# token are fixed across its layer loop (written at token start by the draft),
+# so each launch may start its LM-head row prefetch before the previous
+# launch retires (include/specexit_b200.h, spx_predictor_args.pdl)
+PDL = int(os.environ.get("SPX_PDL", "2"))
 METRIC = "predictor evals/sec + early-exit decode tok/s, Llama2-7B shape, 1/2/4/8 B200"
 
 
@@ -334,9 +338,16 @@ def main():
     g.manual_seed(SEED + 17 * rank)
     hidden = torch.randn((PRED_LAYERS, B, D), generator=g, device=dev, dtype=torch.float32)
     hidden = hidden.to(torch.bfloat16).float()            # bf16-valued rows
-    ids_np = distinct_ids(SEED + 1 + rank, B, K, V)
-    ids = torch.as_tensor(ids_np, device=dev)
-    U = int(np.unique(ids_np).size)
+    # Distinct speculative ids per layer launch: in the engine the decoder layer
+    # between two predictor launches streams ~315 MB and evicts the previous
+    # launch's LM-head rows from the 126 MB L2; a predictor-only loop with one
+    # id set would re-read the same 31 MB of head rows from L2 every launch.
+    ids_all = np.stack([distinct_ids(SEED + 1 + 1000 * rank + l, B, K, V)
+                        for l in range(PRED_LAYERS)])
+    ids_np = ids_all[0]
+    ids_l = torch.as_tensor(ids_all, device=dev)               # (layers, B, K)
+    ids = ids_l[0]
+    U = float(np.mean([np.unique(ids_all[l]).size for l in range(PRED_LAYERS)]))
     prev0 = torch.full((B, K), float(np.float32(1.0 / K)), device=dev)
     prev = prev0.clone()
     err = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -348,7 +359,7 @@ def main():
     def step():
         prev.copy_(prev0)                                  # token start: uniform prior
         for l in range(PRED_LAYERS):
-            spx.evaluate_batch(model, bank, hidden[l], ids, prev, threshold=THRESHOLD, layer=l,
+            spx.evaluate_batch(model, bank, hidden[l], ids_l[l], prev, threshold=THRESHOLD, layer=l,
                                outputs=False, out=outs[l], pdl=PDL)
 
     stream = torch.cuda.Stream()
@@ -435,11 +446,11 @@ def main():
     e2e = None
     if not args.no_e2e:
         h_host = hidden.cpu().pin_memory()
-        ids_host = ids.cpu().pin_memory()
+        ids_host = ids_l.cpu().pin_memory()
         fired_host = torch.empty((PRED_LAYERS, B), dtype=torch.uint8).pin_memory()
         prob_host = torch.empty((PRED_LAYERS, B), dtype=torch.float64).pin_memory()
         hid_dev = torch.empty_like(hidden)
-        ids_dev = torch.empty_like(ids)
+        ids_dev = torch.empty_like(ids_l)
         eo = [spx.predictor.BatchResult(logits=None, z=None,
                                         prob=torch.empty(B, dtype=torch.float64, device=dev),
                                         fired=torch.empty(B, dtype=torch.uint8, device=dev),
@@ -450,7 +461,7 @@ def main():
             ids_dev.copy_(ids_host, non_blocking=True)
             prev.copy_(prev0)
             for l in range(PRED_LAYERS):
-                spx.evaluate_batch(model, bank, hid_dev[l], ids_dev, prev, threshold=THRESHOLD,
+                spx.evaluate_batch(model, bank, hid_dev[l], ids_dev[l], prev, threshold=THRESHOLD,
                                    layer=l, outputs=False, out=eo[l], pdl=PDL)
             for l in range(PRED_LAYERS):
                 fired_host[l].copy_(eo[l].fired, non_blocking=True)
@@ -472,7 +483,7 @@ def main():
             dist.all_reduce(xms, op=dist.ReduceOp.MAX)
         e2e = {"value": evals_per_step * e2e_steps / (float(xms.item()) / 1000.0),
                "unit": "evals/s",
-               "h2d_bytes_per_step": int(hidden.numel() * 4 + ids.numel() * 4),
+               "h2d_bytes_per_step": int(hidden.numel() * 4 + ids_l.numel() * 4),
                "d2h_bytes_per_step": int(PRED_LAYERS * B * (1 + 8)),
                "path": "paper_2504_08850_b200.evaluate_batch -> spx_predictor_eval (C ABI)"}
 
@@ -510,9 +521,10 @@ def main():
                                    f"K={K}, H={H}, thr={THRESHOLD}, mode={args.mode}",
                        "batch_per_gpu": B, "layers_per_step": PRED_LAYERS, "k": K,
                        "predictor_hidden": H, "unique_ids_per_launch": U,
-                       "l2": "inputs (520 MB hidden + 262 MB head) exceed the 126 MB L2; no flush",
+                       "l2": "no flush: inputs exceed the 126 MB L2 (520 MB of hidden rows per step, "
+                             "distinct speculative ids per layer launch over the 262 MB head)",
                        "parallelism": f"dp{ws} (request sharding, no hot-path collective)",
-                       "cuda_graph": True},
+                       "cuda_graph": True, "pdl": PDL},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": None,
                          "kernel": "predictor_fast_kernel<bf16,4>",

@@ -87,7 +87,13 @@ typedef struct {
   int32_t layer;
   int32_t mode;              /* SPX_MODE_*                                     */
   int32_t pdl;               /* 1: programmatic dependent launch (overlap the  */
-                             /*    prologue with the previous kernel)          */
+                             /*    prologue with the previous kernel);         */
+                             /* 2: as 1, and `ids` is not written by the       */
+                             /*    immediately preceding kernel, so the        */
+                             /*    LM-head row prefetch of each team's first   */
+                             /*    rows starts before griddepcontrol.wait     */
+                             /*    (ignored when row_done / row_layer_mask     */
+                             /*    are given: those flags are written late)    */
   int32_t *err;              /* device error word                              */
   int64_t B, d, V, K, H;
 } spx_predictor_args;

@@ -21,11 +21,13 @@
 // i.e. the LayerNorm is folded into the head dot (one pass over the row for
 // the variance and the K dots), with packed FP32 (FADD2/FMUL2/FFMA2).
 
+#include <type_traits>
+
 constexpr int NTEAM = 4;
 constexpr int TEAM = 4;
 constexpr int NTAIL = 4;
 constexpr int HALF = 2;                        // LM-head rows per TMA unit
-constexpr int RING = 2;                        // units in flight per team
+constexpr int MAX_RING = 3;                    // units in flight per team (2 or 3)
 constexpr int QS = 8;                          // tail queue slots (multiple of NTEAM, NTAIL)
 constexpr int RED_FLOATS = 32;
 constexpr int FAST_THREADS = 32 * (TEAM * NTEAM + NTAIL);
@@ -38,38 +40,57 @@ struct QSlot {                                 // dot team -> tail warp hand-off
 
 struct SmemPlan {
   int w1_smem;     // W1 staged in shared memory?
+  int ring;        // TMA units in flight per team
+  int g_smem;      // final_norm.g staged in shared memory (else read through L1)
   size_t bytes;
   size_t off_g, off_w2, off_b1, off_w1, off_team, team_bytes, off_ring, unit_bytes, off_tail,
       tail_bytes, off_q, off_bar;
 };
 
 template <typename TW>
-inline SmemPlan plan_smem(int d, int K, int H, int max_bytes, int force_w1 = -1) {
+inline SmemPlan plan_smem_ring(int d, int K, int H, int max_bytes, int force_w1, int ring,
+                               bool g_smem = true) {
   SmemPlan s{};
+  const size_t gb = g_smem ? (size_t)d * 4 : 0;
   const size_t unit = ((size_t)HALF * d * sizeof(TW) + 127) / 128 * 128;
   const size_t team = ((size_t)(RED_FLOATS + 4 + MAXK) * 4 + 127) / 128 * 128;
   const size_t tail = ((size_t)(3 * MAXK + (H > 0 ? H : 4) + 64) * 4 + 127) / 128 * 128;
   const size_t qbytes = (sizeof(QSlot) * QS + 127) / 128 * 128;
   const size_t w1b = ((size_t)3 * K * H * 4 + 127) / 128 * 128;
-  const size_t bars = (NTEAM * RING + 2 * QS + 1) * 8;
-  const size_t base = (((size_t)d + 2 * H) * 4 + 127) / 128 * 128 + NTEAM * team +
-                      (size_t)NTEAM * RING * unit + NTAIL * tail + qbytes + bars + 128;
+  const size_t bars = (NTEAM * MAX_RING + 2 * QS + 1) * 8;
+  const size_t base = (gb + (size_t)2 * H * 4 + 127) / 128 * 128 + NTEAM * team +
+                      (size_t)NTEAM * ring * unit + NTAIL * tail + qbytes + bars + 128;
   const bool w1 = H > 0 && force_w1 != 0 && base + w1b <= (size_t)max_bytes;
   if (base > (size_t)max_bytes) return s;          // does not fit: bytes == 0
   size_t o = 0;
   s.w1_smem = w1;
-  s.off_g = o; o += (size_t)d * 4;
+  s.ring = ring;
+  s.g_smem = g_smem;
+  s.off_g = o; o += gb;
   s.off_w2 = o; o += (size_t)H * 4;
   s.off_b1 = o; o += (size_t)H * 4;
   o = (o + 127) / 128 * 128;
   s.off_w1 = o; if (w1) o += w1b;
   s.off_team = o; s.team_bytes = team; o += NTEAM * team;
-  s.off_ring = o; s.unit_bytes = unit; o += (size_t)NTEAM * RING * unit;
+  s.off_ring = o; s.unit_bytes = unit; o += (size_t)NTEAM * ring * unit;
   s.off_tail = o; s.tail_bytes = tail; o += NTAIL * tail;
   s.off_q = o; o += qbytes;
   s.off_bar = o; o += bars;
   s.bytes = o;
   return s;
+}
+
+// Ring depth 2 (one row's LM-head rows per team in flight); force_ring = 3
+// (sweeps) trades W1/g shared-memory residency for a third unit.
+template <typename TW>
+inline SmemPlan plan_smem(int d, int K, int H, int max_bytes, int force_w1 = -1,
+                          int force_ring = -1) {
+  if (force_ring == 3) {     // measured slower at 7B (W1 and g then come from L1)
+    SmemPlan s = plan_smem_ring<TW>(d, K, H, max_bytes, force_w1, 3);
+    if (!s.bytes) s = plan_smem_ring<TW>(d, K, H, max_bytes, force_w1, 3, false);
+    if (s.bytes) return s;
+  }
+  return plan_smem_ring<TW>(d, K, H, max_bytes, force_w1, 2);
 }
 
 __device__ __forceinline__ void team_sync(int team) {
@@ -79,19 +100,21 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <typename TW, int CPL, bool FULL, bool W1S>
+// KC / HC: compile-time K / H (0 = runtime) -- the K=4, H=512 configuration
+// of the paper gets fully unrolled softmax, MLP and dot loops.
+template <typename TW, int CPL, bool FULL, bool W1S, int KC, int HC, int RING>
 __global__ void __launch_bounds__(FAST_THREADS, 1)
 predictor_fast_kernel(PredParams p, SmemPlan sp) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int d = p.d, K = p.K, H = p.H, nchunk = d / CHUNK;
-  float *gs = reinterpret_cast<float *>(smem + sp.off_g);
+  const int d = p.d, K = KC ? KC : p.K, H = HC ? HC : p.H, nchunk = d / CHUNK;
+  const float *gs = sp.g_smem ? reinterpret_cast<const float *>(smem + sp.off_g) : p.norm_g;
   float *w2s = reinterpret_cast<float *>(smem + sp.off_w2);
   float *b1s = reinterpret_cast<float *>(smem + sp.off_b1);
   float *w1s = reinterpret_cast<float *>(smem + sp.off_w1);
   QSlot *queue = reinterpret_cast<QSlot *>(smem + sp.off_q);
   uint64_t *ringbar = reinterpret_cast<uint64_t *>(smem + sp.off_bar);   // [NTEAM][RING]
-  uint64_t *qfull = ringbar + NTEAM * RING;
+  uint64_t *qfull = ringbar + NTEAM * MAX_RING;
   uint64_t *qempty = qfull + QS;
   uint64_t *setup_bar = qempty + QS;
   const TW *head = reinterpret_cast<const TW *>(p.head);
@@ -110,10 +133,10 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
   fence_mbar_init();
   __syncthreads();
   if (threadIdx.x == 0) {                  // per-CTA constants (weights) by TMA
-    uint32_t bytes = (uint32_t)d * 4u;
+    uint32_t bytes = sp.g_smem ? (uint32_t)d * 4u : 0u;
     if (mlp && bulk_consts) bytes += 2u * H * 4u + (sp.w1_smem ? 3u * K * H * 4u : 0u);
     mbar_arrive_expect_tx(setup_bar, bytes);
-    bulk_g2s(gs, p.norm_g, (uint32_t)d * 4u, setup_bar);
+    if (sp.g_smem) bulk_g2s(smem + sp.off_g, p.norm_g, (uint32_t)d * 4u, setup_bar);
     if (mlp && bulk_consts) {
       bulk_g2s(w2s, p.w2, (uint32_t)H * 4u, setup_bar);
       bulk_g2s(b1s, p.b1, (uint32_t)H * 4u, setup_bar);
@@ -130,7 +153,14 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
   // per-request inputs (hidden rows, ids, prev, engine flags) may be written
   // by the previous kernel in the stream, so wait for it here, then let the
   // next kernel's CTAs start their own prologue as SMs free up.
-  if (p.pdl) {
+  // pdl == 2 ("ids ready"): the dot teams first issue the LM-head prefetch of
+  // their first rows -- it depends only on ids and the head -- and wait after.
+  const bool early = p.pdl == 2 && !p.row_done && !p.row_layer_mask;
+  if (p.pdl && !early) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
+  if (early && warp >= TEAM * NTEAM) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   }
@@ -147,77 +177,146 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
       mbar_wait(qfull + slot, (k / QS) & 1);
       const QSlot &q = queue[slot];
       const int row = q.row, flags = q.flags;
-      const bool v0 = lane < K, v1 = lane + 32 < K;
-      const float x0 = v0 ? q.logits[lane] : 0.f, x1 = v1 ? q.logits[lane + 32] : 0.f;
-      const float pv0 = v0 ? q.prev[lane] : 0.f, pv1 = v1 ? q.prev[lane + 32] : 0.f;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(qempty + slot);               // slot consumed
-      if (flags & 1) {                                          // skipped row
-        if (lane == 0 && p.fired) p.fired[row] = 0;
-        continue;
+      if (p.trace && lane == 0 && !(flags & 1)) {
+        p.trace[(size_t)row * 16 + 0] = gtimer();
+        p.trace[(size_t)row * 16 + 8] = clock64();
       }
-      if (flags & 6) {
-        if (lane == 0) {
-          atomicOr(p.err, ((flags & 2) ? ERR_ID_RANGE : 0) | ((flags & 4) ? ERR_HIDDEN_NONFINITE : 0));
-          if (p.fired) p.fired[row] = 0;
-        }
-        continue;
-      }
-      // ---- softmax over the K ids (model.py:149-152), features (predictor.py:42-52)
-      bool bad = (v0 && !is_finite(x0)) || (v1 && !is_finite(x1));
-      bad = __any_sync(0xffffffffu, bad);
-      float m = v0 ? x0 : -INFINITY;
-      if (v1) m = fmaxf(m, x1);
+      if constexpr (KC > 0 && KC <= 8) {
+        // every lane holds all K logits: no shuffles on the critical path
+        float x[KC], pv[KC];
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      float e0 = 0.f, e1 = 0.f;
+        for (int c = 0; c < KC; ++c) { x[c] = q.logits[c]; pv[c] = q.prev[c]; }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(qempty + slot);             // slot consumed
+        if (flags & 1) {                                        // skipped row
+          if (lane == 0 && p.fired) p.fired[row] = 0;
+          continue;
+        }
+        if (flags & 6) {
+          if (lane == 0) {
+            atomicOr(p.err, ((flags & 2) ? ERR_ID_RANGE : 0) | ((flags & 4) ? ERR_HIDDEN_NONFINITE : 0));
+            if (p.fired) p.fired[row] = 0;
+          }
+          continue;
+        }
+        bool bad = false;
+        float m = x[0];
+#pragma unroll
+        for (int c = 0; c < KC; ++c) { bad |= !is_finite(x[c]); m = fmaxf(m, x[c]); }
+        float e[KC], esum = 0.f, psum = 0.f;
+#pragma unroll
+        for (int c = 0; c < KC; ++c) e[c] = np_expf(__fsub_rn(x[c], m));
+#pragma unroll
+        for (int c = 0; c < KC; ++c) { esum = __fadd_rn(esum, e[c]); psum = __fadd_rn(psum, pv[c]); }
+        if (p.logits_out && lane < KC) {
+#pragma unroll
+          for (int c = 0; c < KC; ++c) if (lane == c) p.logits_out[(size_t)row * KC + c] = x[c];
+        }
+        int ecode = 0;
+        if (bad) ecode |= ERR_LOGIT_NONFINITE;
+        if (fabsf(psum - 1.0f) > 1e-5f && fabs((double)psum - 1.0) > 1e-5) ecode |= ERR_PREV_SUM;
+        if (ecode) {
+          if (lane == 0) {
+            atomicOr(p.err, ecode);
+            if (p.fired) p.fired[row] = 0;
+          }
+          continue;
+        }
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+          if (lane == c) {
+            const float pr = __fdiv_rn(e[c], esum);
+            feats[c] = x[c];
+            feats[KC + c] = pr;
+            feats[2 * KC + c] = __fsub_rn(pr, pv[c]);
+            p.prev[(size_t)row * KC + c] = pr;                 // engine.py:196
+          }
+        }
+      } else {
+        const bool v0 = lane < K, v1 = lane + 32 < K;
+        const float x0 = v0 ? q.logits[lane] : 0.f, x1 = v1 ? q.logits[lane + 32] : 0.f;
+        const float pv0 = v0 ? q.prev[lane] : 0.f, pv1 = v1 ? q.prev[lane + 32] : 0.f;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(qempty + slot);               // slot consumed
+        if (flags & 1) {                                          // skipped row
+          if (lane == 0 && p.fired) p.fired[row] = 0;
+          continue;
+        }
+        if (flags & 6) {
+          if (lane == 0) {
+            atomicOr(p.err, ((flags & 2) ? ERR_ID_RANGE : 0) | ((flags & 4) ? ERR_HIDDEN_NONFINITE : 0));
+            if (p.fired) p.fired[row] = 0;
+          }
+          continue;
+        }
+        // ---- softmax over the K ids (model.py:149-152), features (predictor.py:42-52)
+        bool bad = (v0 && !is_finite(x0)) || (v1 && !is_finite(x1));
+        bad = __any_sync(0xffffffffu, bad);
+        float m = v0 ? x0 : -INFINITY;
+        if (v1) m = fmaxf(m, x1);
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        float e0 = 0.f, e1 = 0.f;
 #pragma unroll 1
-      for (int hh = 0; hh < 2; ++hh) {                          // one np_expf copy
-        if (hh ? v1 : v0) {
-          const float ev = np_expf(__fsub_rn(hh ? x1 : x0, m));
-          if (hh) e1 = ev; else e0 = ev;
+        for (int hh = 0; hh < 2; ++hh) {                          // one np_expf copy
+          if (hh ? v1 : v0) {
+            const float ev = np_expf(__fsub_rn(hh ? x1 : x0, m));
+            if (hh) e1 = ev; else e0 = ev;
+          }
         }
-      }
-      float esum = 0.f, psum = 0.f;                             // strict left-to-right
-      for (int c = 0; c < K; ++c) {
-        esum = __fadd_rn(esum, __shfl_sync(0xffffffffu, c < 32 ? e0 : e1, c & 31));
-        psum = __fadd_rn(psum, __shfl_sync(0xffffffffu, c < 32 ? pv0 : pv1, c & 31));
-      }
-      if (p.logits_out) {
-        if (v0) p.logits_out[(size_t)row * K + lane] = x0;
-        if (v1) p.logits_out[(size_t)row * K + lane + 32] = x1;
-      }
-      int e = 0;
-      if (bad) e |= ERR_LOGIT_NONFINITE;
-      if (fabs((double)psum - 1.0) > 1e-5) e |= ERR_PREV_SUM;
-      if (e) {
-        if (lane == 0) {
-          atomicOr(p.err, e);
-          if (p.fired) p.fired[row] = 0;
+        float esum = 0.f, psum = 0.f;                             // strict left-to-right
+        for (int c = 0; c < K; ++c) {
+          esum = __fadd_rn(esum, __shfl_sync(0xffffffffu, c < 32 ? e0 : e1, c & 31));
+          psum = __fadd_rn(psum, __shfl_sync(0xffffffffu, c < 32 ? pv0 : pv1, c & 31));
         }
-        continue;
-      }
-      if (v0) {
-        const float pr = __fdiv_rn(e0, esum);
-        feats[lane] = x0;
-        feats[K + lane] = pr;
-        feats[2 * K + lane] = __fsub_rn(pr, pv0);
-        p.prev[(size_t)row * K + lane] = pr;                   // engine.py:196
-      }
-      if (v1) {
-        const float pr = __fdiv_rn(e1, esum);
-        feats[lane + 32] = x1;
-        feats[K + lane + 32] = pr;
-        feats[2 * K + lane + 32] = __fsub_rn(pr, pv1);
-        p.prev[(size_t)row * K + lane + 32] = pr;
+        if (p.logits_out) {
+          if (v0) p.logits_out[(size_t)row * K + lane] = x0;
+          if (v1) p.logits_out[(size_t)row * K + lane + 32] = x1;
+        }
+        int e = 0;
+        if (bad) e |= ERR_LOGIT_NONFINITE;
+        if (fabs((double)psum - 1.0) > 1e-5) e |= ERR_PREV_SUM;
+        if (e) {
+          if (lane == 0) {
+            atomicOr(p.err, e);
+            if (p.fired) p.fired[row] = 0;
+          }
+          continue;
+        }
+        if (v0) {
+          const float pr = __fdiv_rn(e0, esum);
+          feats[lane] = x0;
+          feats[K + lane] = pr;
+          feats[2 * K + lane] = __fsub_rn(pr, pv0);
+          p.prev[(size_t)row * K + lane] = pr;                   // engine.py:196
+        }
+        if (v1) {
+          const float pr = __fdiv_rn(e1, esum);
+          feats[lane + 32] = x1;
+          feats[K + lane + 32] = pr;
+          feats[2 * K + lane + 32] = __fsub_rn(pr, pv1);
+          p.prev[(size_t)row * K + lane + 32] = pr;
+        }
       }
       __syncwarp();
       if (p.feat_out)
         for (int i = lane; i < 3 * K; i += 32) p.feat_out[(size_t)row * 3 * K + i] = feats[i];
       if (lane == 0 && p.evals) p.evals[row] += 1;
+      if (p.trace && lane == 0) p.trace[(size_t)row * 16 + 10] = clock64();
       if (mlp) {
-        const float z2 = W1S ? warp_mlp(feats, w1s, b1s, w2s, p.b2, K, H, hs, lane)
-                             : warp_mlp_g(feats, p.w1, b1s, w2s, p.b2, K, H, hs, lane);
+        float z2;
+        if (p.trace) {
+          mlp_z1<4, !W1S>(feats, W1S ? w1s : p.w1, b1s, 3 * K, H, hs, lane, 0);
+          __syncwarp();
+          if (lane == 0) p.trace[(size_t)row * 16 + 11] = clock64();
+          const float a0 = z2_partial(hs, w2s, H, lane), a1 = z2_partial(hs, w2s, H, lane + 32);
+          if (lane == 0) p.trace[(size_t)row * 16 + 12] = clock64();
+          z2 = z2_tree(a0, a1, hs, w2s, H, p.b2, lane);
+          if (lane == 0) p.trace[(size_t)row * 16 + 13] = clock64();
+        } else {
+          z2 = W1S ? warp_mlp(feats, w1s, b1s, w2s, p.b2, K, H, hs, lane)
+                   : warp_mlp_g(feats, p.w1, b1s, w2s, p.b2, K, H, hs, lane);
+        }
         if (lane == 0) {
           if (p.z_out) p.z_out[row] = z2;
           // the decision is exact (z2 >= z_cut); the reported probability is
@@ -230,7 +329,10 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
         if (p.z_out) p.z_out[row] = 0.0f;
         if (p.fired) p.fired[row] = (p.const_prob > p.threshold) ? 1 : 0;
       }
-      if (p.trace && lane == 0) p.trace[(size_t)row * 8 + 4] = gtimer();
+      if (p.trace && lane == 0) {
+        p.trace[(size_t)row * 16 + 4] = gtimer();
+        p.trace[(size_t)row * 16 + 9] = clock64();
+      }
     }
     return;
   }
@@ -315,7 +417,7 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
       mbar_arrive_expect_tx(tbar + slot, (uint32_t)nr * wrow_bytes);
       for (int q = 0; q < nr; ++q)
         bulk_g2s(dst + (size_t)q * d, head + (size_t)idv[q] * d, wrow_bytes, tbar + slot);
-      if (p.trace && h == 0) p.trace[(size_t)row_of(kk) * 8 + 5] = gtimer();
+      if (p.trace && h == 0) p.trace[(size_t)row_of(kk) * 16 + 5] = gtimer();
     }
     ++n_issue;
   };
@@ -347,6 +449,10 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
     load_ids(k + NTEAM, nid0, nid1, nbad, nskip);
     pump();
   }
+  if (early) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
   {  // every warp needs the skip status of its current row
     const int row = row_of(k);
     cskip = k >= rows_cta || row_skipped(p, row);
@@ -359,7 +465,7 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
     if (cskip) {
       if (w == 0) handoff(k, row, 1, 0.f, 0.f);
     } else {
-      if (p.trace && leader) p.trace[(size_t)row * 8 + 1] = gtimer();
+      if (p.trace && leader) p.trace[(size_t)row * 16 + 1] = gtimer();
       // ---- pass 1: mean (this warp = canonical group w), from registers
       float part = 0.f;
 #pragma unroll
@@ -386,12 +492,13 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
         hbad = (tflag[0] | tflag[1] | tflag[2] | tflag[3]) != 0;
         team_sync(team);
       }
-      if (p.trace && leader) p.trace[(size_t)row * 8 + 2] = gtimer();
+      if (p.trace && leader) p.trace[(size_t)row * 16 + 2] = gtimer();
       float r = 0.f;
       const float2 nmean = make_float2(-mean, -mean);
       for (int h = 0; h < nhalf; ++h) {
         const int slot = n_wait % RING;
         mbar_wait(tbar + slot, (n_wait / RING) & 1);
+        if (p.trace && leader && h < 2) p.trace[(size_t)row * 16 + 6 + h] = gtimer();
         const TW *sw = reinterpret_cast<const TW *>(tring + (size_t)slot * sp.unit_bytes);
         const int c0 = h * HALF, nr = (K - c0) < HALF ? (K - c0) : HALF;
         float2 acc = make_float2(0.f, 0.f);
@@ -449,7 +556,7 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
         }
         if (h + 1 < nhalf) team_sync(team);    // red reused by the next half
       }
-      if (p.trace && leader) p.trace[(size_t)row * 8 + 3] = gtimer();
+      if (p.trace && leader) p.trace[(size_t)row * 16 + 3] = gtimer();
       if (w == 0) {
         __syncwarp();
         handoff(k, row, (cbad ? 2 : 0) | (hbad ? 4 : 0), pv0, pv1);
@@ -476,13 +583,34 @@ struct FastLaunch {
   const PredParams &p; const SmemPlan &sp; int grid; cudaStream_t stream; int smem_optin;
   template <int CPL> void operator()() const {
     const bool full = p.d == CHUNK * NPART * CPL;
-    if (sp.w1_smem) { if (full) launch<CPL, true, true>(); else launch<CPL, false, true>(); }
-    else { if (full) launch<CPL, true, false>(); else launch<CPL, false, false>(); }
+    // the 3-deep ring only for the bf16 full-width kernels (LLM shapes); the
+    // smem plan of a 3-ring also holds a 2-ring
+    if constexpr (std::is_same<TW, __nv_bfloat16>::value) {
+      if (sp.ring == 3 && full) { go<CPL, 3>(); return; }
+    }
+    go<CPL, 2>();
   }
-  template <int CPL, bool FULL, bool W1S> void launch() const {
+  template <int CPL, int RG> void go() const {
+    const bool full = p.d == CHUNK * NPART * CPL;
+    if constexpr (RG == 3) {
+      if (p.K == 4 && p.H == 512 && p.policy == SPX_POLICY_MLP) {
+        if (sp.w1_smem) launch<CPL, true, true, 4, 512, 3>(); else launch<CPL, true, false, 4, 512, 3>();
+      } else {
+        if (sp.w1_smem) launch<CPL, true, true, 0, 0, 3>(); else launch<CPL, true, false, 0, 0, 3>();
+      }
+      return;
+    }
+    if (full && p.K == 4 && p.H == 512 && p.policy == SPX_POLICY_MLP) {
+      if (sp.w1_smem) launch<CPL, true, true, 4, 512, RG>(); else launch<CPL, true, false, 4, 512, RG>();
+      return;
+    }
+    if (sp.w1_smem) { if (full) launch<CPL, true, true, 0, 0, RG>(); else launch<CPL, false, true, 0, 0, RG>(); }
+    else { if (full) launch<CPL, true, false, 0, 0, RG>(); else launch<CPL, false, false, 0, 0, RG>(); }
+  }
+  template <int CPL, bool FULL, bool W1S, int KC, int HC, int RG> void launch() const {
     static bool configured = false;
     if (!configured) {
-      cudaFuncSetAttribute(predictor_fast_kernel<TW, CPL, FULL, W1S>,
+      cudaFuncSetAttribute(predictor_fast_kernel<TW, CPL, FULL, W1S, KC, HC, RG>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
       configured = true;
     }
@@ -496,6 +624,6 @@ struct FastLaunch {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = p.pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, predictor_fast_kernel<TW, CPL, FULL, W1S>, p, sp);
+    cudaLaunchKernelEx(&cfg, predictor_fast_kernel<TW, CPL, FULL, W1S, KC, HC, RG>, p, sp);
   }
 };

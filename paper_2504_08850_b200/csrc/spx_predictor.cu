@@ -1,3 +1,4 @@
+#include <type_traits>
 // K1+K2+K3: fused speculative early-exit predictor evaluation (sm_100a).
 //
 // One launch evaluates one decoder layer's exit predictor for B rows
@@ -154,7 +155,7 @@ __device__ __forceinline__ float4 ld_w1(const float *p) {
 }
 
 template <int NU, bool W1G = false>
-__device__ void mlp_z1(const float *feats, const float *w1, const float *b1, int n, int H,
+__device__ __forceinline__ void mlp_z1(const float *feats, const float *w1, const float *b1, int n, int H,
                        float *hs, int lane, int u0) {
   if ((H % 4) == 0) {
     for (int jb = 0; jb < H; jb += 512) {
@@ -164,7 +165,7 @@ __device__ void mlp_z1(const float *feats, const float *w1, const float *b1, int
 #pragma unroll
         for (int e = 0; e < 4; ++e) y[u][e] = 0.f;
       if (n <= 48) {
-#pragma unroll 4
+#pragma unroll 12
         for (int i = 0; i < n; ++i) {
           const float f = feats[i];
 #pragma unroll
@@ -246,7 +247,7 @@ __device__ __forceinline__ float z2_partial(const float *hs, const float *w2, in
 // 4 x 16-lane FMA accumulators over 64-element blocks (alo = A[lane], ahi =
 // A[lane+32]), fold 16->8, optional 32-element AVX2 step, lane-wise
 // ((a0+a1)+a2)+a3, 8->4, ((q0+q1)+(q2+q3)), scalar tail, + b2.  Whole warp.
-__device__ float z2_tree(float alo, float ahi, const float *hs, const float *w2, int H, float b2,
+__device__ __forceinline__ float z2_tree(float alo, float ahi, const float *hs, const float *w2, int H, float b2,
                          int lane) {
   const int n1 = H & ~31, n64 = n1 & ~63;
   float blo = __fadd_rn(alo, __shfl_down_sync(0xffffffffu, alo, 8));
@@ -271,7 +272,7 @@ __device__ float z2_tree(float alo, float ahi, const float *hs, const float *w2,
 
 // MLP of one row by one warp.  w1/b1/w2 may point to shared or global memory;
 // hs: scratch of H floats.  Returns z2 in every lane.
-__device__ float warp_mlp(const float *feats, const float *w1, const float *b1, const float *w2,
+__device__ __forceinline__ float warp_mlp(const float *feats, const float *w1, const float *b1, const float *w2,
                           float b2, int K, int H, float *hs, int lane) {
   mlp_z1<4>(feats, w1, b1, 3 * K, H, hs, lane, 0);
   __syncwarp();
@@ -279,7 +280,7 @@ __device__ float warp_mlp(const float *feats, const float *w1, const float *b1, 
                  lane);
 }
 // Same, W1 read from global memory through the read-only path.
-__device__ float warp_mlp_g(const float *feats, const float *w1, const float *b1, const float *w2,
+__device__ __forceinline__ float warp_mlp_g(const float *feats, const float *w1, const float *b1, const float *w2,
                             float b2, int K, int H, float *hs, int lane) {
   mlp_z1<4, true>(feats, w1, b1, 3 * K, H, hs, lane, 0);
   __syncwarp();
@@ -334,6 +335,7 @@ __device__ void warp_row_tail(const PredParams &p, int row, float *feats, const 
 
 // ------------------------------------------------------------ FAST
 #include "spx_pred_fast.cuh"
+#include "spx_pred_stream.cuh"
 
 // ----------------------------------------------------------- STRICT (parity)
 // The reference's own operation sequence: every sum a left-to-right chain of
@@ -531,9 +533,28 @@ static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cu
     predictor_strict_kernel<TW><<<(unsigned)a->B, STRICT_THREADS, smem, stream>>>(p);
   } else {
     if (((size_t)p.d * sizeof(TW)) % 16) return SPX_EINVAL;   // TMA bulk: 16-byte rows
+    static const int env_stream = getenv("SPX_PRED_STREAM") ? atoi(getenv("SPX_PRED_STREAM")) : 2;
+    if (std::is_same<TW, __nv_bfloat16>::value && env_stream && p.K <= SKMAX &&
+        (p.d == 2048 || p.d == 4096 || p.d == 8192) && (p.policy != SPX_POLICY_MLP || p.H <= 1024)) {
+      // env_stream: 1 = ring of whole evaluations, one CTA/SM; 2 = hidden rows by
+      // ld.global, LM-head ring, two CTAs/SM
+      const bool ldgx = env_stream == 2;
+      const int budget = ldgx ? 113 * 1024 : g_smem_optin;
+      StreamPlan st = plan_stream<TW>(p.d, p.K, p.H, budget, ldgx);
+      if (st.bytes) {
+        const long long cap = ldgx ? 2LL * g_sms : g_sms;
+        const int grid = (int)(a->B < cap ? a->B : cap);
+        StreamLaunch<TW> L{p, st, grid, stream, g_smem_optin, ldgx};
+        if (p.d == 2048) L.template operator()<4>();
+        else if (p.d == 4096) L.template operator()<8>();
+        else L.template operator()<16>();
+        return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+      }
+    }
     // tuning overrides (benchmark sweeps only)
     static const int env_w1 = getenv("SPX_PRED_W1SMEM") ? atoi(getenv("SPX_PRED_W1SMEM")) : -1;
-    SmemPlan sp = plan_smem<TW>(p.d, p.K, p.H, g_smem_optin, env_w1);
+    static const int env_ring = getenv("SPX_PRED_RING") ? atoi(getenv("SPX_PRED_RING")) : -1;
+    SmemPlan sp = plan_smem<TW>(p.d, p.K, p.H, g_smem_optin, env_w1, env_ring);
     if (sp.bytes == 0) return SPX_EINVAL;
     const long long need = (a->B + NTEAM - 1) / NTEAM;
     const int grid = (int)(need < g_sms ? need : g_sms);
@@ -565,7 +586,7 @@ extern "C" int spx_predictor_eval(const spx_predictor_args *a, void *stream_) {
   p.prob_out = a->prob_out; p.fired = a->fired;
   p.row_layer_mask = a->row_layer_mask; p.row_done = a->row_done; p.evals = a->evals;
   p.layer = a->layer; p.err = a->err; p.trace = g_debug_trace;
-  p.pdl = a->pdl ? 1 : 0;
+  p.pdl = a->pdl == 2 ? 2 : a->pdl ? 1 : 0;
   p.B = (int)a->B; p.d = (int)a->d; p.V = (int)a->V; p.K = (int)a->K;
   p.H = a->policy == SPX_POLICY_MLP ? (int)a->H : 0;
   if (a->head_dtype == SPX_DTYPE_F32) return launch_predictor<float>(p, a, stream);

@@ -337,7 +337,7 @@ def evaluate_batch(model, weights, hidden, ids, prev, threshold=0.5, layer=0, ou
     a.row_layer_mask, a.row_done, a.evals = N.ptr(row_layer_mask), N.ptr(row_done), N.ptr(evals)
     a.layer = layer
     a.mode = numerics.mode() if mode is None else mode
-    a.pdl = 1 if pdl else 0
+    a.pdl = 2 if (pdl == 2 and pdl is not True) else (1 if pdl else 0)
     a.err = N.ptr(out.err)
     a.B, a.d, a.V, a.K, a.H = B, d, model.config.vocab_size, K, H
     N.check(N.lib().spx_predictor_eval(a, N.stream_ptr()), "spx_predictor_eval")
