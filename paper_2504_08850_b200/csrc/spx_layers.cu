@@ -13,6 +13,7 @@
 // accumulation with 16-byte vector loads and packed FFMA2 (HBM-bound GEMVs).
 // STRICT: the reference's own operation order (sequential chains, no FMA,
 // numpy exp), used for bit-exact parity with the reference trace.
+#include <cstdio>
 #include "spx_common.cuh"
 #include "../../include/specexit_b200.h"
 

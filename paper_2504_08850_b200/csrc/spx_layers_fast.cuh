@@ -30,6 +30,7 @@
 // FFN2+residual (+ frontier update and newest-row copy by the last CTA).
 #pragma once
 #include <type_traits>
+#include <cstdlib>
 
 namespace spx {
 
@@ -467,6 +468,7 @@ static void launch_pdl(K kern, int grid, int block, size_t smem, cudaStream_t s,
 }
 
 #include "spx_gemv_tc.cuh"
+#include "spx_layer_mega.cuh"
 
 // ------------------------------------------------------------------ host side
 
@@ -524,7 +526,14 @@ static void launch_gemv(const LayerParams &p, int nout, int kin, int sms, cudaSt
 
 template <typename TW>
 static void launch_layer_fast(const LayerParams &p, int sms, cudaStream_t s) {
-  if (std::is_same<TW, __nv_bfloat16>::value && tc_layer_supported(p)) {
+  // SPX_LAYER_MEGA=0 selects the per-matrix kernel chain (sweeps / A-B runs)
+  static const int env_mega = getenv("SPX_LAYER_MEGA") ? atoi(getenv("SPX_LAYER_MEGA")) : 1;
+  if (std::is_same<TW, __nv_bfloat16>::value && env_mega && mega_layer_supported(p, sms)) {
+    launch_layer_mega(p, sms, s);
+    return;
+  }
+  static const int env_tc = getenv("SPX_LAYER_TC") ? atoi(getenv("SPX_LAYER_TC")) : 1;
+  if (std::is_same<TW, __nv_bfloat16>::value && env_tc && tc_layer_supported(p)) {
     launch_tc<EPI_QKV>(p, 3 * p.d, p.d, sms, s);
     const size_t ab = (size_t)p.max_ctx * 8 + (size_t)(p.d / p.nh) * 4;
     cudaFuncSetAttribute(attn_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);

@@ -46,6 +46,25 @@ def main():
     ms = e0.elapsed_time(e1) / args.steps
     lay_bytes = (4 * args.d * args.d + 2 * args.d * args.ffn) * 2
     us_layer = ms * 1e3 / args.layers
+    try:
+        import ctypes
+        import numpy as np
+        from paper_2504_08850_b200 import _native as N
+        buf = np.zeros(64, np.uint64)
+        N.lib().spx_debug_mega_trace(ctypes.c_void_p(buf.ctypes.data))
+        names = ["start", "rowset", "qkv", "bar0", "attn", "bar1", "wo", "bar2", "ffn1", "bar3",
+                 "ffn2", "end"]
+        for c in range(2):
+            t = buf[c * 16:c * 16 + 13].astype(np.int64)
+            if t[0] and t[12]:
+                print(f"mega CTA{c}: " + " ".join(f"{names[k]}={(t[k + 1] - t[k]) / 1e3:.2f}"
+                                                  for k in range(12)) +
+                      f" total={(t[12] - t[0]) / 1e3:.2f}us")
+        a = buf[32:37].astype(np.int64)
+        print(f"attn item0: start->scores {(a[0]-a[4])/1e3:.2f} scores->exp {(a[1]-a[0])/1e3:.2f} "
+              f"exp->out {(a[2]-a[1])/1e3:.2f} nctx {a[3]}")
+    except Exception as e:  # noqa: BLE001
+        print("no mega trace:", e)
     print(json.dumps({"us_per_layer": us_layer, "GBps": lay_bytes / (us_layer * 1e-6) / 1e9,
                       "layer_MB": lay_bytes / 1e6}))
 
