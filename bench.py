@@ -314,7 +314,7 @@ def main():
 
     import paper_2504_08850_b200 as spx
     from paper_2504_08850_b200 import _native as N
-    from paper_2504_08850_b200 import numerics, rng
+    from paper_2504_08850_b200 import numerics, rng, shard
 
     ws, rank, local = dist_env()
     if ws > 1:
@@ -395,10 +395,7 @@ def main():
     clocks = clk.stop()
     barrier()
     ms = e0.elapsed_time(e1)
-    t_local = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-    ms_max = float(t_local.item())
+    ms_max = shard.max_over_ranks(ms, dev)                # device time, max over ranks
     evals_per_step = PRED_LAYERS * B * ws
     value = evals_per_step * args.steps / (ms_max / 1000.0)
     launches = PRED_LAYERS * args.steps
@@ -410,6 +407,12 @@ def main():
     except OSError:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None                       # ncu dram bytes per launch (profiles/, one capture)
+    try:
+        ncu = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_summary.json")))
+        traffic = ncu["predictor_stream_kernel"]["traffic_bytes"]
+    except (OSError, KeyError, ValueError):
+        pass
     achieved = bytes_launch / t_launch / 1e9
 
     fired = torch.stack([o.fired for o in outs]).float().mean().item()
@@ -526,8 +529,9 @@ def main():
                        "parallelism": f"dp{ws} (request sharding, no hot-path collective)",
                        "cuda_graph": True, "pdl": PDL},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": None,
-                         "kernel": "predictor_fast_kernel<bf16,4>",
+                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "traffic_source": "profiles/r01_ncu_summary.json (ncu --set full, 1 launch)",
+                         "kernel": "predictor_stream_kernel<bf16, d=4096, K=4, H=512>",
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "us_per_launch": t_launch * 1e6,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
