@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mode", default="fast", choices=["fast", "strict"])
     ap.add_argument("--no-decode", action="store_true")
+    ap.add_argument("--no-tree", action="store_true")
     ap.add_argument("--decode-tokens", type=int, default=32)
     return ap.parse_args()
 
@@ -289,7 +290,13 @@ def decode_bench(args, rank, ws, dev):
     ms_tok = float(ms.item()) / n
     # executed decoder layers = exit layer + 1; plus full-head GEMVs (262 MB)
     tok_bytes = (el + 1) * layer_bytes + heads * V * D * 2 + 2 * layer_bytes + V * D * 2
-    return {"tok_s": ws * n / (float(ms.item()) / 1e3), "unit": "tokens/s",
+    tree = None
+    if not args.no_tree:
+        # configs[2]: EAGLE-like token tree, context-aware merged mapping
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        import tree_bench
+        tree = tree_bench.run(steps=3, seed=seed, models=(t, d))
+    return {"tok_s": ws * n / (float(ms.item()) / 1e3), "unit": "tokens/s", "tree": tree,
             "ms_per_token": ms_tok, "streams": ws, "tokens_per_stream": n,
             "e2e_tok_s": ws * n / float(e2e_s.item()),
             "avg_exit_layer": el, "full_heads_per_token": heads,

@@ -249,6 +249,10 @@ typedef struct {
   int32_t layer, mode;
   int32_t *err;
   int64_t max_ctx, d, n_heads, ffn;
+  int32_t rows_hint;               /* new rows this call appends (begin() size), 0 =  */
+                                   /* unknown; > 2 selects the multi-row kernel     */
+                                   /* chain (prefill, token trees) over the         */
+                                   /* persistent single-launch decode layer         */
 } spx_layer_args;
 int spx_layer_forward(const spx_layer_args *args, void *stream);
 /* floats needed for s_part and int32s for s_flag at these dimensions */

@@ -67,7 +67,8 @@ class LayerArgs(ctypes.Structure):
                 ("rows", _vp), ("nrows", _vp), ("s_q", _vp), ("s_att", _vp), ("s_f", _vp),
                 ("s_part", _vp), ("s_flag", _vp),
                 ("layer", _i32), ("mode", _i32), ("err", _vp),
-                ("max_ctx", _i64), ("d", _i64), ("n_heads", _i64), ("ffn", _i64)]
+                ("max_ctx", _i64), ("d", _i64), ("n_heads", _i64), ("ffn", _i64),
+                ("rows_hint", _i32)]
 
 
 class TokenStateC(ctypes.Structure):

@@ -41,6 +41,7 @@ struct LayerParams {
   int layer, strict;
   int *err;
   int max_ctx, d, nh, ffn;
+  int rows_hint;
 };
 
 __device__ __forceinline__ bool exited(const LayerParams &p) { return p.done && *p.done; }
@@ -453,6 +454,7 @@ extern "C" int spx_layer_forward(const spx_layer_args *a, void *stream) {
   p.s_part = a->s_part; p.s_flag = a->s_flag;
   p.layer = a->layer; p.strict = a->mode == SPX_MODE_STRICT; p.err = a->err;
   p.max_ctx = (int)a->max_ctx; p.d = (int)a->d; p.nh = (int)a->n_heads; p.ffn = (int)a->ffn;
+  p.rows_hint = a->rows_hint;
   cudaStream_t s = (cudaStream_t)stream;
   if (a->w_dtype == SPX_DTYPE_BF16) launch_layer<__nv_bfloat16>(p, s);
   else if (a->w_dtype == SPX_DTYPE_F32) launch_layer<float>(p, s);

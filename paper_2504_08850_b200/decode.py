@@ -54,6 +54,7 @@ class DecodeState:
         self._tok_buf = torch.zeros(C, dtype=torch.int32, device=dev)
         self._pos_buf = torch.zeros(C, dtype=torch.int32, device=dev)
         self._any_frozen = False
+        self._hint = 0                   # rows appended by the last begin / embed_device
         self._largs = [self._layer_args(l) for l in range(L)]
 
     @property
@@ -80,12 +81,14 @@ class DecodeState:
         if attn_lists is not None:
             self._set_attn(rows, attn_lists)
         self.embed_device(self._tok_buf, toks.size, pos)
+        self._hint = int(toks.size)
         self.n += toks.size
         self.new_rows = rows
         return rows
 
     def embed_device(self, tokens: torch.Tensor, T: int, pos: torch.Tensor = None):
         """Append T rows whose tokens live in device memory (graph-capturable)."""
+        self._hint = int(T)
         m = self.model
         cfg = m.config
         N.check(N.lib().spx_embed(N.ptr(m.embedding), m.spx_dtype, N.ptr(m.pos_encoding),
@@ -147,6 +150,7 @@ class DecodeState:
         """Enqueue layer l (no host sync; graph-capturable)."""
         a = self._largs[l]
         a.mode = numerics.mode()
+        a.rows_hint = self._hint
         N.check(N.lib().spx_layer_forward(a, N.stream_ptr()), "spx_layer_forward")
 
     def run_layer(self, l: int):

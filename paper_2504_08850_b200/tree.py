@@ -18,8 +18,8 @@ from .model import (TransformerModel, _VerifyScratch, full_head_logits, head_pre
                     merged_logits, verify_args)
 from .predictor import decide_exit, extract_features, z_cut
 from .scheduler import OfflineProfile, OnlineState, ScheduleConfig, active_layers, update_online
-from .speculation import (SpeculativeSet, TokenTree, build_token_tree, enumerate_paths,
-                          propose_topk, speculative_set_from_logits)
+from .speculation import (SpeculativeSet, TokenTree, TreeNode, build_token_tree,
+                          enumerate_paths, propose_topk, speculative_set_from_logits)
 
 
 def grouped_speculative_logits(model: TransformerModel, hiddens, token_id_lists):
@@ -207,13 +207,66 @@ class TreeEngine:
             self.tstate = DecodeState(self.target)
         else:
             self.tstate.reset()
+        if self._dstate is None:
+            self._dstate = DecodeState(self.draft)
+        else:
+            self._dstate.reset()
         if len(prompt) > 1:
-            self.tstate.begin(prompt[:-1])
-            for l in range(self.target.config.num_layers):
-                self.tstate.launch_layer(l)
+            for st, m in ((self.tstate, self.target), (self._dstate, self.draft)):
+                st.begin(prompt[:-1])
+                for l in range(m.config.num_layers):
+                    st.launch_layer(l)
         self.online.reset()
         self.context = prompt
         self.policy.start(prompt)
+
+    def _draft_tree(self):
+        """build_token_tree + the per-node draft top-k of merge_paths
+        (speculation.py:87-125, tree.py:64-73) with a persistent draft KV cache:
+        the draft state holds context[:-1]; the tree is drafted level by level,
+        each level ONE batched forward of its nodes at positions m + depth with
+        ancestor-only attention -- exactly the keys and positions of the
+        reference's fresh full-context forward per node (speculation.py:63-68),
+        so the node logits are the same.  Returns (tree, node logits)."""
+        from .model import head_argmax
+        ds, d = self._dstate, self.draft
+        ctx = self.context
+        m = len(ctx) - 1
+        total, cnt = 1, 1
+        for b in self.branching:
+            cnt *= b
+            total += cnt
+        if len(ctx) + total > d.config.max_context:
+            raise ValueError("tree exceeds max context")
+        nodes = [TreeNode(token=int(ctx[-1]), parent=-1, depth=0)]
+        anc = {0: [0]}
+        level = [0]
+        logits = {}
+        for depth in range(len(self.branching) + 1):
+            toks = [nodes[j].token for j in level]
+            if depth == 0:
+                ds.begin(toks)
+            else:
+                ds.begin(toks, pos_ids=[m + depth] * len(level),
+                         attn_lists=[list(range(m)) + [m + a for a in anc[j]] for j in level])
+            for l in range(d.config.num_layers):
+                ds.launch_layer(l)
+            r0 = ds.n - len(level)
+            _, _, lg = head_argmax(d, ds.pending[r0:ds.n], want_logits=True)
+            for i, j in enumerate(level):
+                logits[j] = lg[i]
+            if depth == len(self.branching):
+                break
+            nxt = []
+            for j in level:
+                spec = speculative_set_from_logits(logits[j], self.branching[depth])
+                for tok, pr in zip(spec.tokens, spec.draft_probs):
+                    nodes.append(TreeNode(token=int(tok), parent=j, depth=depth + 1, prob=pr))
+                    c = len(nodes) - 1
+                    anc[c] = anc[j] + [c]
+                    nxt.append(c)
+            level = nxt
+        return TokenTree(nodes=nodes, branching=self.branching), logits
 
     def _active_layers(self):
         L = self.target.config.num_layers
@@ -234,9 +287,18 @@ class TreeEngine:
         from .engine import PredictorPolicy  # noqa: F401
         cfg = self.target.config
         L, K = cfg.num_layers, self.config.k
-        self._logit_cache = {}
-        tree = build_token_tree(self.draft, self.context, self.branching, propose=self._propose)
-        hts = merge_paths(tree, self.draft, self.context, K, propose=self._propose)
+        tree, node_logits = self._draft_tree()
+        ctx_len = len(self.context)
+        if K > self.draft.config.vocab_size:
+            raise ValueError("k exceeds vocabulary size")
+        def propose(context, k):                  # node context -> that node's own logits
+            j = self._node_of_context[tuple(context[ctx_len:])]
+            return speculative_set_from_logits(node_logits[j], k)
+        self._node_of_context = {}
+        for j, n in enumerate(tree.nodes):
+            if j:
+                self._node_of_context[tuple(tree.nodes[i].token for i in tree.path_to(j))] = j
+        hts = merge_paths(tree, self.draft, self.context, K, propose=propose)
         paths = [ht.path for ht in hts]
         P, n_nodes = len(paths), len(tree.nodes)
         m = len(self.context) - 1
@@ -391,6 +453,7 @@ class TreeEngine:
         accepted = [tree.nodes[j].token for j in acc_nodes]
         correction = preds[best_p][best_len]
         self.tstate.compact([rows[0]] + [rows[j] for j in acc_nodes], m)
+        self._dstate.compact([m] + [m + j for j in acc_nodes], m)
         self.context.extend(accepted + [correction])
         for _ in range(len(accepted) + 1):
             update_online(self.online, exit_layer[best_p])
