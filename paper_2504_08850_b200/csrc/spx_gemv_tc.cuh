@@ -36,6 +36,7 @@ constexpr int TC_SMEM = 210 * 1024;
 
 struct TcGeom {
   int nout, kin, nblk, P, units, maxr, xpitch;
+  int r_begin, last;       // row slice of this launch (multi-row calls: one launch per slice)
 };
 
 __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1,
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(TT, 1) gemv_tc_kernel(LayerParams p, TcGeom g)
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char *xa = smem;
   float *scr = reinterpret_cast<float *>(smem + (size_t)2 * g.maxr * g.xpitch);
-  int *rows = reinterpret_cast<int *>(scr + TWARPS);
+  int *rows_all = reinterpret_cast<int *>(scr + TWARPS);
   __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g8 = lane >> 2, cq = lane & 3;
@@ -224,7 +225,11 @@ __global__ void __launch_bounds__(TT, 1) gemv_tc_kernel(LayerParams p, TcGeom g)
   pdl_wait();
   if (flag_set(p.done)) return;
   pdl_trigger();
-  const int nrows = cta_row_set(p, rows);
+  const int nall = cta_row_set(p, rows_all);
+  // this launch's slice of the row set: maxr rows, or everything left (last)
+  const int rb = g.r_begin < nall ? g.r_begin : nall;
+  const int nrows = g.last ? nall - rb : (nall - rb < g.maxr ? nall - rb : g.maxr);
+  const int *rows = rows_all + rb;
 
   if (nrows <= g.maxr) {
     const int nr = nrows;
@@ -326,8 +331,9 @@ __global__ void __launch_bounds__(TT, 1) gemv_tc_kernel(LayerParams p, TcGeom g)
     __syncthreads();
     if (s_last) {
       __threadfence();
-      for (int i = tid; i < nrows; i += TT) p.frontier[rows[i]] = p.layer + 1;
-      if (p.cur_hidden && p.new_row) {
+      if (g.last)
+        for (int i = tid; i < nall; i += TT) p.frontier[rows_all[i]] = p.layer + 1;
+      if (g.last && p.cur_hidden && p.new_row) {
         const int nw = *reinterpret_cast<const volatile int32_t *>(p.new_row);
         if (nw >= 0)
           for (int j = tid; j < p.d; j += TT) p.cur_hidden[j] = __ldcg(p.pending + (size_t)nw * p.d + j);
@@ -352,6 +358,8 @@ static TcGeom tc_geom(int nout, int kin, int max_ctx, size_t &smem) {
   const size_t fixed = TWARPS * 4 + (size_t)max_ctx * 4 + 256;
   int mr = (int)((TC_SMEM - fixed) / (2 * (size_t)pitch));
   g.maxr = mr > 8 ? 8 : mr;
+  g.r_begin = 0;
+  g.last = 1;
   smem = 2 * (size_t)g.maxr * pitch + fixed;
   return g;
 }
@@ -363,13 +371,22 @@ static bool tc_layer_supported(const LayerParams &p) {
          tc_geom(p.ffn, p.d, p.max_ctx, smem).maxr >= 1;
 }
 
+// Multi-row calls (rows_hint > maxr: prefill, token trees) run one launch per
+// slice of maxr rows so every slice takes the split-K path; the frontier and
+// newest-row copy happen in the last slice only, so all slices see the same
+// row set.
 template <int EPI>
 static void launch_tc(const LayerParams &p, int nout, int kin, int sms, cudaStream_t s) {
   size_t smem;
-  const TcGeom g = tc_geom(nout, kin, p.max_ctx, smem);
+  TcGeom g = tc_geom(nout, kin, p.max_ctx, smem);
   cudaFuncSetAttribute(gemv_tc_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   int grid = g.units / TWARPS;
   grid = grid < 1 ? 1 : grid > sms ? sms : grid;
-  launch_pdl(gemv_tc_kernel<EPI>, grid, TT, smem, s, p, g);
+  const int slices = p.rows_hint > g.maxr ? (p.rows_hint + g.maxr - 1) / g.maxr : 1;
+  for (int sl = 0; sl < slices; ++sl) {
+    g.r_begin = sl * g.maxr;
+    g.last = sl == slices - 1;
+    launch_pdl(gemv_tc_kernel<EPI>, grid, TT, smem, s, p, g);
+  }
 }
