@@ -273,15 +273,19 @@ __device__ __forceinline__ void mg_phase(const LayerParams &p, const MegaGeom &g
 constexpr int MG_ATT_KEYS = 512;                // max context per item
 constexpr int MG_ATT_W = 8;                     // attention warps per CTA
 constexpr int MG_AB = 8;                        // keys per batch
-template <int NP>                               // 4-dim pieces per lane: dh <= 128 * NP
-__device__ void mg_attention_np(const LayerParams &p, const int *rows, int nrows) {
+// Items (row, head) are few at decode (32 at 7B) and the HBM is saturated by
+// the weight stream, so latency dominates: each item takes one CTA and its 8
+// attention warps split the keys (contiguous ranges); every warp runs the
+// batched online softmax over its range, then the 8 partial (max, sum, acc)
+// triples are merged in shared memory in warp order.
+template <int NP>
+__device__ void mg_attention_split(const LayerParams &p, const int *rows, int nrows, float *sc_all) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp >= MG_ATT_W) return;
   const int d = p.d, nh = p.nh, dh = d / nh;
   const float scale = (float)(1.0 / sqrt((double)dh));
-  const int gw = blockIdx.x * MG_ATT_W + warp, nw = gridDim.x * MG_ATT_W;
-  const int npart = NP;
-  for (int item = gw; item < nrows * nh; item += nw) {
+  float *part = sc_all;                        // [MG_ATT_W][4 + 128 * NP]: m, l, pad, acc
+  const int pstride = 4 + 128 * NP;
+  for (int item = blockIdx.x; item < nrows * nh; item += gridDim.x) {
     const int row = rows[item / nh], h = item % nh;
     const int *ctx = nullptr;
     int nctx = row + 1;
@@ -290,87 +294,104 @@ __device__ void mg_attention_np(const LayerParams &p, const int *rows, int nrows
       nctx = p.attn_ptr[row + 1] - p.attn_ptr[row];
     }
     const size_t hoff = (size_t)h * dh;
-    float4 qv[NP];
-#pragma unroll
-    for (int k = 0; k < NP; ++k) {
-      const int e = lane * 4 + 128 * k;
-      qv[k] = (k < npart && e < dh)
-                  ? __ldcg(reinterpret_cast<const float4 *>(p.s_q + (size_t)row * d + hoff + e))
-                  : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    float m = -INFINITY, l = 0.f;
-    float4 acc[NP];
-#pragma unroll
-    for (int k = 0; k < NP; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int j0 = 0; j0 < nctx; j0 += MG_AB) {
-      float4 kb[MG_AB][NP], vb[MG_AB][NP];
-#pragma unroll
-      for (int t = 0; t < MG_AB; ++t) {
-        const int jj = j0 + t;
-        const int pos = jj < nctx ? (ctx ? ctx[jj] : jj) : 0;
-#pragma unroll
-        for (int k = 0; k < NP; ++k) {
-          const int e = lane * 4 + 128 * k;
-          const bool ok = jj < nctx && k < npart && e < dh;
-          kb[t][k] = ok ? __ldcg(reinterpret_cast<const float4 *>(p.kc + (size_t)pos * d + hoff + e))
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
-          vb[t][k] = ok ? __ldcg(reinterpret_cast<const float4 *>(p.vc + (size_t)pos * d + hoff + e))
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
-      float sc[MG_AB];
-#pragma unroll
-      for (int t = 0; t < MG_AB; ++t) {
-        float a = 0.f;
-#pragma unroll
-        for (int k = 0; k < NP; ++k)
-          a = fmaf(kb[t][k].x, qv[k].x, fmaf(kb[t][k].y, qv[k].y,
-              fmaf(kb[t][k].z, qv[k].z, fmaf(kb[t][k].w, qv[k].w, a))));
-        sc[t] = a;
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1)
-#pragma unroll
-        for (int t = 0; t < MG_AB; ++t) sc[t] += __shfl_xor_sync(0xffffffffu, sc[t], o);
-      float bm = m;
-#pragma unroll
-      for (int t = 0; t < MG_AB; ++t) {
-        sc[t] = (j0 + t < nctx) ? sc[t] * scale : -INFINITY;
-        bm = fmaxf(bm, sc[t]);
-      }
-      const float corr = np_expf(m - bm);
-      l *= corr;
+    if (warp < MG_ATT_W) {
+      const int per = (nctx + MG_ATT_W - 1) / MG_ATT_W;
+      const int ja = warp * per, jb = ja + per < nctx ? ja + per : nctx;
+      float4 qv[NP];
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
-        acc[k].x *= corr; acc[k].y *= corr; acc[k].z *= corr; acc[k].w *= corr;
+        const int e = lane * 4 + 128 * k;
+        qv[k] = e < dh ? __ldcg(reinterpret_cast<const float4 *>(p.s_q + (size_t)row * d + hoff + e))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
       }
+      float m = -INFINITY, l = 0.f;
+      float4 acc[NP];
 #pragma unroll
-      for (int t = 0; t < MG_AB; ++t) {
-        const float pe = np_expf(sc[t] - bm);
-        l += pe;
+      for (int k = 0; k < NP; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j0 = ja; j0 < jb; j0 += MG_AB) {
+        float4 kb[MG_AB][NP], vb[MG_AB][NP];
+#pragma unroll
+        for (int t = 0; t < MG_AB; ++t) {
+          const int jj = j0 + t;
+          const int pos = jj < jb ? (ctx ? ctx[jj] : jj) : 0;
+#pragma unroll
+          for (int k = 0; k < NP; ++k) {
+            const int e = lane * 4 + 128 * k;
+            const bool ok = jj < jb && e < dh;
+            kb[t][k] = ok ? __ldcg(reinterpret_cast<const float4 *>(p.kc + (size_t)pos * d + hoff + e))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+            vb[t][k] = ok ? __ldcg(reinterpret_cast<const float4 *>(p.vc + (size_t)pos * d + hoff + e))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+        float sc[MG_AB];
+#pragma unroll
+        for (int t = 0; t < MG_AB; ++t) {
+          float a = 0.f;
+#pragma unroll
+          for (int k = 0; k < NP; ++k)
+            a = fmaf(kb[t][k].x, qv[k].x, fmaf(kb[t][k].y, qv[k].y,
+                fmaf(kb[t][k].z, qv[k].z, fmaf(kb[t][k].w, qv[k].w, a))));
+          sc[t] = a;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1)
+#pragma unroll
+          for (int t = 0; t < MG_AB; ++t) sc[t] += __shfl_xor_sync(0xffffffffu, sc[t], o);
+        float bm = m;
+#pragma unroll
+        for (int t = 0; t < MG_AB; ++t) {
+          sc[t] = (j0 + t < jb) ? sc[t] * scale : -INFINITY;
+          bm = fmaxf(bm, sc[t]);
+        }
+        const float corr = np_expf(m - bm);
+        l *= corr;
 #pragma unroll
         for (int k = 0; k < NP; ++k) {
-          acc[k].x = fmaf(pe, vb[t][k].x, acc[k].x); acc[k].y = fmaf(pe, vb[t][k].y, acc[k].y);
-          acc[k].z = fmaf(pe, vb[t][k].z, acc[k].z); acc[k].w = fmaf(pe, vb[t][k].w, acc[k].w);
+          acc[k].x *= corr; acc[k].y *= corr; acc[k].z *= corr; acc[k].w *= corr;
         }
-      }
-      m = bm;
-    }
-    const float inv = 1.0f / l;
 #pragma unroll
-    for (int k = 0; k < NP; ++k) {
-      const int e = lane * 4 + 128 * k;
-      if (k < npart && e < dh)
-        *reinterpret_cast<float4 *>(p.s_att + (size_t)row * d + hoff + e) =
-            make_float4(acc[k].x * inv, acc[k].y * inv, acc[k].z * inv, acc[k].w * inv);
+        for (int t = 0; t < MG_AB; ++t) {
+          const float pe = np_expf(sc[t] - bm);
+          l += pe;
+#pragma unroll
+          for (int k = 0; k < NP; ++k) {
+            acc[k].x = fmaf(pe, vb[t][k].x, acc[k].x); acc[k].y = fmaf(pe, vb[t][k].y, acc[k].y);
+            acc[k].z = fmaf(pe, vb[t][k].z, acc[k].z); acc[k].w = fmaf(pe, vb[t][k].w, acc[k].w);
+          }
+        }
+        m = bm;
+      }
+      float *pw = part + (size_t)warp * pstride;
+      if (lane == 0) { pw[0] = m; pw[1] = l; }
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const int e = lane * 4 + 128 * k;
+        if (e < dh) *reinterpret_cast<float4 *>(pw + 4 + e) = acc[k];
+      }
     }
+    mg_cbar();
+    // merge the warps' partials in warp order (threads own dims)
+    for (int e = threadIdx.x; e < dh; e += MG_CT) {
+      float M = -INFINITY;
+      for (int w = 0; w < MG_ATT_W; ++w) M = fmaxf(M, part[(size_t)w * pstride]);
+      float L = 0.f, A = 0.f;
+      for (int w = 0; w < MG_ATT_W; ++w) {
+        const float mw = part[(size_t)w * pstride];
+        const float f = mw == -INFINITY ? 0.f : np_expf(mw - M);
+        L = fmaf(part[(size_t)w * pstride + 1], f, L);
+        A = fmaf(part[(size_t)w * pstride + 4 + e], f, A);
+      }
+      p.s_att[(size_t)row * d + hoff + e] = A / L;
+    }
+    mg_cbar();
   }
 }
 
 __device__ __forceinline__ void mg_attention(const LayerParams &p, const int *rows, int nrows,
-                                             float *) {
-  if (p.d / p.nh <= 128) mg_attention_np<1>(p, rows, nrows);
-  else mg_attention_np<2>(p, rows, nrows);
+                                             float *sc) {
+  if (p.d / p.nh <= 128) mg_attention_split<1>(p, rows, nrows, sc);
+  else mg_attention_split<2>(p, rows, nrows, sc);
 }
 
 template <int CD, int CF>                       // chunks per thread for d / ffn inputs
