@@ -542,7 +542,10 @@ static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cu
       const int budget = ldgx ? 113 * 1024 : g_smem_optin;
       StreamPlan st = plan_stream<TW>(p.d, p.K, p.H, budget, ldgx);
       if (st.bytes) {
-        const long long cap = ldgx ? 2LL * g_sms : g_sms;
+        // SPX_PRED_CTAS_PER_SM (sweeps): 1 leaves the second CTA slot of every SM
+        // free for the next (programmatic dependent) launch's prefetch
+        static const int env_cps = getenv("SPX_PRED_CTAS_PER_SM") ? atoi(getenv("SPX_PRED_CTAS_PER_SM")) : 2;
+        const long long cap = ldgx ? (long long)(env_cps > 0 ? env_cps : 2) * g_sms : g_sms;
         const int grid = (int)(a->B < cap ? a->B : cap);
         StreamLaunch<TW> L{p, st, grid, stream, g_smem_optin, ldgx};
         if (p.d == 2048) L.template operator()<4>();
