@@ -57,9 +57,10 @@ inline StreamPlan plan_stream(int d, int K, int H, int max_bytes, bool ldgx = fa
                        /*tail*/ SW_TAIL * (((size_t)(3 * SKMAX + H + 32) * 4 + 127) / 128 * 128) +
                        /*hdr*/ 8 * 16 + /*ids*/ SWIN * SKMAX * 4 + /*bars*/ (2 * 8 + 2 * SQS + 2) * 8 +
                        1024;
-  for (int S = 4; S >= 2; --S) {
-    const bool w1 = H > 0 && fixed + S * slot + w1b <= (size_t)max_bytes;
-    if (ldgx && !w1) continue;                          // two CTAs/SM only with W1 resident
+  // deepest ring with W1 resident first; W1 through L1 only as the last resort
+  for (int S = 4; S >= 1; --S) {
+    bool w1 = H > 0 && fixed + S * slot + w1b <= (size_t)max_bytes;
+    if (!w1 && S > 1 && H > 0) continue;
     if (fixed + S * slot + (w1 ? w1b : 0) > (size_t)max_bytes) continue;
     size_t o = 0;
     s.S = S;
@@ -91,7 +92,7 @@ __device__ __forceinline__ void cbar_sync() {          // the 16 compute warps
 }
 
 template <typename TW, int CPL, int KC, int HC, bool W1S, bool LDGX>
-__global__ void __launch_bounds__(SW_THREADS, LDGX ? 2 : 1)
+__global__ void __launch_bounds__(SW_THREADS, 2)
 predictor_stream_kernel(PredParams p, StreamPlan sp) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -451,8 +452,11 @@ struct StreamLaunch {
   bool ldgx;
   template <int CPL> void operator()() const {
     if (ldgx) {
-      if (p.K == 4 && p.H == 512 && p.policy == SPX_POLICY_MLP) launch<CPL, 4, 512, true, true>();
-      else launch<CPL, 0, 0, true, true>();
+      if (p.K == 4 && p.H == 512 && p.policy == SPX_POLICY_MLP) {
+        if (sp.w1_smem) launch<CPL, 4, 512, true, true>(); else launch<CPL, 4, 512, false, true>();
+      } else {
+        if (sp.w1_smem) launch<CPL, 0, 0, true, true>(); else launch<CPL, 0, 0, false, true>();
+      }
       return;
     }
     if (p.K == 4 && p.H == 512 && p.policy == SPX_POLICY_MLP) {

@@ -525,7 +525,16 @@ static void device_limits() {
 template <typename TW>
 static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cudaStream_t stream) {
   device_limits();
-  if (a->mode == SPX_MODE_STRICT) {
+  bool strict = a->mode == SPX_MODE_STRICT;
+  if (!strict) {
+    // FAST shapes that neither the stream nor the team kernel can stage in shared
+    // memory (e.g. d = 8192 with K > 8) take the reference-order kernel: exact,
+    // one CTA per request
+    const bool stream_ok = std::is_same<TW, __nv_bfloat16>::value && p.K <= SKMAX &&
+                           (p.d == 2048 || p.d == 4096 || p.d == 8192);
+    if (!stream_ok && plan_smem<TW>(p.d, p.K, p.H, g_smem_optin).bytes == 0) strict = true;
+  }
+  if (strict) {
     const size_t smem = (size_t)a->d * sizeof(float);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(predictor_strict_kernel<TW>,
@@ -533,19 +542,37 @@ static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cu
     predictor_strict_kernel<TW><<<(unsigned)a->B, STRICT_THREADS, smem, stream>>>(p);
   } else {
     if (((size_t)p.d * sizeof(TW)) % 16) return SPX_EINVAL;   // TMA bulk: 16-byte rows
-    static const int env_stream = getenv("SPX_PRED_STREAM") ? atoi(getenv("SPX_PRED_STREAM")) : 2;
+    static const int env_stream = getenv("SPX_PRED_STREAM") ? atoi(getenv("SPX_PRED_STREAM")) : 3;
     if (std::is_same<TW, __nv_bfloat16>::value && env_stream && p.K <= SKMAX &&
         (p.d == 2048 || p.d == 4096 || p.d == 8192) && (p.policy != SPX_POLICY_MLP || p.H <= 1024)) {
       // env_stream: 1 = ring of whole evaluations, one CTA/SM; 2 = hidden rows by
       // ld.global, LM-head ring, two CTAs/SM
-      const bool ldgx = env_stream == 2;
-      const int budget = ldgx ? 113 * 1024 : g_smem_optin;
-      StreamPlan st = plan_stream<TW>(p.d, p.K, p.H, budget, ldgx);
+      // Two CTAs per SM whenever a 2-slot ring + W1 fit in half the shared
+      // memory: hidden rows staged with the LM-head rows when the slot is small
+      // (K <= 2 at d = 4096), else hidden rows by ld.global (LDGX, K <= 4);
+      // otherwise one CTA per SM with the whole budget.  SPX_PRED_STREAM: 1 /
+      // 2 force the staged / LDGX variant (sweeps), 3 = automatic.
+      // (measured: with two CTAs per SM the ld.global hidden rows win; with one
+      // CTA per SM staging the hidden rows in the slot wins, e.g. d = 8192)
+      const int half = 113 * 1024;
+      bool ldgx = env_stream != 1;
+      int per_sm = 2;
+      StreamPlan st = plan_stream<TW>(p.d, p.K, p.H, half, ldgx);
+      if ((!st.bytes || st.S < 2) && env_stream == 3) {
+        ldgx = false;
+        st = plan_stream<TW>(p.d, p.K, p.H, half, false);
+      }
+      if (!st.bytes || st.S < 2) {
+        ldgx = env_stream == 2;
+        st = plan_stream<TW>(p.d, p.K, p.H, g_smem_optin, ldgx);
+        per_sm = 1;
+      }
       if (st.bytes) {
         // SPX_PRED_CTAS_PER_SM (sweeps): 1 leaves the second CTA slot of every SM
         // free for the next (programmatic dependent) launch's prefetch
         static const int env_cps = getenv("SPX_PRED_CTAS_PER_SM") ? atoi(getenv("SPX_PRED_CTAS_PER_SM")) : 2;
-        const long long cap = ldgx ? (long long)(env_cps > 0 ? env_cps : 2) * g_sms : g_sms;
+        if (env_cps == 1) per_sm = 1;
+        const long long cap = (long long)per_sm * g_sms;
         const int grid = (int)(a->B < cap ? a->B : cap);
         StreamLaunch<TW> L{p, st, grid, stream, g_smem_optin, ldgx};
         if (p.d == 2048) L.template operator()<4>();

@@ -48,7 +48,7 @@ def run(m, w, hidden, ids, prev, mode, thr=0.5, **kw):
     return out, p
 
 
-@pytest.mark.parametrize("d", [2048, 4096])
+@pytest.mark.parametrize("d", [2048, 4096, 8192])
 @pytest.mark.parametrize("K", [1, 2, 3, 4, 5, 8])
 def test_stream_matches_strict(d, K):
     m = head(d)
