@@ -278,6 +278,13 @@ def decode_bench(args, rank, ws, dev):
     torch.cuda.synchronize()
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     recs = eng._dev.records(n)
+    if ws > 1:
+        # results gather after the timed region: every rank's
+        # ExitRecord fields, one all_gather over NCCL
+        from paper_2504_08850_b200 import shard
+        packed = torch.as_tensor(shard.pack_records(recs), device=dev)
+        gathered = [torch.empty_like(packed) for _ in range(ws)]
+        dist.all_gather(gathered, packed)
     t0 = time.perf_counter()
     toks, trace = eng.generate(prompt, n)
     e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
