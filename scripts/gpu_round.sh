@@ -15,7 +15,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 B=1024 ITERS=8 timeout 600 ncu --set full --clock-control none --import-source on -k regex:predictor_stream -s 4 -c 1 -o gpurun_out/prof_pred -f python scripts/prof_predictor.py > gpurun_out/prof_pred.log 2>&1; echo "ncu_pred rc=$?" >> gpurun_out/status.txt
 ncu -i gpurun_out/prof_pred.ncu-rep --page raw --csv > gpurun_out/prof_pred_raw.csv 2>/dev/null
 ncu -i gpurun_out/prof_pred.ncu-rep --page details --csv > gpurun_out/prof_pred_details.csv 2>/dev/null
-timeout 600 ncu --set full --clock-control none -k regex:layer_mega -s 6 -c 1 -o /tmp/prof_layer -f python scripts/prof_layer.py --layers 2 --steps 2 > gpurun_out/prof_layer.log 2>&1; echo "ncu_layer rc=$?" >> gpurun_out/status.txt
+timeout 600 ncu --set full --clock-control none -k regex:layer_mega -s 2 -c 1 -o /tmp/prof_layer -f python scripts/prof_layer.py --layers 2 --steps 2 > gpurun_out/prof_layer.log 2>&1; echo "ncu_layer rc=$?" >> gpurun_out/status.txt
 ncu -i /tmp/prof_layer.ncu-rep --page raw --csv > gpurun_out/prof_layer_raw.csv 2>/dev/null
 ncu -i /tmp/prof_layer.ncu-rep --page details --csv > gpurun_out/prof_layer_details.csv 2>/dev/null
 ls -la gpurun_out >> gpurun_out/status.txt; du -sh gpurun_out >> gpurun_out/status.txt
