@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(MG_T, 1) layer_mega_kernel(LayerParams p, Mega
   float *scr = red + (size_t)MG_CW * g.red_stride;                    // [NRP][16]
   int *rows = reinterpret_cast<int *>(scr + MG_NRP * MG_CW);          // [max_ctx]
   float *att_sc = red;        // attention scores [8][512] alias the idle partial buffer
-  __shared__ int s_last, s_skip, s_nrows;
+  __shared__ int s_last, s_skip, s_skip2;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x;
   int32_t *bar_ctr = p.s_flag, *end_ctr = p.s_flag + 1;
@@ -449,9 +449,9 @@ __global__ void __launch_bounds__(MG_T, 1) layer_mega_kernel(LayerParams p, Mega
     for (; pre < MG_SLOTS && pre < n0; ++pre) issue(pre, 0, pre);
   }
   pdl_wait();
-  if (tid == 0) s_skip = flag_set(p.done) ? 1 : 0;
+  if (tid == 0) s_skip2 = flag_set(p.done) ? 1 : 0;
   __syncthreads();
-  if (s_skip) {                                   // exit decided just before: drain
+  if (s_skip2) {                                  // exit decided just before: drain
     if (warp == MG_CW && lane == 0)
       for (int j = 0; j < pre; ++j) mbar_wait(&full[j], 0);
     __syncthreads();
@@ -517,7 +517,6 @@ __global__ void __launch_bounds__(MG_T, 1) layer_mega_kernel(LayerParams p, Mega
     if (tid == 0) { *bar_ctr = 0; *end_ctr = 0; }
   }
   mg_stamp(12);
-  (void)s_nrows;
 }
 
 static size_t mega_smem(const LayerParams &p, int sms) {

@@ -1,0 +1,55 @@
+"""Small workload for compute-sanitizer (memcheck / racecheck / synccheck):
+the stream predictor kernel (d=4096, K=4, two CTAs per SM), the team kernel
+(tiny d), one device TreeEngine step and a few decode steps through the
+persistent layer kernel."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2504_08850_b200 as spx  # noqa: E402
+from paper_2504_08850_b200 import engine as E  # noqa: E402
+from paper_2504_08850_b200 import numerics, rng  # noqa: E402
+from paper_2504_08850_b200 import tree as T  # noqa: E402
+
+numerics.set_mode("fast")
+# stream predictor kernel
+cfg = spx.ModelConfig(vocab_size=2048, hidden_dim=4096, num_layers=2, num_heads=32, ffn_dim=8192,
+                      max_context=32, seed=3)
+m = spx.init_model(cfg, dtype="bf16", head_only=True)
+w = spx.init_predictor(4, 512, 1)
+B = 320
+h = torch.randn((B, 4096), device="cuda")
+ids = torch.randint(0, 2048, (B, 4), device="cuda", dtype=torch.int32)
+ids[:, 1] = (ids[:, 0] + 1) % 2048
+ids[:, 2] = (ids[:, 0] + 2) % 2048
+ids[:, 3] = (ids[:, 0] + 3) % 2048
+prev = torch.full((B, 4), 0.25, device="cuda")
+out = spx.evaluate_batch(m, w, h, ids, prev, threshold=0.5, pdl=2)
+torch.cuda.synchronize()
+assert out.err.item() == 0
+# tiny engine (team kernel + decode layers + device graph) and one tree step
+t = spx.init_model(spx.ModelConfig(num_layers=4, seed=31), dtype="bf16")
+d = spx.init_model(spx.ModelConfig(num_layers=2, seed=32), dtype="bf16")
+bank = {l: spx.init_predictor(4, 512, rng.derive(77, l)) for l in range(3)}
+eng = E.ExitEngine(t, d, E.PredictorPolicy(bank), E.EngineConfig(threshold=0.5))
+print(eng.generate([84, 104, 101, 32], 3)[0])
+te = T.TreeEngine(t, d, E.PredictorPolicy(bank), (2, 2))
+te.start([84, 104, 101, 32])
+print(te.step().accepted_tokens)
+# persistent layer kernel at an LLM width (decode rows)
+cfg2 = spx.ModelConfig(vocab_size=512, hidden_dim=1024, num_layers=2, num_heads=8, ffn_dim=2816,
+                       max_context=32, seed=9)
+m2 = spx.init_model(cfg2, dtype="bf16")
+st = spx.DecodeState(m2)
+st.begin([1, 2, 3])
+for l in range(2):
+    st.run_layer(l)
+st.begin([4])
+for l in range(2):
+    st.run_layer(l)
+st.check()
+torch.cuda.synchronize()
+print("sanitize workload ok")
