@@ -15,7 +15,8 @@ from .predictor import (FeatureVector, PredictorBank, PredictorWeights, decide_e
 from .scheduler import (OfflineProfile, OnlineState, ScheduleConfig, active_layers,  # noqa: F401
                         load_profile, online_hot_layers, profile_offline, recompute_counts,
                         save_profile, update_online, weight_fingerprint)
-from .tree import grouped_speculative_logits, hypertoken_exit_decision  # noqa: F401
+from .tree import (HyperToken, TreeEngine, TreeStepResult, grouped_speculative_logits,  # noqa: F401
+                   hypertoken_exit_decision, hypertoken_oracle_exit, merge_paths)
 from .decode import DecodeState, forward_to_layer, prefill  # noqa: F401
 from .speculation import (SpeculativeSet, TokenTree, TreeNode, build_token_tree,  # noqa: F401
                           enumerate_paths, propose_topk, speculative_set_from_logits,
