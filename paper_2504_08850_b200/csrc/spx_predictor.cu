@@ -460,12 +460,25 @@ __global__ void features_wide_kernel(const float *logits, const float *prev, flo
     f[K + i] = np_expf(__fsub_rn(x[i], m));
   }
   __syncthreads();
-  if (tid == 0) {
-    float esum = 0.f, psum = 0.f;
-    for (int c = 0; c < K; ++c) {
-      esum = __fadd_rn(esum, f[K + c]);
-      psum = __fadd_rn(psum, pv[c]);
+  // the two sums stay strict left-to-right chains on thread 0; the operands are
+  // staged through shared memory in chunks so the chain never waits on HBM
+  constexpr int WCH = 2048;
+  __shared__ float s_e[WCH], s_p[WCH];
+  float esum = 0.f, psum = 0.f;
+  for (int c0 = 0; c0 < K; c0 += WCH) {
+    const int n = K - c0 < WCH ? K - c0 : WCH;
+    for (int i = tid; i < n; i += blockDim.x) { s_e[i] = f[K + c0 + i]; s_p[i] = pv[c0 + i]; }
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll 8
+      for (int c = 0; c < n; ++c) {
+        esum = __fadd_rn(esum, s_e[c]);
+        psum = __fadd_rn(psum, s_p[c]);
+      }
     }
+    __syncthreads();
+  }
+  if (tid == 0) {
     int e = 0;
     if (s_bad) e |= ERR_LOGIT_NONFINITE;
     if (fabs((double)psum - 1.0) > 1e-5) e |= ERR_PREV_SUM;
