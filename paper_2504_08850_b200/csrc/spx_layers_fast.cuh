@@ -62,11 +62,18 @@ __device__ int cta_row_set(const LayerParams &p, int *rows) {
   __shared__ int s_cnt;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (threadIdx.x == 0) s_cnt = 0;
+  // the first block of frontier / frozen entries is read together with n_ctx
+  // (independent loads: one memory round trip instead of two)
+  const int t0 = threadIdx.x;
+  const int f0 = t0 < p.max_ctx ? __ldcg(p.frontier + t0) : -1;
+  const bool z0 = p.frozen && t0 < p.max_ctx && p.frozen[t0];
   __syncthreads();
   const int n = *reinterpret_cast<const volatile int32_t *>(p.n_ctx);
   for (int base = 0; base < n; base += blockDim.x) {
     const int i = base + threadIdx.x;
-    const bool take = i < n && __ldcg(p.frontier + i) == p.layer && !(p.frozen && p.frozen[i]);
+    const bool take = i < n && (base == 0 ? (f0 == p.layer && !z0)
+                                          : (__ldcg(p.frontier + i) == p.layer &&
+                                             !(p.frozen && p.frozen[i])));
     const unsigned m = __ballot_sync(0xffffffffu, take);
     if (lane == 0) s_wc[w] = __popc(m);
     __syncthreads();
