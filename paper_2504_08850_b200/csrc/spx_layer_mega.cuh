@@ -207,6 +207,17 @@ __device__ __forceinline__ void mg_phase(const LayerParams &p, const MegaGeom &g
     const int nr = nrows - r0 < MG_NRP ? nrows - r0 : MG_NRP;
     float x[MG_NRP][CPT * 8];
     mg_load_x<EPI, CPT>(p, rows, r0, nr, kin, x, scr);
+    // the epilogue's operands (residual row entries, biases) of this thread's
+    // first output are fetched now, so their latency hides behind the stages
+    float pre_a = 0.f, pre_b = 0.f;
+    const int idx0 = tid;
+    const bool has0 = idx0 < nloc * MG_NRP && (idx0 % MG_NRP) < nr;
+    if (has0) {
+      const int o = o_begin + idx0 / MG_NRP, row = rows[r0 + idx0 % MG_NRP];
+      if (EPI == EPI_WO || EPI == EPI_FFN2) pre_a = __ldcg(p.pending + (size_t)row * p.d + o);
+      if (EPI == EPI_FFN1) pre_b = __ldg(p.b1 + o);
+      if (EPI == EPI_FFN2) pre_b = __ldg(p.b2 + o);
+    }
     for (int st = 0; st < nst; ++st, ++job) {
       const int slot = job % MG_SLOTS;
       mbar_wait(&full[slot], (job / MG_SLOTS) & 1);
@@ -257,7 +268,17 @@ __device__ __forceinline__ void mg_phase(const LayerParams &p, const MegaGeom &g
         float v = 0.f;
 #pragma unroll
         for (int w2 = 0; w2 < MG_CW; ++w2) v += red[(size_t)w2 * g.red_stride + idx];
-        gemv_epilogue<EPI>(p, rows[r0 + r], o_begin + i, v);
+        const int row = rows[r0 + r], o = o_begin + i;
+        if (idx != idx0 || EPI == EPI_QKV) {
+          gemv_epilogue<EPI>(p, row, o, v);
+        } else if (EPI == EPI_WO) {
+          p.pending[(size_t)row * p.d + o] = __fadd_rn(pre_a, v);
+        } else if (EPI == EPI_FFN1) {
+          const float z = __fadd_rn(v, pre_b);
+          p.s_f[(size_t)row * p.ffn + o] = z > 0.f ? z : 0.f;
+        } else {
+          p.pending[(size_t)row * p.d + o] = __fadd_rn(__fadd_rn(pre_a, v), pre_b);
+        }
       }
     }
     mg_cbar();                                    // red reused by the next pass
