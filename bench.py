@@ -65,7 +65,27 @@ def parse():
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-tree", action="store_true")
     ap.add_argument("--decode-tokens", type=int, default=32)
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU/gloo rehearsal of the N-rank plumbing (no kernels)")
     return ap.parse_args()
+
+
+def maybe_relaunch(args):
+    """`bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run
+    with N ranks on this node (one process per GPU, 127.0.0.1 rendezvous) and
+    exit with its status; rank 0 prints the JSON line."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def dist_env():
@@ -318,8 +338,94 @@ def decode_bench(args, rank, ws, dev):
 
 
 
+def parity_check(spx, model, bank, bank_w, hidden, ids_all, outs, stream, prev, prev0, B,
+                 rows=64):
+    """Checker (untimed, rank 0): the decisions and probabilities of the
+    benchmarked step against the oracle's reference chain (oracle/, the CPU
+    restatement of model.py:298-314 + predictor.py:42-109) on a row sample,
+    all 31 layers chained through prev -- at the bench threshold (the last
+    timed replay's outputs) and at thr 0.5 (one extra untimed step)."""
+    import torch
+    from oracle import specexit_oracle as O
+    from paper_2504_08850_b200 import numerics
+    sel = np.linspace(0, B - 1, rows).astype(np.int64)
+    ids_s = ids_all[:, sel]
+    uniq, inv = np.unique(ids_s, return_inverse=True)
+    cols = model.lm_head[torch.as_tensor(uniq, device=hidden.device, dtype=torch.long)]
+    t = {"lm_head": np.ascontiguousarray(cols.float().cpu().numpy().T),
+         "final_norm.g": model.final_g.cpu().numpy(), "final_norm.b": model.final_b.cpu().numpy()}
+    oid = inv.reshape(ids_s.shape)
+    hid = hidden[:, torch.as_tensor(sel, device=hidden.device)].cpu().numpy()
+    ow = [O.PredictorWeights(bank_w[l].w1, bank_w[l].b1, bank_w[l].w2, bank_w[l].b2)
+          for l in range(PRED_LAYERS)]
+    res = {}
+    for thr in (THRESHOLD, 0.5):
+        if thr == THRESHOLD:
+            torch.cuda.synchronize()
+            fired = torch.stack([o.fired for o in outs]).cpu().numpy()[:, sel]
+            prob = torch.stack([o.prob for o in outs]).cpu().numpy()[:, sel]
+        else:
+            with torch.cuda.stream(stream), numerics.using("fast"):
+                prev.copy_(prev0)
+                spx.prev_error(prev).zero_()
+                fs, ps = [], []
+                for l in range(PRED_LAYERS):
+                    o = spx.evaluate_batch(model, bank, hidden[l], torch.as_tensor(
+                        ids_all[l], device=hidden.device), prev, threshold=thr, layer=l)
+                    fs.append(o.fired)
+                    ps.append(o.prob)
+            torch.cuda.synchronize()
+            fired = torch.stack(fs).cpu().numpy()[:, sel]
+            prob = torch.stack(ps).cpu().numpy()[:, sel]
+        mism, perr, margin = 0, 0.0, float("inf")
+        for j in range(rows):
+            pv = O.uniform_probs(K)
+            for l in range(PRED_LAYERS):
+                fv = O.extract_features(O.sliced_head_logits(t, hid[l, j], oid[l, j]), pv)
+                p = O.predictor_forward(ow[l], fv)
+                mism += int(bool(fired[l, j]) != (p > thr))
+                perr = max(perr, abs(float(prob[l, j]) - p))
+                margin = min(margin, abs(p - thr))
+                pv = fv.local_probs
+        res[str(thr)] = {"decision_mismatches": mism, "max_prob_err": perr, "min_margin": margin,
+                         "fire_rate": float(fired.mean())}
+    return {"checker": "oracle/specexit_oracle.py reference chain (CPU)", "rows": rows,
+            "layers": PRED_LAYERS, "thresholds": res}
+
+
+def dry_run(args):
+    """CPU rehearsal of the N-rank plumbing with gloo: each rank takes its
+    contiguous request shard, produces per-request records, and rank 0 prints
+    the gathered shapes -- the same collectives the GPU run makes after its
+    timed region, no kernels."""
+    import torch
+    import torch.distributed as dist
+    from paper_2504_08850_b200 import shard
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    total = args.batch * ws
+    a, b = shard.shard_range(total, rank, ws)
+    ids = np.arange(a, b)
+    local = torch.as_tensor(np.stack([ids, ids % LAYERS, ids % 2, ids % 3 == 0, np.ones_like(ids),
+                                      ids % 7], axis=1).astype(np.int32))
+    full = shard.gather_rows(local, total) if ws > 1 else local
+    tmax = shard.max_over_ranks(1.0 + rank, "cpu")
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": ws, "requests": total,
+                          "gathered_shape": list(full.shape),
+                          "gathered_ok": bool((full[:, 0] == torch.arange(total)).all()),
+                          "max_over_ranks": tmax}))
+    if ws > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    maybe_relaunch(args)
+    if args.dry_run:
+        dry_run(args)
+        return
     if args.impl == "reference":
         run_reference(args)
         return
@@ -370,14 +476,19 @@ def main():
                                       fired=torch.empty(B, dtype=torch.uint8, device=dev), err=err)
             for _ in range(PRED_LAYERS)]
 
+    prev_err = spx.prev_error(prev)
+    recheck = spx.recheck_buffer(B)
+
     def step():
         prev.copy_(prev0)                                  # token start: uniform prior
+        prev_err.zero_()                                   # ... which is exact
         for l in range(PRED_LAYERS):
             spx.evaluate_batch(model, bank, hidden[l], ids_l[l], prev, threshold=THRESHOLD, layer=l,
                                outputs=False, out=outs[l], pdl=PDL)
 
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
+        recheck = spx.recheck_buffer(B)                    # this stream's work list
         for _ in range(3):
             step()
         torch.cuda.synchronize()
@@ -396,6 +507,7 @@ def main():
         for _ in range(args.warmup):
             graph.replay()
     barrier()
+    rc0 = recheck[3:5].cpu().tolist()
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.3)
@@ -409,6 +521,9 @@ def main():
     clocks = clk.stop()
     barrier()
     ms = e0.elapsed_time(e1)
+    rc1 = recheck[3:5].cpu().tolist()
+    certified = {"rows_reevaluated_strict": rc1[0] - rc0[0], "unresolved": rc1[1] - rc0[1],
+                 "evals": PRED_LAYERS * B * args.steps}
     ms_max = shard.max_over_ranks(ms, dev)                # device time, max over ranks
     evals_per_step = PRED_LAYERS * B * ws
     value = evals_per_step * args.steps / (ms_max / 1000.0)
@@ -511,6 +626,7 @@ def main():
 
     # ---- CPU baseline (rank 0, N=1) ----------------------------------------
     cpu = None
+    parity = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         head_dv = model.lm_head.float().t().contiguous().cpu().numpy()
         from oracle import specexit_oracle as O
@@ -525,6 +641,9 @@ def main():
                          f"{args.cpu_seconds:.0f}s on {P} forked single-core processes; "
                          f"strict kernel: {kind}"}
         del head_dv
+        if not args.no_parity:
+            parity = parity_check(spx, model, bank, bank_w, hidden, ids_all, outs, stream, prev,
+                                  prev0, B)
 
     if rank == 0:
         line = {
@@ -555,6 +674,8 @@ def main():
             "clocks": clocks,
             "decode": decode,
             "fire_rate": fired,
+            "certified": certified,
+            "parity": parity,
             "batch1_us_per_eval": us_per_eval_b1,
             "lib": N.version(),
         }

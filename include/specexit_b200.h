@@ -96,8 +96,35 @@ typedef struct {
                              /*    are given: those flags are written late)    */
   int32_t *err;              /* device error word                              */
   int64_t B, d, V, K, H;
+  /* ---- FAST-mode decision certification.  When
+   * `recheck` is given, every FAST decision is either certified equal to the
+   * reference's (|z2 - z_cut| beyond the stated FAST-vs-strict error bound of
+   * that row) or the row is re-evaluated by the STRICT chain in a follow-up
+   * launch enqueued by this same call, so `fired` matches the reference's
+   * `prob > threshold` (predictor.py:106-109) row for row.               */
+  const float *head_wmax;    /* (V) max_j |head[v][j]| (spx_head_stats)        */
+  const float *cert;         /* (3K+2) spx_predictor_cert of this layer's MLP  */
+  float cert_kappa;          /* 2 * lambda * 2^-24 * sqrt(d)  (lambda = 8)      */
+  float cert_hnorm;          /* max|final_norm.g| * sqrt(d) + ||final_norm.b||  */
+  float *prev_err;           /* (B) in: bound on |prev - prev_ref|; out: bound */
+                             /*     for the new probabilities (0 after STRICT) */
+  int32_t *recheck;          /* (5 + B) zeroed once by the caller, self-reset: */
+                             /* [0] rows deferred, [1] CTA ticket, [2] pop     */
+                             /* cursor, [3] total rows re-evaluated            */
+                             /* (cumulative), [4] rows whose STRICT decision   */
+                             /* still sat inside the carried prev bound        */
+                             /* (cumulative), [5..] row list                   */
 } spx_predictor_args;
 int spx_predictor_eval(const spx_predictor_args *args, void *stream);
+
+/* Per-layer constants of the certification bound for one predictor:
+ * cert[i] = sum_j |w2[j]| |w1[i][j]| (i < 3K), cert[3K] = sum_j |w2[j] b1[j]|,
+ * cert[3K+1] = sum_j |w2[j]|. */
+int spx_predictor_cert(const float *w1, const float *b1, const float *w2, int64_t K, int64_t H,
+                       float *cert, void *stream);
+/* Per-vocabulary-row statistics of the LM head: wmax[v] = max_j |head[v][j]|. */
+int spx_head_stats(const void *head, int32_t head_dtype, int64_t V, int64_t d, float *wmax,
+                   void *stream);
 
 /* extract_features alone (src/specexit/predictor.py:42-52) for B rows:
  * feats_out (B, 3K) = [logits | softmax | softmax - prev]; prev is read only. */
@@ -276,6 +303,7 @@ typedef struct {
   int32_t *rec_token, *rec_exit_layer, *rec_evals, *rec_full_heads;
   uint8_t *rec_fired, *rec_verified;
   uint64_t *rec_active;
+  float *prev_err;                              /* (1) bound carried with prev */
 } spx_token_state;
 /* stable top-K (value desc, lower id on ties) of n logits
  * (speculation.py:57-60 topk_from_logits). K <= 64. */

@@ -10,8 +10,8 @@ from .model import (LN_EPS, ModelConfig, TransformerModel, final_norm, from_tens
                     sliced_head_logits, tensor_specs)
 from .predictor import (FeatureVector, PredictorBank, PredictorWeights, decide_exit,  # noqa: F401
                         evaluate_batch, extract_features, init_predictor, load_predictors,
-                        predictor_forward, predictor_param_count, save_predictors,
-                        uniform_probs, z_cut)
+                        predictor_forward, predictor_param_count, prev_error,
+                        recheck_buffer, recheck_stats, save_predictors, uniform_probs, z_cut)
 from .scheduler import (OfflineProfile, OnlineState, ScheduleConfig, active_layers,  # noqa: F401
                         load_profile, online_hot_layers, profile_offline, recompute_counts,
                         save_profile, update_online, weight_fingerprint)

@@ -39,7 +39,9 @@ class PredictorArgs(ctypes.Structure):
                 ("logits_out", _vp), ("feat_out", _vp), ("z_out", _vp), ("prob_out", _vp),
                 ("fired", _vp), ("row_layer_mask", _vp), ("row_done", _vp), ("evals", _vp),
                 ("layer", _i32), ("mode", _i32), ("pdl", _i32), ("err", _vp),
-                ("B", _i64), ("d", _i64), ("V", _i64), ("K", _i64), ("H", _i64)]
+                ("B", _i64), ("d", _i64), ("V", _i64), ("K", _i64), ("H", _i64),
+                ("head_wmax", _vp), ("cert", _vp), ("cert_kappa", _f32), ("cert_hnorm", _f32),
+                ("prev_err", _vp), ("recheck", _vp)]
 
 
 class VerifyArgs(ctypes.Structure):
@@ -78,7 +80,7 @@ class TokenStateC(ctypes.Structure):
                 ("full_heads", _vp), ("next_in", _vp), ("step", _vp), ("active", _vp),
                 ("rec_token", _vp), ("rec_exit_layer", _vp), ("rec_evals", _vp),
                 ("rec_full_heads", _vp), ("rec_fired", _vp), ("rec_verified", _vp),
-                ("rec_active", _vp)]
+                ("rec_active", _vp), ("prev_err", _vp)]
 
 
 _LIB = None
@@ -124,6 +126,8 @@ def lib():
     L.spx_token_end.argtypes = [TokenStateC, OnlineStateC, _i32, _i32, _i32, _i64, _vp]
     L.spx_or_flag.argtypes = [_vp, _vp, _vp]
     L.spx_force_next.argtypes = [_vp, _vp, _vp, _i64, _vp]
+    L.spx_predictor_cert.argtypes = [_vp, _vp, _vp, _i64, _i64, _vp, _vp]
+    L.spx_head_stats.argtypes = [_vp, _i32, _i64, _i64, _vp, _vp]
     L.spx_debug_trace.argtypes = [_vp]
     L.spx_debug_trace.restype = None
     _LIB = L

@@ -11,33 +11,73 @@
 
 namespace spx {
 
-// Stable top-K (value desc, index asc) of n logits; one CTA.
-__global__ void topk_kernel(const float *logits, int n, int K, int32_t *ids_out) {
-  extern __shared__ unsigned long long keys[];      // blockDim.x * K
-  const int tid = threadIdx.x;
-  unsigned long long best[64];
-  for (int q = 0; q < 64; ++q) best[q] = 0ull;
-  for (int i = tid; i < n; i += blockDim.x) {
-    unsigned long long k = argmax_key(logits[i], (uint32_t)i);
-    // insert into the descending list
-    for (int q = 0; q < K; ++q) {
-      if (k > best[q]) { const unsigned long long t = best[q]; best[q] = k; k = t; }
-    }
+// Stable top-K (value desc, index asc) of n logits (speculation.py:57-60
+// topk_from_logits: np.argsort(-x, kind="stable")[:K]).  One CTA of 1024
+// threads: each thread keeps the best TK keys of its strided share in
+// registers (fully unrolled insertion, no local memory); K rounds of a block
+// argmax pop the winner from its owner's list.  An owner whose list runs dry
+// rescans its share for the best keys below the last one it gave up (keys are
+// unique, so "below" is exact).  Keys: order-preserving value bits << 32 |
+// ~index, i.e. ties go to the lower index (np.argmax / stable argsort).
+constexpr int TOPK_THREADS = 1024;
+constexpr int TK = 4;
+
+__device__ __forceinline__ void topk_insert(unsigned long long (&l)[TK], unsigned long long k) {
+#pragma unroll
+  for (int q = 0; q < TK; ++q) {
+    const bool sw = k > l[q];
+    const unsigned long long t = l[q];
+    l[q] = sw ? k : t;
+    k = sw ? t : k;
   }
-  for (int q = 0; q < K; ++q) keys[(size_t)tid * K + q] = best[q];
-  __syncthreads();
-  // tree merge of sorted lists
-  for (int stride = 1; stride < (int)blockDim.x; stride <<= 1) {
-    if ((tid % (2 * stride)) == 0 && tid + stride < (int)blockDim.x) {
-      unsigned long long *a = keys + (size_t)tid * K, *b = keys + (size_t)(tid + stride) * K;
-      unsigned long long m[64];
-      int i = 0, j = 0;
-      for (int q = 0; q < K; ++q) m[q] = (a[i] >= b[j]) ? a[i++] : b[j++];
-      for (int q = 0; q < K; ++q) a[q] = m[q];
+}
+
+__global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(const float *logits, int n, int K,
+                                                           int32_t *ids_out) {
+  __shared__ unsigned long long s_red[TOPK_THREADS / 32];
+  __shared__ unsigned long long s_win;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  unsigned long long l[TK];
+  auto scan = [&](unsigned long long below) {
+#pragma unroll
+    for (int q = 0; q < TK; ++q) l[q] = 0ull;
+    for (int i = tid; i < n; i += TOPK_THREADS) {
+      const unsigned long long k = argmax_key(logits[i], (uint32_t)i);
+      if (k < below) topk_insert(l, k);
+    }
+  };
+  scan(~0ull);
+  int taken = 0;
+  for (int r = 0; r < K; ++r) {
+    unsigned long long m = l[0];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+      m = v > m ? v : m;
+    }
+    if (lane == 0) s_red[wid] = m;
+    __syncthreads();
+    if (wid == 0) {
+      m = s_red[lane];
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+        m = v > m ? v : m;
+      }
+      if (lane == 0) {
+        s_win = m;
+        ids_out[r] = (int32_t)(0xffffffffu - (uint32_t)(m & 0xffffffffull));
+      }
     }
     __syncthreads();
+    const unsigned long long win = s_win;
+    if (l[0] == win && win != 0ull) {              // the owner pops its head
+#pragma unroll
+      for (int q = 0; q + 1 < TK; ++q) l[q] = l[q + 1];
+      l[TK - 1] = 0ull;
+      if (++taken % TK == 0) scan(win);            // list dry: next keys below
+    }
   }
-  if (tid < K) ids_out[tid] = (int32_t)(0xffffffffu - (uint32_t)(keys[tid] & 0xffffffffull));
 }
 
 // Per-token reset (engine.py:183-191): prev = uniform(K) as f32, flags clear.
@@ -45,6 +85,7 @@ __global__ void token_begin_kernel(spx_token_state st, int K, int L, float inv_k
   const int t = threadIdx.x;
   if (t < K) st.prev[t] = inv_k;                       // np.float32(1.0 / k), host-rounded
   if (t == 0) {
+    if (st.prev_err) *st.prev_err = 0.f;                // the uniform prior is exact
     *st.done = 0; *st.fired = 0; *st.fired_any = 0;
     *st.exit_layer = L - 1; *st.evals = 0; *st.full_heads = 0;
   }
@@ -108,9 +149,7 @@ using namespace spx;
 extern "C" int spx_topk(const float *logits, int64_t n, int32_t K, int32_t *ids_out,
                         void *stream) {
   if (!logits || !ids_out || n <= 0 || K < 1 || K > 64 || K > n) return SPX_EINVAL;
-  const int threads = 256;
-  topk_kernel<<<1, threads, (size_t)threads * K * 8, (cudaStream_t)stream>>>(logits, (int)n, K,
-                                                                              ids_out);
+  topk_kernel<<<1, TOPK_THREADS, 0, (cudaStream_t)stream>>>(logits, (int)n, K, ids_out);
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
 }
 

@@ -28,8 +28,15 @@
 // The early-exit flag `done` is read before griddepcontrol.wait (an exit
 // decided by an earlier kernel) and after it (decided by the kernel just
 // before): an exited stream streams nothing or drains its prefetch and
-// returns.  launch_dependents fires only after the last grid barrier, so a
-// dependent kernel can never occupy an SM this grid still needs.
+// returns.  launch_dependents fires after grid barrier 1, i.e. once every CTA
+// of this grid is resident and running, so a dependent kernel can never take
+// an SM this grid still needs.
+// Co-residency of the whole grid (one CTA per SM, spun on by the grid
+// barriers) is guaranteed by the launch: the occupancy API must report one
+// CTA per SM for every SM, and the kernel is launched with the cooperative
+// attribute, so the driver rejects a grid that cannot be co-resident (MPS SM
+// limits, green contexts) instead of letting it spin; the caller then takes
+// the per-matrix kernel chain.
 #pragma once
 
 constexpr int MG_CW = 16;                       // consumer warps
@@ -565,7 +572,7 @@ static bool mega_layer_supported(const LayerParams &p, int sms) {
   return sms > 0 && mega_smem(p, sms) <= 220 * 1024;
 }
 
-static void launch_layer_mega(const LayerParams &p, int sms, cudaStream_t s) {
+static bool launch_layer_mega(const LayerParams &p, int sms, cudaStream_t s) {
   MegaGeom g;
   const int no[4] = {3 * p.d, p.d, p.ffn, p.d}, ki[4] = {p.d, p.d, p.d, p.ffn};
   for (int m = 0; m < 4; ++m) {
@@ -586,19 +593,39 @@ static void launch_layer_mega(const LayerParams &p, int sms, cudaStream_t s) {
   g.dbg = env_dbg;
   g.smem = mega_smem(p, sms);
   const int cd = (p.d / 8 + MG_CT - 1) / MG_CT, cf = (p.ffn / 8 + MG_CT - 1) / MG_CT;
-  auto go = [&](auto kern) {
+  static const int env_coop = getenv("SPX_MEGA_COOP") ? atoi(getenv("SPX_MEGA_COOP")) : 1;
+  auto go = [&](auto kern) -> bool {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)g.smem);
-    if (e != cudaSuccess) fprintf(stderr, "spx mega: set smem %zu: %s\n", g.smem, cudaGetErrorString(e));
-    launch_pdl(kern, sms, MG_T, g.smem, s, p, g);
-    e = cudaPeekAtLastError();
-    if (e != cudaSuccess) fprintf(stderr, "spx mega: launch: %s\n", cudaGetErrorString(e));
+    if (e != cudaSuccess) { cudaGetLastError(); return false; }
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, MG_T, g.smem);
+    if (e != cudaSuccess || per_sm < 1) { cudaGetLastError(); return false; }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sms);
+    cfg.blockDim = dim3(MG_T);
+    cfg.dynamicSmemBytes = g.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = env_coop ? 2 : 1;
+    e = cudaLaunchKernelEx(&cfg, kern, p, g);
+    if (e != cudaSuccess) {
+      fprintf(stderr, "spx mega: launch: %s\n", cudaGetErrorString(e));
+      cudaGetLastError();
+      return false;
+    }
+    return true;
   };
-  if (cd == 1 && cf == 1) go(layer_mega_kernel<1, 1>);
-  else if (cd == 1 && cf == 2) go(layer_mega_kernel<1, 2>);
-  else if (cd == 1 && cf == 3) go(layer_mega_kernel<1, 3>);
-  else if (cd == 2 && cf == 2) go(layer_mega_kernel<2, 2>);
-  else go(layer_mega_kernel<2, 3>);
+  if (cd == 1 && cf == 1) return go(layer_mega_kernel<1, 1>);
+  if (cd == 1 && cf == 2) return go(layer_mega_kernel<1, 2>);
+  if (cd == 1 && cf == 3) return go(layer_mega_kernel<1, 3>);
+  if (cd == 2 && cf == 2) return go(layer_mega_kernel<2, 2>);
+  return go(layer_mega_kernel<2, 3>);
 }
 
 extern "C" void spx_debug_mega_trace(void *host_out) {

@@ -536,10 +536,8 @@ static void launch_layer_fast(const LayerParams &p, int sms, cudaStream_t s) {
   // SPX_LAYER_MEGA=0 selects the per-matrix kernel chain (sweeps / A-B runs)
   static const int env_mega = getenv("SPX_LAYER_MEGA") ? atoi(getenv("SPX_LAYER_MEGA")) : 1;
   if (std::is_same<TW, __nv_bfloat16>::value && env_mega && p.rows_hint <= MG_NRP &&
-      mega_layer_supported(p, sms)) {
-    launch_layer_mega(p, sms, s);
+      mega_layer_supported(p, sms) && launch_layer_mega(p, sms, s))
     return;
-  }
   static const int env_tc = getenv("SPX_LAYER_TC") ? atoi(getenv("SPX_LAYER_TC")) : 1;
   if (std::is_same<TW, __nv_bfloat16>::value && env_tc && tc_layer_supported(p)) {
     launch_tc<EPI_QKV>(p, 3 * p.d, p.d, sms, s);

@@ -54,10 +54,10 @@ inline SmemPlan plan_smem_ring(int d, int K, int H, int max_bytes, int force_w1,
   const size_t gb = g_smem ? (size_t)d * 4 : 0;
   const size_t unit = ((size_t)HALF * d * sizeof(TW) + 127) / 128 * 128;
   const size_t team = ((size_t)(RED_FLOATS + 4 + MAXK) * 4 + 127) / 128 * 128;
-  const size_t tail = ((size_t)(3 * MAXK + (H > 0 ? H : 4) + 64) * 4 + 127) / 128 * 128;
+  const size_t tail = ((size_t)(6 * MAXK + (H > 0 ? H : 4) + 64) * 4 + 127) / 128 * 128;
   const size_t qbytes = (sizeof(QSlot) * QS + 127) / 128 * 128;
   const size_t w1b = ((size_t)3 * K * H * 4 + 127) / 128 * 128;
-  const size_t bars = (NTEAM * MAX_RING + 2 * QS + 1) * 8;
+  const size_t bars = (NTEAM * MAX_RING + 2 * QS + 2) * 8;    // + the deferred-row count
   const size_t base = (gb + (size_t)2 * H * 4 + 127) / 128 * 128 + NTEAM * team +
                       (size_t)NTEAM * ring * unit + NTAIL * tail + qbytes + bars + 128;
   const bool w1 = H > 0 && force_w1 != 0 && base + w1b <= (size_t)max_bytes;
@@ -125,7 +125,9 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
   const int rows_cta =
       p.B > (int)blockIdx.x ? (p.B - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
 
+  int &s_defer = *reinterpret_cast<int *>(setup_bar + 1);   // rows deferred (recheck)
   if (threadIdx.x == 0) {
+    s_defer = 0;
     for (int s = 0; s < NTEAM * RING; ++s) mbar_init(ringbar + s, 1);
     for (int s = 0; s < QS; ++s) { mbar_init(qfull + s, 1); mbar_init(qempty + s, 1); }
     mbar_init(setup_bar, 1);
@@ -176,7 +178,7 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
       const int slot = k % QS;
       mbar_wait(qfull + slot, (k / QS) & 1);
       const QSlot &q = queue[slot];
-      const int row = q.row, flags = q.flags;
+      const int row = q.row, flags = q.flags, q_lnf = q.pad0;
       if (p.trace && lane == 0 && !(flags & 1)) {
         p.trace[(size_t)row * 16 + 0] = gtimer();
         p.trace[(size_t)row * 16 + 8] = clock64();
@@ -207,7 +209,13 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
 #pragma unroll
         for (int c = 0; c < KC; ++c) e[c] = np_expf(__fsub_rn(x[c], m));
 #pragma unroll
-        for (int c = 0; c < KC; ++c) { esum = __fadd_rn(esum, e[c]); psum = __fadd_rn(psum, pv[c]); }
+        for (int c = 0; c < KC; ++c) esum = __fadd_rn(esum, e[c]);
+        {
+          float pv8[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) pv8[c] = c < KC ? pv[c] : 0.f;
+          psum = np_sum_upto8(pv8, KC);                     // numpy pairwise (predictor.py:49)
+        }
         if (p.logits_out && lane < KC) {
 #pragma unroll
           for (int c = 0; c < KC; ++c) if (lane == c) p.logits_out[(size_t)row * KC + c] = x[c];
@@ -229,7 +237,6 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
             feats[c] = x[c];
             feats[KC + c] = pr;
             feats[2 * KC + c] = __fsub_rn(pr, pv[c]);
-            p.prev[(size_t)row * KC + c] = pr;                 // engine.py:196
           }
         }
       } else {
@@ -264,11 +271,11 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
             if (hh) e1 = ev; else e0 = ev;
           }
         }
-        float esum = 0.f, psum = 0.f;                             // strict left-to-right
-        for (int c = 0; c < K; ++c) {
+        float esum = 0.f;                                         // strict left-to-right
+        for (int c = 0; c < K; ++c)
           esum = __fadd_rn(esum, __shfl_sync(0xffffffffu, c < 32 ? e0 : e1, c & 31));
-          psum = __fadd_rn(psum, __shfl_sync(0xffffffffu, c < 32 ? pv0 : pv1, c & 31));
-        }
+        const float psum = np_pairwise_block(                     // numpy pairwise (predictor.py:49)
+            0, K, [&](int c) { return __shfl_sync(0xffffffffu, c < 32 ? pv0 : pv1, c & 31); });
         if (p.logits_out) {
           if (v0) p.logits_out[(size_t)row * K + lane] = x0;
           if (v1) p.logits_out[(size_t)row * K + lane + 32] = x1;
@@ -288,23 +295,18 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
           feats[lane] = x0;
           feats[K + lane] = pr;
           feats[2 * K + lane] = __fsub_rn(pr, pv0);
-          p.prev[(size_t)row * K + lane] = pr;                   // engine.py:196
         }
         if (v1) {
           const float pr = __fdiv_rn(e1, esum);
           feats[lane + 32] = x1;
           feats[K + lane + 32] = pr;
           feats[2 * K + lane + 32] = __fsub_rn(pr, pv1);
-          p.prev[(size_t)row * K + lane + 32] = pr;
         }
       }
       __syncwarp();
-      if (p.feat_out)
-        for (int i = lane; i < 3 * K; i += 32) p.feat_out[(size_t)row * 3 * K + i] = feats[i];
-      if (lane == 0 && p.evals) p.evals[row] += 1;
       if (p.trace && lane == 0) p.trace[(size_t)row * 16 + 10] = clock64();
+      float z2 = 0.f;
       if (mlp) {
-        float z2;
         if (p.trace) {
           mlp_z1<4, !W1S>(feats, W1S ? w1s : p.w1, b1s, 3 * K, H, hs, lane, 0);
           __syncwarp();
@@ -317,6 +319,23 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
           z2 = W1S ? warp_mlp(feats, w1s, b1s, w2s, p.b2, K, H, hs, lane)
                    : warp_mlp_g(feats, p.w1, b1s, w2s, p.b2, K, H, hs, lane);
         }
+      }
+      float perr = 0.f;
+      if (p.recheck &&
+          !certify_row(p, row, feats, hs + (H > 0 ? H : 4), hs, W1S ? w1s : p.w1, b1s, w2s, z2,
+                       __int_as_float(q_lnf), K, H, mlp, lane, perr, [&](int c) {
+                         return __ldg(p.head_wmax + p.ids[(size_t)row * K + c]);
+                       })) {
+        if (lane == 0) defer_row(p, row, &s_defer);  // STRICT re-evaluation decides
+        __syncwarp();
+        continue;
+      }
+      for (int c = lane; c < K; c += 32) p.prev[(size_t)row * K + c] = feats[K + c];  // engine.py:196
+      if (lane == 0 && p.prev_err) p.prev_err[row] = perr;
+      if (p.feat_out)
+        for (int i = lane; i < 3 * K; i += 32) p.feat_out[(size_t)row * 3 * K + i] = feats[i];
+      if (lane == 0 && p.evals) p.evals[row] += 1;
+      if (mlp) {
         if (lane == 0) {
           if (p.z_out) p.z_out[row] = z2;
           // the decision is exact (z2 >= z_cut); the reported probability is
@@ -334,8 +353,7 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
         p.trace[(size_t)row * 16 + 9] = clock64();
       }
     }
-    return;
-  }
+  } else {
 
   // =========================== DOT TEAMS ===========================
   const int team = warp / TEAM, w = warp % TEAM;
@@ -432,12 +450,12 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
     }
   };
   // hand a row to its tail warp (warp 0 of the team)
-  auto handoff = [&](int kk, int row, int flags, float cpv0, float cpv1) {
+  auto handoff = [&](int kk, int row, int flags, float cpv0, float cpv1, float lnf) {
     const int slot = kk % QS;
     if (lane == 0) mbar_wait(qempty + slot, ((kk / QS) & 1) ^ 1);
     __syncwarp();
     QSlot &q = queue[slot];
-    if (lane == 0) { q.row = row; q.flags = flags; }
+    if (lane == 0) { q.row = row; q.flags = flags; q.pad0 = __float_as_int(lnf); }
     if (lane < K) { q.logits[lane] = logit[lane]; q.prev[lane] = cpv0; }
     if (lane + 32 < K) { q.logits[lane + 32] = logit[lane + 32]; q.prev[lane + 32] = cpv1; }
     __syncwarp();
@@ -463,7 +481,7 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
   while (k < rows_cta) {
     const int row = row_of(k);
     if (cskip) {
-      if (w == 0) handoff(k, row, 1, 0.f, 0.f);
+      if (w == 0) handoff(k, row, 1, 0.f, 0.f, 0.f);
     } else {
       if (p.trace && leader) p.trace[(size_t)row * 16 + 1] = gtimer();
       // ---- pass 1: mean (this warp = canonical group w), from registers
@@ -493,7 +511,7 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
         team_sync(team);
       }
       if (p.trace && leader) p.trace[(size_t)row * 16 + 2] = gtimer();
-      float r = 0.f;
+      float r = 0.f, lnf = 0.f;
       const float2 nmean = make_float2(-mean, -mean);
       for (int h = 0; h < nhalf; ++h) {
         const int slot = n_wait % RING;
@@ -544,6 +562,7 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
                                                     red[(HALF + 1) * 4 + 2], red[(HALF + 1) * 4 + 3]),
                                       (float)d);
           r = __frcp_rn(__fsqrt_rn(__fadd_rn(var, 1e-5f)));
+          lnf = sqrtf(1.f + mean * mean / var);
         }
         if (w == 0) {
           const float bwa = __shfl_sync(0xffffffffu, bw0, (c0 + lane) & 31);
@@ -559,7 +578,7 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
       if (p.trace && leader) p.trace[(size_t)row * 16 + 3] = gtimer();
       if (w == 0) {
         __syncwarp();
-        handoff(k, row, (cbad ? 2 : 0) | (hbad ? 4 : 0), pv0, pv1);
+        handoff(k, row, (cbad ? 2 : 0) | (hbad ? 4 : 0), pv0, pv1, lnf);
       }
     }
     // ---- advance: next row becomes current; load its data; fetch the ids of
@@ -576,6 +595,9 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
       pump();
     }
   }
+  }  // dot teams
+  recheck_epilogue<TW>(p, smem, &s_defer, rows_cta,
+                       [&](int kk) { return (int)blockIdx.x + kk * (int)gridDim.x; });
 }
 
 template <typename TW>

@@ -12,10 +12,10 @@
 //     copy issue never waits on a dependent load.  With pdl == 2 ("ids
 //     ready") the LM-head copies of the first S rows are issued before
 //     griddepcontrol.wait.
-//   * 16 COMPUTE warps, all on the same slot: warp (k, g) owns canonical
-//     partial group g of LM-head row k (k < 4; rows k and k+4 when K > 4).
-//     Group-0..3 warps of k = 0 also form the mean / variance partials.  Two
-//     named barriers per row; the slot is released right after the second.
+//   * 4 COMPUTE warps, all on the same slot: warp g owns canonical partial
+//     group g of every LM-head row of the slot and of the mean / variance
+//     passes.  Two named barriers per row; the slot is released right after
+//     the second.
 //   * 4 TAIL warps: softmax over the K ids + features, MLP (W1/b1/w2 in
 //     shared memory), f32 sigmoid for the reported prob, exact decision
 //     z2 >= z_cut.  Each tail warp prefetches its next row's prev / bias-fold
@@ -87,7 +87,7 @@ inline StreamPlan plan_stream(int d, int K, int H, int max_bytes, bool ldgx = fa
   return s;                                             // bytes == 0: does not fit
 }
 
-__device__ __forceinline__ void cbar_sync() {          // the 16 compute warps
+__device__ __forceinline__ void cbar_sync() {          // the 4 compute warps
   asm volatile("bar.sync 1, %0;" ::"r"(32 * SW_COMPUTE) : "memory");
 }
 
@@ -115,7 +115,9 @@ predictor_stream_kernel(PredParams p, StreamPlan sp) {
       p.B > (int)blockIdx.x ? (p.B - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
   auto row_of = [&](int i) { return (int)blockIdx.x + i * (int)gridDim.x; };
 
+  int &s_defer = reinterpret_cast<int *>(smem + sp.off_hdr)[31];   // rows deferred (recheck)
   if (threadIdx.x == 0) {
+    s_defer = 0;
     for (int s = 0; s < S; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
     for (int s = 0; s < SQS; ++s) { mbar_init(qfull + s, 1); mbar_init(qempty + s, 1); }
     mbar_init(setup_bar, 1);
@@ -203,8 +205,7 @@ predictor_stream_kernel(PredParams p, StreamPlan sp) {
       j = __shfl_sync(0xffffffffu, j, 0);
     }
     if (!waited) pdl_wait_trigger();
-    return;
-  }
+  } else {
 
   if (early) pdl_wait_trigger();             // compute + tail warps: after the prefetch
   mbar_wait(setup_bar, 0);
@@ -227,15 +228,17 @@ predictor_stream_kernel(PredParams p, StreamPlan sp) {
       }
       const int myj = j++;
       if ((myj % SW_TAIL) != tw) continue;
-      float pv[SKMAX], bw[SKMAX];
+      float pv[SKMAX], bw[SKMAX], wmx[SKMAX];
 #pragma unroll
       for (int c = 0; c < SKMAX; ++c) {
-        pv[c] = 0.f; bw[c] = 0.f;
+        pv[c] = 0.f; bw[c] = 0.f; wmx[c] = 0.f;
         if (c < K) {
           pv[c] = p.prev[(size_t)row * K + c];
-          if (p.head_bw) {
+          if (p.head_bw || p.recheck) {
             const int id = p.ids[(size_t)row * K + c];
-            bw[c] = (id >= 0 && id < p.V) ? __ldg(p.head_bw + id) : 0.f;
+            const bool ok = id >= 0 && id < p.V;
+            if (p.head_bw && ok) bw[c] = __ldg(p.head_bw + id);
+            if (p.recheck && ok) wmx[c] = __ldg(p.head_wmax + id);
           }
         }
       }
@@ -243,6 +246,7 @@ predictor_stream_kernel(PredParams p, StreamPlan sp) {
       mbar_wait(qfull + qs, (myj / SQS) & 1);
       if (p.trace && lane == 0) p.trace[(size_t)row * 16 + 0] = gtimer();
       const int flags = queue[qs].flags;
+      const int lnf_bits = queue[qs].pad0;        // sqrt(1 + mean^2/var) of the row
       float x[SKMAX];
 #pragma unroll
       for (int c = 0; c < SKMAX; ++c) x[c] = c < K ? __fadd_rn(queue[qs].logit[c], bw[c]) : 0.f;
@@ -266,7 +270,8 @@ predictor_stream_kernel(PredParams p, StreamPlan sp) {
       for (int c = 0; c < SKMAX; ++c) e[c] = c < K ? np_expf(__fsub_rn(x[c], m)) : 0.f;
 #pragma unroll
       for (int c = 0; c < SKMAX; ++c)
-        if (c < K) { esum = __fadd_rn(esum, e[c]); psum = __fadd_rn(psum, pv[c]); }
+        if (c < K) esum = __fadd_rn(esum, e[c]);
+      psum = np_sum_upto8(pv, K);                        // numpy pairwise (predictor.py:49)
       if (p.logits_out && lane < K) {
 #pragma unroll
         for (int c = 0; c < SKMAX; ++c) if (lane == c) p.logits_out[(size_t)row * K + c] = x[c];
@@ -290,18 +295,37 @@ predictor_stream_kernel(PredParams p, StreamPlan sp) {
           feats[c] = x[c];
           feats[K + c] = pr[c];
           feats[2 * K + c] = __fsub_rn(pr[c], pv[c]);
-          p.prev[(size_t)row * K + c] = pr[c];          // engine.py:196
         }
       }
       __syncwarp();
+      float z2 = 0.f;
+      if (mlp) {
+        mlp_z1<4, !W1S>(feats, w1, b1s, 3 * K, H, hs, lane, 0);
+        __syncwarp();
+        z2 = z2_tree(z2_partial(hs, w2s, H, lane), z2_partial(hs, w2s, H, lane + 32), hs, w2s, H,
+                     p.b2, lane);
+      }
+      float perr = 0.f;
+      if (p.recheck &&
+          !certify_row(p, row, feats, hs + H, hs, w1, b1s, w2s, z2, __int_as_float(lnf_bits), K,
+                       H, mlp, lane, perr, [&](int c) {
+                         float v = 0.f;
+#pragma unroll
+                         for (int cc = 0; cc < SKMAX; ++cc) v = cc == c ? wmx[cc] : v;
+                         return v;
+                       })) {
+        if (lane == 0) defer_row(p, row, &s_defer);  // STRICT re-evaluation decides
+        __syncwarp();
+        continue;
+      }
+#pragma unroll
+      for (int c = 0; c < SKMAX; ++c)
+        if (c < K && lane == c) p.prev[(size_t)row * K + c] = pr[c];   // engine.py:196
+      if (lane == 0 && p.prev_err) p.prev_err[row] = perr;
       if (p.feat_out)
         for (int q = lane; q < 3 * K; q += 32) p.feat_out[(size_t)row * 3 * K + q] = feats[q];
       if (lane == 0 && p.evals) p.evals[row] += 1;
       if (mlp) {
-        mlp_z1<4, !W1S>(feats, w1, b1s, 3 * K, H, hs, lane, 0);
-        __syncwarp();
-        const float z2 = z2_tree(z2_partial(hs, w2s, H, lane), z2_partial(hs, w2s, H, lane + 32),
-                                 hs, w2s, H, p.b2, lane);
         if (lane == 0) {
           if (p.z_out) p.z_out[row] = z2;
           if (p.prob_out) p.prob_out[row] = (double)sigmoid32(z2);
@@ -315,8 +339,7 @@ predictor_stream_kernel(PredParams p, StreamPlan sp) {
       if (p.trace && lane == 0) p.trace[(size_t)row * 16 + 4] = gtimer();
       __syncwarp();
     }
-    return;
-  }
+  } else {
 
   // ============================== COMPUTE WARPS ==============================
   // warp g = canonical partial group g, for every LM-head row of the slot;
@@ -438,12 +461,16 @@ predictor_stream_kernel(PredParams p, StreamPlan sp) {
       if (lane == 0) {
         queue[qs].row = row;
         queue[qs].flags = flags0 | (hflag ? 4 : 0);
+        queue[qs].pad0 = __float_as_int(sqrtf(1.f + mean * mean / var));
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(qfull + qs);
     }
     ++j;
   }
+  }  // compute warps
+  }  // compute + tail warps
+  recheck_epilogue<TW>(p, smem, &s_defer, rows_cta, row_of);   // deferred rows: STRICT
 }
 
 template <typename TW>

@@ -1,0 +1,14 @@
+// Translation unit of the TEAM fused predictor kernel family (any K <= 64,
+// any d): bf16 head, 2048 < d <= 4096; dispatched by spx_predictor.cu.
+#include "spx_pred_common.cuh"
+namespace spx {
+#include "spx_pred_fast.cuh"
+
+template <typename TW, int CPL>
+int launch_team_cpl(const PredParams &p, const SmemPlan &sp, int grid, cudaStream_t stream,
+                    int smem_optin) {
+  FastLaunch<TW>{p, sp, grid, stream, smem_optin}.template operator()<CPL>();
+  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+}
+template int launch_team_cpl<__nv_bfloat16, 8>(const PredParams &, const SmemPlan &, int, cudaStream_t, int);
+}  // namespace spx

@@ -1,347 +1,29 @@
-#include <type_traits>
-// K1+K2+K3: fused speculative early-exit predictor evaluation (sm_100a).
-//
-// One launch evaluates one decoder layer's exit predictor for B rows
-// (independent requests, or tree nodes).  Per row:
-//   final LayerNorm of the hidden row        reference model.py:140-146, :312
-//   gather of the K speculative LM-head rows reference model.py:313 (our head
-//     is stored (V, d) so the gather is K contiguous rows, fetched by TMA)
-//   K local logits                          reference model.py:314
-//   softmax over the K ids + delta vs prev  reference predictor.py:42-52,
-//                                           model.py:149-152
-//   2-layer MLP + bias, ReLU                reference predictor.py:97-103
-//   f64 sigmoid + strict threshold          reference predictor.py:87-94,
-//                                           :106-109
-// and writes prob / fired / the updated local probs (the next layer's
-// "prev", engine.py:196) to device memory.  Rows whose engine state says
-// "already exited" or "layer not scheduled" are skipped at entry: that is how
-// the device exit flag gates later launches without a host sync.
-//
-// FAST kernel (production): persistent, one CTA per SM, one WARP per row.
-// Each warp owns a shared-memory stage (hidden row + G LM-head rows) filled by
-// 1-D TMA bulk copies (cp.async.bulk, mbarrier completion); the next row's
-// copies are issued as soon as the current row's dot products are done, so
-// HBM traffic overlaps the softmax/MLP tail.  The predictor weights (W1, b1,
-// w2) and the final-norm params are staged in shared memory once per CTA.
-// Every reduction is the canonical CDOT order (spx_common.cuh).
-//
-// MLP arithmetic reproduces the reference's numpy/OpenBLAS (SkylakeX
-// kernels) order exactly: z1 = ascending FMA chain from 0 (3K <= 48) or
-// 8/4/2/1-column blocks each chained from 0 and added (3K >= 51), then + b1;
-// z2 = the AVX-512 sdot tree.  The decision is z2 >= z_cut with z_cut the
-// smallest f32 whose f64 sigmoid exceeds the threshold, i.e. exactly the
-// reference's `prob > threshold`.
-#include "spx_common.cuh"
-#include "../../include/specexit_b200.h"
-#include <cstdlib>
+#include "spx_pred_common.cuh"
+namespace spx {
+#include "spx_pred_fast.cuh"
+#include "spx_pred_stream.cuh"
+}  // namespace spx
 
 namespace spx {
 
-constexpr int MAXK = 64;
-constexpr int MAXH = 1024;
-constexpr int GROUP = 4;              // LM-head rows per TMA stage
-
-struct PredParams {
-  const float *hidden; int64_t hidden_stride;
-  const float *norm_g, *norm_b;
-  const void *head;            // (V, d) bf16 or f32
-  const float *head_bw;        // (V) CDOT(final_norm.b, head_v) (FAST path), may be null
-  const int32_t *ids;          // (B, K)
-  float *prev;                 // (B, K) in: previous local probs; out: new
-  const float *w1, *b1, *w2;   // (3K, H), (H), (H)
-  float b2, z_cut;
-  int policy;                  // 0 = MLP, 1 = constant probability
-  double const_prob, threshold;
-  float *logits_out;           // (B, K) optional
-  float *feat_out;             // (B, 3K) optional
-  float *z_out;                // (B) optional
-  double *prob_out;            // (B) optional
-  uint8_t *fired;              // (B) optional
-  const uint64_t *row_layer_mask;  // (B) optional: bit `layer` must be set
-  const uint8_t *row_done;         // (B) optional: nonzero -> skip row
-  int32_t *evals;                  // (B) optional: += 1 per evaluated row
-  int layer;
-  int *err;
-  unsigned long long *trace;       // debug: per-row globaltimer stamps (8 per row)
-  int pdl;                         // launched with programmatic stream serialization
-  int B, d, V, K, H;
-};
-
-__device__ __forceinline__ bool row_skipped(const PredParams &p, int row) {
-  if (p.row_done && p.row_done[row]) return true;
-  if (p.row_layer_mask && !((p.row_layer_mask[row] >> p.layer) & 1ull)) return true;
-  return false;
+// FAST kernel families, one translation unit each (spx_pred_stream.cu,
+// spx_pred_team.cu)
+int launch_stream_bf16(const PredParams &p, const StreamPlan &sp, int grid, cudaStream_t stream,
+                       int smem_optin, bool ldgx);
+template <typename TW, int CPL>
+int launch_team_cpl(const PredParams &p, const SmemPlan &sp, int grid, cudaStream_t stream,
+                    int smem_optin);
+template <typename TW>
+int launch_team(const PredParams &p, const SmemPlan &sp, int grid, cudaStream_t stream,
+                int smem_optin) {
+  const int nchunk = p.d / CHUNK;
+  if (nchunk <= NPART * 1) return launch_team_cpl<TW, 1>(p, sp, grid, stream, smem_optin);
+  if (nchunk <= NPART * 2) return launch_team_cpl<TW, 2>(p, sp, grid, stream, smem_optin);
+  if (nchunk <= NPART * 4) return launch_team_cpl<TW, 4>(p, sp, grid, stream, smem_optin);
+  if (nchunk <= NPART * 8) return launch_team_cpl<TW, 8>(p, sp, grid, stream, smem_optin);
+  if (nchunk <= NPART * 16) return launch_team_cpl<TW, 16>(p, sp, grid, stream, smem_optin);
+  return SPX_EINVAL;
 }
-
-// ---------------------------------------------------------------- warp tail
-// Softmax over the K logits in feats[0..K) (model.py:149-152), features
-// (predictor.py:51-52) into feats[K..3K), validation (predictor.py:45-50).
-// Whole warp; returns false (and flags err) on invalid input.
-__device__ bool warp_softmax_features(const PredParams &p, int row, float *feats, int lane) {
-  const int K = p.K;
-  const bool v0 = lane < K, v1 = lane + 32 < K;
-  const float x0 = v0 ? feats[lane] : 0.f, x1 = v1 ? feats[lane + 32] : 0.f;
-  const float pv0 = v0 ? p.prev[(size_t)row * K + lane] : 0.f;
-  const float pv1 = v1 ? p.prev[(size_t)row * K + lane + 32] : 0.f;
-  bool bad = (v0 && !is_finite(x0)) || (v1 && !is_finite(x1));
-  bad = __any_sync(0xffffffffu, bad);
-  float m = v0 ? x0 : -INFINITY;
-  if (v1) m = fmaxf(m, x1);
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, s));
-  const float e0 = v0 ? np_expf(__fsub_rn(x0, m)) : 0.f;
-  const float e1 = v1 ? np_expf(__fsub_rn(x1, m)) : 0.f;
-  // strict left-to-right sums (seq_sum) over c = 0..K-1, replicated per lane
-  float esum = 0.f, psum = 0.f;
-  for (int c = 0; c < K; ++c) {
-    const float ec = __shfl_sync(0xffffffffu, c < 32 ? e0 : e1, c & 31);
-    const float pc = __shfl_sync(0xffffffffu, c < 32 ? pv0 : pv1, c & 31);
-    esum = __fadd_rn(esum, ec);
-    psum = __fadd_rn(psum, pc);
-  }
-  int e = 0;
-  if (bad) e |= ERR_LOGIT_NONFINITE;
-  if (fabs((double)psum - 1.0) > 1e-5) e |= ERR_PREV_SUM;
-  if (e) {
-    if (lane == 0) atomicOr(p.err, e);
-    return false;
-  }
-  if (v0) {
-    const float pr = __fdiv_rn(e0, esum);
-    feats[K + lane] = pr;
-    feats[2 * K + lane] = __fsub_rn(pr, pv0);
-  }
-  if (v1) {
-    const float pr = __fdiv_rn(e1, esum);
-    feats[K + lane + 32] = pr;
-    feats[2 * K + lane + 32] = __fsub_rn(pr, pv1);
-  }
-  __syncwarp();
-  return true;
-}
-
-// z1 of one unit j (scalar path; ragged H tails).
-__device__ __forceinline__ float z1_unit(const float *feats, const float *w1, int n, int H,
-                                         int j) {
-  float acc = 0.f;
-  if (n <= 48) {
-    for (int i = 0; i < n; ++i) acc = __fmaf_rn(feats[i], w1[(size_t)i * H + j], acc);
-    return acc;
-  }
-  int i = 0;
-  const int blocks[4] = {8, 4, 2, 1};
-  for (int bi = 0; bi < 4; ++bi) {
-    const int bs = blocks[bi];
-    while (n - i >= bs) {
-      float t = 0.f;
-      for (int q = 0; q < bs; ++q) t = __fmaf_rn(feats[i + q], w1[(size_t)(i + q) * H + j], t);
-      acc = __fadd_rn(acc, t);
-      i += bs;
-      if (bs != 8) break;
-    }
-  }
-  return acc;
-}
-
-// z1 = feats @ W1 + b1 and ReLU into hs, for the units owned by this warp:
-// j = jb + 4*lane + 128*(u0 + u) + e (jb over 512-blocks, u < NU, e < 4),
-// i.e. NU*4 independent FMA chains per lane with 16-byte conflict-free W1
-// reads.  NU = 4, u0 = 0: one warp does all units; NU = 1, u0 = w: warp w of
-// a 4-warp team does a quarter.  Per-unit arithmetic is identical.
-template <bool G>
-__device__ __forceinline__ float4 ld_w1(const float *p) {
-  if (G) return __ldg(reinterpret_cast<const float4 *>(p));
-  return *reinterpret_cast<const float4 *>(p);
-}
-
-template <int NU, bool W1G = false>
-__device__ __forceinline__ void mlp_z1(const float *feats, const float *w1, const float *b1, int n, int H,
-                       float *hs, int lane, int u0) {
-  if ((H % 4) == 0) {
-    for (int jb = 0; jb < H; jb += 512) {
-      float y[NU][4];
-#pragma unroll
-      for (int u = 0; u < NU; ++u)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) y[u][e] = 0.f;
-      if (n <= 48) {
-#pragma unroll 12
-        for (int i = 0; i < n; ++i) {
-          const float f = feats[i];
-#pragma unroll
-          for (int u = 0; u < NU; ++u) {
-            const int j0 = jb + 4 * lane + 128 * (u0 + u);
-            if (j0 < H) {
-              const float4 w = ld_w1<W1G>(w1 + (size_t)i * H + j0);
-              const float2 ff = make_float2(f, f);
-              const float2 a = ffma2(ff, make_float2(w.x, w.y), make_float2(y[u][0], y[u][1]));
-              const float2 b = ffma2(ff, make_float2(w.z, w.w), make_float2(y[u][2], y[u][3]));
-              y[u][0] = a.x; y[u][1] = a.y; y[u][2] = b.x; y[u][3] = b.y;
-            }
-          }
-        }
-      } else {
-        int i = 0;
-        const int blocks[4] = {8, 4, 2, 1};
-        for (int bi = 0; bi < 4; ++bi) {
-          const int bs = blocks[bi];
-          while (n - i >= bs) {
-            float t[NU][4];
-#pragma unroll
-            for (int u = 0; u < NU; ++u)
-#pragma unroll
-              for (int e = 0; e < 4; ++e) t[u][e] = 0.f;
-            for (int q = 0; q < bs; ++q) {
-              const float f = feats[i + q];
-#pragma unroll
-              for (int u = 0; u < NU; ++u) {
-                const int j0 = jb + 4 * lane + 128 * (u0 + u);
-                if (j0 < H) {
-                  const float4 w = ld_w1<W1G>(w1 + (size_t)(i + q) * H + j0);
-                  const float2 ff = make_float2(f, f);
-                  const float2 a = ffma2(ff, make_float2(w.x, w.y), make_float2(t[u][0], t[u][1]));
-                  const float2 b = ffma2(ff, make_float2(w.z, w.w), make_float2(t[u][2], t[u][3]));
-                  t[u][0] = a.x; t[u][1] = a.y; t[u][2] = b.x; t[u][3] = b.y;
-                }
-              }
-            }
-#pragma unroll
-            for (int u = 0; u < NU; ++u)
-#pragma unroll
-              for (int e = 0; e < 4; ++e) y[u][e] = __fadd_rn(y[u][e], t[u][e]);
-            i += bs;
-            if (bs != 8) break;
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < NU; ++u) {
-        const int j0 = jb + 4 * lane + 128 * (u0 + u);
-        if (j0 < H) {
-          const float4 bb = *reinterpret_cast<const float4 *>(b1 + j0);
-          float4 r;
-          r.x = fmaxf(__fadd_rn(y[u][0], bb.x), 0.f); r.y = fmaxf(__fadd_rn(y[u][1], bb.y), 0.f);
-          r.z = fmaxf(__fadd_rn(y[u][2], bb.z), 0.f); r.w = fmaxf(__fadd_rn(y[u][3], bb.w), 0.f);
-          *reinterpret_cast<float4 *>(hs + j0) = r;
-        }
-      }
-    }
-  } else {
-    // ragged H: scalar units, split over the same NU/u0 ownership by lanes
-    for (int j = lane + 32 * u0; j < H; j += 32 * (NU == 4 ? 1 : 4)) {
-      const float z1 = __fadd_rn(z1_unit(feats, w1, n, H, j), b1[j]);
-      hs[j] = z1 > 0.f ? z1 : 0.f;
-    }
-  }
-}
-
-// sdot partial A[c] (c < 64) = FMA chain over the 64-element blocks.
-__device__ __forceinline__ float z2_partial(const float *hs, const float *w2, int H, int c) {
-  const int n64 = (H & ~31) & ~63;
-  float a = 0.f;
-  for (int b = 0; b < n64; b += 64) a = __fmaf_rn(hs[b + c], w2[b + c], a);
-  return a;
-}
-
-// z2: OpenBLAS SkylakeX sdot order (sdot.c + sdot_microk_skylakex-2.c):
-// 4 x 16-lane FMA accumulators over 64-element blocks (alo = A[lane], ahi =
-// A[lane+32]), fold 16->8, optional 32-element AVX2 step, lane-wise
-// ((a0+a1)+a2)+a3, 8->4, ((q0+q1)+(q2+q3)), scalar tail, + b2.  Whole warp.
-__device__ __forceinline__ float z2_tree(float alo, float ahi, const float *hs, const float *w2, int H, float b2,
-                         int lane) {
-  const int n1 = H & ~31, n64 = n1 & ~63;
-  float blo = __fadd_rn(alo, __shfl_down_sync(0xffffffffu, alo, 8));
-  float bhi = __fadd_rn(ahi, __shfl_down_sync(0xffffffffu, ahi, 8));
-  const int m = lane & 15;
-  if (n1 > n64 && m < 8) {
-    const int a = lane >> 4;                 // 0 or 1 (lo), 2 or 3 (hi)
-    blo = __fmaf_rn(hs[n64 + 8 * a + m], w2[n64 + 8 * a + m], blo);
-    bhi = __fmaf_rn(hs[n64 + 8 * (a + 2) + m], w2[n64 + 8 * (a + 2) + m], bhi);
-  }
-  const float b1v = __shfl_down_sync(0xffffffffu, blo, 16);   // B_1[m] for lanes 0..7
-  const float b3v = __shfl_down_sync(0xffffffffu, bhi, 16);   // B_3[m]
-  const float s = __fadd_rn(__fadd_rn(__fadd_rn(blo, b1v), bhi), b3v);
-  const float q = __fadd_rn(s, __shfl_down_sync(0xffffffffu, s, 4));
-  const float q0 = __shfl_sync(0xffffffffu, q, 0), q1 = __shfl_sync(0xffffffffu, q, 1);
-  const float q2 = __shfl_sync(0xffffffffu, q, 2), q3 = __shfl_sync(0xffffffffu, q, 3);
-  float dot = n1 ? __fadd_rn(__fadd_rn(q0, q1), __fadd_rn(q2, q3)) : 0.f;
-  for (int i = n1; i < H; ++i) dot = __fadd_rn(dot, __fmul_rn(hs[i], w2[i]));
-  __syncwarp();
-  return __fadd_rn(dot, b2);
-}
-
-// MLP of one row by one warp.  w1/b1/w2 may point to shared or global memory;
-// hs: scratch of H floats.  Returns z2 in every lane.
-__device__ __forceinline__ float warp_mlp(const float *feats, const float *w1, const float *b1, const float *w2,
-                          float b2, int K, int H, float *hs, int lane) {
-  mlp_z1<4>(feats, w1, b1, 3 * K, H, hs, lane, 0);
-  __syncwarp();
-  return z2_tree(z2_partial(hs, w2, H, lane), z2_partial(hs, w2, H, lane + 32), hs, w2, H, b2,
-                 lane);
-}
-// Same, W1 read from global memory through the read-only path.
-__device__ __forceinline__ float warp_mlp_g(const float *feats, const float *w1, const float *b1, const float *w2,
-                            float b2, int K, int H, float *hs, int lane) {
-  mlp_z1<4, true>(feats, w1, b1, 3 * K, H, hs, lane, 0);
-  __syncwarp();
-  return z2_tree(z2_partial(hs, w2, H, lane), z2_partial(hs, w2, H, lane + 32), hs, w2, H, b2,
-                 lane);
-}
-
-__device__ __forceinline__ float sigmoid32(float z) {     // predictor.py:87-94, in f32
-  if (z >= 0.f) return 1.f / (1.f + __expf(-z));
-  const float ez = __expf(z);
-  return ez / (1.f + ez);
-}
-
-__device__ __forceinline__ double sigmoid64(float z2) {   // predictor.py:87-94
-  const double z = (double)z2;
-  if (z >= 0.0) return 1.0 / (1.0 + exp(-z));
-  const double ez = exp(z);
-  return ez / (1.0 + ez);
-}
-
-// Everything after the logits, for one row (whole warp).
-__device__ void warp_row_tail(const PredParams &p, int row, float *feats, const float *w1,
-                              const float *b1, const float *w2, float *hs, int lane) {
-  const int K = p.K;
-  const bool ok = warp_softmax_features(p, row, feats, lane);
-  if (p.logits_out) {
-    if (lane < K) p.logits_out[(size_t)row * K + lane] = feats[lane];
-    if (lane + 32 < K) p.logits_out[(size_t)row * K + lane + 32] = feats[lane + 32];
-  }
-  if (!ok) {
-    if (lane == 0 && p.fired) p.fired[row] = 0;
-    return;
-  }
-  if (p.feat_out)
-    for (int i = lane; i < 3 * K; i += 32) p.feat_out[(size_t)row * 3 * K + i] = feats[i];
-  if (lane < K) p.prev[(size_t)row * K + lane] = feats[K + lane];            // engine.py:196
-  if (lane + 32 < K) p.prev[(size_t)row * K + lane + 32] = feats[K + lane + 32];
-  if (lane == 0 && p.evals) p.evals[row] += 1;
-  if (p.policy == SPX_POLICY_MLP) {
-    const float z2 = warp_mlp(feats, w1, b1, w2, p.b2, K, p.H, hs, lane);
-    if (lane == 0) {
-      if (p.z_out) p.z_out[row] = z2;
-      if (p.prob_out) p.prob_out[row] = sigmoid64(z2);
-      if (p.fired) p.fired[row] = (z2 >= p.z_cut) ? 1 : 0;
-    }
-  } else if (lane == 0) {
-    if (p.prob_out) p.prob_out[row] = p.const_prob;
-    if (p.z_out) p.z_out[row] = 0.0f;
-    if (p.fired) p.fired[row] = (p.const_prob > p.threshold) ? 1 : 0;
-  }
-}
-
-// ------------------------------------------------------------ FAST
-#include "spx_pred_fast.cuh"
-#include "spx_pred_stream.cuh"
-
-// ----------------------------------------------------------- STRICT (parity)
-// The reference's own operation sequence: every sum a left-to-right chain of
-// separately rounded adds from 0, every product rounded (no FMA).  One CTA
-// per row; the softmax/MLP tail is the same warp code as the FAST kernel.
-constexpr int STRICT_THREADS = 128;
 
 template <typename TW>
 __global__ void __launch_bounds__(STRICT_THREADS)
@@ -352,59 +34,52 @@ predictor_strict_kernel(PredParams p) {
     if (threadIdx.x == 0 && p.fired) p.fired[row] = 0;
     return;
   }
-  extern __shared__ float hn[];   // d floats
+  extern __shared__ __align__(16) uint8_t dsm[];
   __shared__ float feats[3 * MAXK];
   __shared__ float hs[MAXH];
-  __shared__ float s_mean, s_denom;
+  __shared__ int ids_s[MAXK];
+  __shared__ float s_stat[2];
   __shared__ int s_flag;
-  const int tid = threadIdx.x, d = p.d;
-  const float *x = p.hidden + (size_t)row * p.hidden_stride;
-  if (tid == 0) s_flag = 0;
-  __syncthreads();
-  bool finite = true;
-  for (int j = tid; j < d; j += STRICT_THREADS) { hn[j] = x[j]; finite &= is_finite(hn[j]); }
-  if (!finite) { atomicOr(p.err, ERR_HIDDEN_NONFINITE); s_flag = 1; }
-  __syncthreads();
-  const float df = (float)d;
-  if (tid == 0) {
-    float acc = 0.0f;
-    for (int j = 0; j < d; ++j) acc = __fadd_rn(acc, hn[j]);
-    s_mean = __fdiv_rn(acc, df);
+  strict_row<TW>(p, row, dsm, feats, hs, ids_s, s_stat, &s_flag);
+  if (threadIdx.x == 0 && p.prev_err) p.prev_err[row] = 0.f;
+}
+
+// STRICT re-evaluation of deferred rows as its own launch: used when the
+// FAST kernel's shared memory cannot hold the re-evaluation scratch (its
+// epilogue then leaves the flagged rows).  Scans the row flags.
+template <typename TW>
+__global__ void __launch_bounds__(STRICT_THREADS)
+predictor_recheck_kernel(PredParams p) {
+  if (p.pdl) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   }
-  __syncthreads();
-  const float mean = s_mean;
-  for (int j = tid; j < d; j += STRICT_THREADS) hn[j] = __fsub_rn(hn[j], mean);
-  __syncthreads();
-  if (tid == 0) {
-    float acc = 0.0f;
-    for (int j = 0; j < d; ++j) acc = __fadd_rn(acc, __fmul_rn(hn[j], hn[j]));
-    s_denom = __fsqrt_rn(__fadd_rn(__fdiv_rn(acc, df), 1e-5f));
-  }
-  __syncthreads();
-  const float denom = s_denom;
-  for (int j = tid; j < d; j += STRICT_THREADS) hn[j] = ln_elem(hn[j], denom, p.norm_g[j], p.norm_b[j]);
-  __syncthreads();
-  const int K = p.K;
-  if (tid < K) {
-    int id = p.ids[(size_t)row * K + tid];
-    if (id < 0 || id >= p.V) { atomicOr(p.err, ERR_ID_RANGE); s_flag = 1; id = 0; }
-    const TW *wr = reinterpret_cast<const TW *>(p.head) + (size_t)id * d;
-    float acc = 0.0f;
-    for (int j = 0; j < d; j += CHUNK) {
-      float w[4];
-      load4_f32<TW>(wr + j, w);
-#pragma unroll
-      for (int e = 0; e < CHUNK; ++e) acc = __fadd_rn(acc, __fmul_rn(hn[j + e], w[e]));
+  extern __shared__ __align__(16) uint8_t dsm[];
+  float *scr = reinterpret_cast<float *>(dsm);
+  for (int row = blockIdx.x; row < p.B; row += gridDim.x) {
+    if (*(volatile int *)(p.recheck + 5 + row)) {
+      __syncthreads();
+      if (threadIdx.x == 0) p.recheck[5 + row] = 0;
+      recheck_row<TW>(p, row, scr);
     }
-    feats[tid] = acc;
   }
-  __syncthreads();
-  if (tid >= 32) return;
-  if (s_flag) {
-    if (tid == 0 && p.fired) p.fired[row] = 0;
-    return;
+}
+
+// spx_predictor_cert: per-layer constants of the bound (see certify_row).
+__global__ void predictor_cert_kernel(const float *w1, const float *b1, const float *w2, int K,
+                                      int H, float *cert) {
+  const int i = blockIdx.x, lane = threadIdx.x;   // one warp per output
+  const int n = 3 * K;
+  float s = 0.f;
+  if (i < n) {
+    for (int j = lane; j < H; j += 32) s = fmaf(fabsf(w2[j]), fabsf(w1[(size_t)i * H + j]), s);
+  } else if (i == n) {
+    for (int j = lane; j < H; j += 32) s = fmaf(fabsf(w2[j]), fabsf(b1[j]), s);
+  } else {
+    for (int j = lane; j < H; j += 32) s += fabsf(w2[j]);
   }
-  warp_row_tail(p, row, feats, p.w1, p.b1, p.w2, hs, tid);
+  s = warp_butterfly_sum(s);
+  if (lane == 0) cert[i] = s * 1.0001f;            // rounded up past the sum's own error
 }
 
 // ---------------------------------------------------------------------------
@@ -460,24 +135,23 @@ __global__ void features_wide_kernel(const float *logits, const float *prev, flo
     f[K + i] = np_expf(__fsub_rn(x[i], m));
   }
   __syncthreads();
-  // the two sums stay strict left-to-right chains on thread 0; the operands are
-  // staged through shared memory in chunks so the chain never waits on HBM
+  // the softmax denominator stays the strict left-to-right chain on thread 0
+  // (operands staged through shared memory in chunks so the chain never waits
+  // on HBM); the prev check is numpy's pairwise sum (predictor.py:49)
   constexpr int WCH = 2048;
-  __shared__ float s_e[WCH], s_p[WCH];
-  float esum = 0.f, psum = 0.f;
+  __shared__ float s_e[WCH];
+  float esum = 0.f;
   for (int c0 = 0; c0 < K; c0 += WCH) {
     const int n = K - c0 < WCH ? K - c0 : WCH;
-    for (int i = tid; i < n; i += blockDim.x) { s_e[i] = f[K + c0 + i]; s_p[i] = pv[c0 + i]; }
+    for (int i = tid; i < n; i += blockDim.x) s_e[i] = f[K + c0 + i];
     __syncthreads();
     if (tid == 0) {
 #pragma unroll 8
-      for (int c = 0; c < n; ++c) {
-        esum = __fadd_rn(esum, s_e[c]);
-        psum = __fadd_rn(psum, s_p[c]);
-      }
+      for (int c = 0; c < n; ++c) esum = __fadd_rn(esum, s_e[c]);
     }
     __syncthreads();
   }
+  const float psum = tid == 0 ? np_pairwise_sum(0, K, [&](int i) { return pv[i]; }) : 0.f;
   if (tid == 0) {
     int e = 0;
     if (s_bad) e |= ERR_LOGIT_NONFINITE;
@@ -536,6 +210,10 @@ static void device_limits() {
 }
 
 template <typename TW>
+static int launch_fast(const PredParams &p, const spx_predictor_args *a, cudaStream_t stream,
+                       bool &inline_rc);
+
+template <typename TW>
 static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cudaStream_t stream) {
   device_limits();
   bool strict = a->mode == SPX_MODE_STRICT;
@@ -548,12 +226,47 @@ static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cu
     if (!stream_ok && plan_smem<TW>(p.d, p.K, p.H, g_smem_optin).bytes == 0) strict = true;
   }
   if (strict) {
-    const size_t smem = (size_t)a->d * sizeof(float);
+    const size_t smem = strict_smem_bytes(p.d, p.K);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(predictor_strict_kernel<TW>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     predictor_strict_kernel<TW><<<(unsigned)a->B, STRICT_THREADS, smem, stream>>>(p);
   } else {
+    bool inline_rc = false;
+    const int rc = launch_fast<TW>(p, a, stream, inline_rc);
+    if (rc) return rc;
+    if (p.recheck && !inline_rc) {
+      // STRICT re-evaluation of deferred rows as a separate launch (the FAST
+      // kernel's shared memory could not hold its scratch)
+      const size_t smem = recheck_scratch_bytes(p.d, p.K);
+      static bool configured = false;
+      if (!configured) {
+        cudaFuncSetAttribute(predictor_recheck_kernel<TW>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        configured = true;
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(p.B < g_sms ? p.B : g_sms));
+      cfg.blockDim = dim3(STRICT_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = p.pdl ? 1 : 0;
+      cudaLaunchKernelEx(&cfg, predictor_recheck_kernel<TW>, p);
+    }
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+}
+
+template <typename TW>
+static int launch_fast(const PredParams &p0, const spx_predictor_args *a, cudaStream_t stream,
+                       bool &inline_rc) {
+  PredParams p = p0;
+  const size_t rscr = recheck_scratch_bytes(p.d, p.K);
+  {
     if (((size_t)p.d * sizeof(TW)) % 16) return SPX_EINVAL;   // TMA bulk: 16-byte rows
     static const int env_stream = getenv("SPX_PRED_STREAM") ? atoi(getenv("SPX_PRED_STREAM")) : 3;
     if (std::is_same<TW, __nv_bfloat16>::value && env_stream && p.K <= SKMAX &&
@@ -581,17 +294,16 @@ static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cu
         per_sm = 1;
       }
       if (st.bytes) {
+        inline_rc = p.recheck && rscr <= st.off_bar;   // epilogue re-evaluates deferred rows
+        p.recheck_inline = inline_rc ? 1 : 0;
         // SPX_PRED_CTAS_PER_SM (sweeps): 1 leaves the second CTA slot of every SM
         // free for the next (programmatic dependent) launch's prefetch
         static const int env_cps = getenv("SPX_PRED_CTAS_PER_SM") ? atoi(getenv("SPX_PRED_CTAS_PER_SM")) : 2;
         if (env_cps == 1) per_sm = 1;
         const long long cap = (long long)per_sm * g_sms;
         const int grid = (int)(a->B < cap ? a->B : cap);
-        StreamLaunch<TW> L{p, st, grid, stream, g_smem_optin, ldgx};
-        if (p.d == 2048) L.template operator()<4>();
-        else if (p.d == 4096) L.template operator()<8>();
-        else L.template operator()<16>();
-        return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+        if constexpr (std::is_same<TW, __nv_bfloat16>::value)
+          return launch_stream_bf16(p, st, grid, stream, g_smem_optin, ldgx);
       }
     }
     // tuning overrides (benchmark sweeps only)
@@ -599,10 +311,11 @@ static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cu
     static const int env_ring = getenv("SPX_PRED_RING") ? atoi(getenv("SPX_PRED_RING")) : -1;
     SmemPlan sp = plan_smem<TW>(p.d, p.K, p.H, g_smem_optin, env_w1, env_ring);
     if (sp.bytes == 0) return SPX_EINVAL;
+    inline_rc = p.recheck && rscr <= sp.off_bar;
+    p.recheck_inline = inline_rc ? 1 : 0;
     const long long need = (a->B + NTEAM - 1) / NTEAM;
     const int grid = (int)(need < g_sms ? need : g_sms);
-    if (!dispatch_cpl(p.d, FastLaunch<TW>{p, sp, grid > 0 ? grid : 1, stream, g_smem_optin}))
-      return SPX_EINVAL;
+    return launch_team<TW>(p, sp, grid > 0 ? grid : 1, stream, g_smem_optin);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
 }
@@ -632,6 +345,14 @@ extern "C" int spx_predictor_eval(const spx_predictor_args *a, void *stream_) {
   p.pdl = a->pdl == 2 ? 2 : a->pdl ? 1 : 0;
   p.B = (int)a->B; p.d = (int)a->d; p.V = (int)a->V; p.K = (int)a->K;
   p.H = a->policy == SPX_POLICY_MLP ? (int)a->H : 0;
+  p.head_wmax = a->head_wmax; p.cert = a->cert;
+  p.cert_kappa = a->cert_kappa; p.cert_hnorm = a->cert_hnorm;
+  p.prev_err = a->prev_err;
+  p.recheck = a->mode == SPX_MODE_FAST ? a->recheck : nullptr;
+  p.recheck_inline = 0;
+  if (p.recheck && (!a->head_wmax || !a->prev_err ||
+                    (a->policy == SPX_POLICY_MLP && !a->cert)))
+    return SPX_EINVAL;
   if (a->head_dtype == SPX_DTYPE_F32) return launch_predictor<float>(p, a, stream);
   if (a->head_dtype == SPX_DTYPE_BF16) return launch_predictor<__nv_bfloat16>(p, a, stream);
   return SPX_EINVAL;
@@ -702,5 +423,47 @@ extern "C" int spx_tree_node_eval(const float *logits, const int32_t *live_idx, 
   p.K = (int)K; p.H = policy == SPX_POLICY_MLP ? (int)H : 0;
   tree_node_eval_kernel<<<(unsigned)n_live, 32, 0, (cudaStream_t)stream>>>(p, logits, live_idx,
                                                                           (int)n_live);
+  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+}
+
+extern "C" int spx_predictor_cert(const float *w1, const float *b1, const float *w2, int64_t K,
+                                  int64_t H, float *cert, void *stream) {
+  if (!w1 || !b1 || !w2 || !cert || K < 1 || K > MAXK || H < 1 || H > MAXH) return SPX_EINVAL;
+  predictor_cert_kernel<<<(unsigned)(3 * K + 2), 32, 0, (cudaStream_t)stream>>>(w1, b1, w2, (int)K,
+                                                                               (int)H, cert);
+  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+}
+
+namespace spx {
+template <typename TW>
+__global__ void head_stats_kernel(const TW *head, int64_t V, int d, float *wmax) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); v < V; v += warps) {
+    float m = 0.f;
+    for (int j = lane * CHUNK; j < d; j += 32 * CHUNK) {
+      float w[4];
+      load4_f32<TW>(head + (size_t)v * d + j, w);
+#pragma unroll
+      for (int e = 0; e < CHUNK; ++e) m = fmaxf(m, fabsf(w[e]));
+    }
+    m = warp_max_f(m);
+    if (lane == 0) wmax[v] = m;
+  }
+}
+}  // namespace spx
+
+extern "C" int spx_head_stats(const void *head, int32_t head_dtype, int64_t V, int64_t d,
+                              float *wmax, void *stream) {
+  if (!head || !wmax || V < 1 || d < CHUNK || d % CHUNK) return SPX_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (head_dtype == SPX_DTYPE_BF16)
+    head_stats_kernel<__nv_bfloat16><<<592, 256, 0, st>>>(
+        reinterpret_cast<const __nv_bfloat16 *>(head), V, (int)d, wmax);
+  else if (head_dtype == SPX_DTYPE_F32)
+    head_stats_kernel<float><<<592, 256, 0, st>>>(reinterpret_cast<const float *>(head), V, (int)d,
+                                                  wmax);
+  else
+    return SPX_EINVAL;
   return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
 }

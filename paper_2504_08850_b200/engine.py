@@ -177,6 +177,8 @@ class _DeviceStep:
         cap = t.max_context
         self.cap = cap
         self.prev = torch.zeros(self.K, dtype=torch.float32, device="cuda")
+        self.prev_err = torch.zeros(1, dtype=torch.float32, device="cuda")
+        self.recheck = torch.zeros(6, dtype=torch.int32, device="cuda")
         self.done, self.fired, self.fired_any = _u8(1), _u8(1), _u8(1)
         self.exit_layer, self.exit_token, self.final_token = _i32(1), _i32(1), _i32(1)
         self.evals, self.full_heads, self.next_in, self.step = _i32(1), _i32(1), _i32(1), _i32(1)
@@ -198,7 +200,7 @@ class _DeviceStep:
         for name in ("prev", "done", "fired", "fired_any", "exit_layer", "exit_token",
                      "final_token", "evals", "full_heads", "next_in", "step", "active",
                      "rec_token", "rec_exit_layer", "rec_evals", "rec_full_heads", "rec_fired",
-                     "rec_verified", "rec_active"):
+                     "rec_verified", "rec_active", "prev_err"):
             setattr(st, name, N.ptr(getattr(self, name)))
         self.cst = st
 
@@ -229,6 +231,12 @@ class _DeviceStep:
         a.row_done, a.evals = N.ptr(self.done), N.ptr(self.evals)
         a.layer, a.mode, a.pdl, a.err = l, mode, 0, N.ptr(self.err)
         a.B, a.d, a.V, a.K, a.H = 1, m.config.hidden_dim, m.config.vocab_size, self.K, H
+        a.prev_err = N.ptr(self.prev_err)
+        if mode == N.SPX_MODE_FAST:        # certified FAST decisions
+            a.head_wmax, a.recheck = N.ptr(m.head_wmax), N.ptr(self.recheck)
+            a.cert_kappa, a.cert_hnorm = m.cert_kappa, m.cert_hnorm
+            if pol.const_prob is None:
+                a.cert = N._vp(pb.cert[l].data_ptr())
         return a
 
     def enqueue(self, mode, forced: bool):
@@ -384,7 +392,8 @@ class ExitEngine:
                 st.begin(prompt[:-1])
                 for l in range(m.config.num_layers):
                     st.launch_layer(l)
-        self.online.reset()
+        # the online window persists across generate() calls, as in the
+        # reference (engine.py:122-160 creates it once, start() keeps it)
         self.context = prompt
         self.next_in = prompt[-1]
         self.policy.start(prompt)

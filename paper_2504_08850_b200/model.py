@@ -93,6 +93,9 @@ _LAYER_VEC = {"ln1.g": "ln1_g", "ln1.b": "ln1_b", "ln2.g": "ln2_g", "ln2.b": "ln
               "ffn.b1": "ffn_b1", "ffn.b2": "ffn_b2"}
 
 
+CERT_LAMBDA = 8.0     # rounding-error model multiplier
+
+
 class TransformerModel:
     """Immutable device weights of one model (target or draft).  Shareable
     across engines/streams (reference SPEC.md:112)."""
@@ -161,6 +164,17 @@ class TransformerModel:
         N.check(N.lib().spx_head_bias(N.ptr(self.lm_head), self.spx_dtype, N.ptr(self.final_b),
                                       self.config.vocab_size, self.config.hidden_dim,
                                       N.ptr(self.head_bw), N.stream_ptr()), "spx_head_bias")
+        # constants of the FAST-decision certification bound:
+        # per-row max |W_v|, ||LN(h)|| <= max|g| sqrt(d) + ||b||, kappa = 2 lambda u sqrt(d)
+        d = self.config.hidden_dim
+        self.head_wmax = torch.empty(self.config.vocab_size, dtype=torch.float32, device="cuda")
+        N.check(N.lib().spx_head_stats(N.ptr(self.lm_head), self.spx_dtype,
+                                       self.config.vocab_size, d, N.ptr(self.head_wmax),
+                                       N.stream_ptr()), "spx_head_stats")
+        gmax = float(self.final_g.abs().max())
+        bnorm = float(self.final_b.double().norm())
+        self.cert_hnorm = (gmax * math.sqrt(d) + bnorm) * (1 + 1e-6)
+        self.cert_kappa = 2.0 * CERT_LAMBDA * 2.0 ** -24 * math.sqrt(d)
         return self
 
     def numel(self):

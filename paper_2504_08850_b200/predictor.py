@@ -176,6 +176,15 @@ def predictor_param_count(k: int, hidden: int, num_layers: int):
     return per_layer * num_layers, per_layer * num_layers * 2 / 1024
 
 
+def _cert(w1, b1, w2, k, hidden):
+    """Per-layer constants of the FAST-decision certification bound
+    (spx_predictor_cert): M_i = sum_j |w2_j||W1_ij|, sum_j |w2_j b1_j|, sum |w2|."""
+    out = torch.empty(3 * k + 2, dtype=torch.float32, device="cuda")
+    N.check(N.lib().spx_predictor_cert(N.ptr(w1), N.ptr(b1), N.ptr(w2), k, hidden, N.ptr(out),
+                                       N.stream_ptr()), "spx_predictor_cert")
+    return out
+
+
 class _DeviceWeights:
     """One PredictorWeights on device (cached per object identity)."""
     _cache = {}
@@ -184,6 +193,7 @@ class _DeviceWeights:
         self.w1 = _dev(np.asarray(w.w1, np.float32))
         self.b1 = _dev(np.asarray(w.b1, np.float32))
         self.w2 = _dev(np.asarray(w.w2, np.float32))
+        self.cert = _cert(self.w1, self.b1, self.w2, w.k, w.hidden)
 
     @classmethod
     def of(cls, w):
@@ -221,6 +231,8 @@ class PredictorBank:
             w1[l], b1[l], w2[l] = w.w1, w.b1, w.w2
             self.b2[l] = np.float32(w.b2)
         self.w1, self.b1, self.w2 = _dev(w1), _dev(b1), _dev(w2)
+        self.cert = torch.stack([_cert(self.w1[l], self.b1[l], self.w2[l], self.k, self.hidden)
+                                 for l in range(num_layers)])
         self.mask = sum(1 << l for l in self.layers if l < 64)
 
 
@@ -292,16 +304,62 @@ class BatchResult:
         self.__dict__.update(kw)
 
 
+_RECHECK = {}
+
+
+def recheck_buffer(B: int, device=None):
+    """The (5 + B) int32 work list of the STRICT re-evaluation, one per
+    (stream, B); zeroed once, self-resetting (spx_predictor_args.recheck)."""
+    key = (torch.cuda.current_stream().cuda_stream, int(B))
+    buf = _RECHECK.get(key)
+    if buf is None:
+        buf = torch.zeros(5 + int(B), dtype=torch.int32, device=device or "cuda")
+        _RECHECK[key] = buf
+    return buf
+
+
+def recheck_stats(buf=None):
+    """(rows re-evaluated by the STRICT chain, rows whose STRICT decision was
+    still inside the carried-prev bound) summed over the given buffer, or over
+    every buffer of this process (synchronises)."""
+    bufs = [buf] if buf is not None else list(_RECHECK.values())
+    tot = [0, 0]
+    for b in bufs:
+        v = b[3:5].cpu().tolist()
+        tot[0] += v[0]
+        tot[1] += v[1]
+    return tuple(tot)
+
+
+def prev_error(prev: torch.Tensor) -> torch.Tensor:
+    """The (B,) bound on |prev - prev_ref| carried with a prev tensor (created
+    as zeros: a freshly filled prev -- the uniform prior or reference values --
+    is exact).  Reset it with ``prev_error(prev).zero_()`` when prev is reset."""
+    e = getattr(prev, "_spx_err", None)
+    B = prev.shape[0] if prev.dim() > 1 else 1
+    if e is None or e.numel() != B:
+        e = torch.zeros(B, dtype=torch.float32, device=prev.device)
+        prev._spx_err = e
+    return e
+
+
 def evaluate_batch(model, weights, hidden, ids, prev, threshold=0.5, layer=0, outputs=True, pdl=False,
                    row_layer_mask=None, row_done=None, evals=None, err=None, mode=None,
-                   policy=None, out=None):
+                   policy=None, out=None, prev_err=None, recheck=None, certify=True):
     """K1+K2+K3 for B rows at one layer in ONE launch (spx_predictor_eval).
 
     model: TransformerModel (head + final norm used); weights: PredictorWeights
     or PredictorBank (row `layer` used); hidden (B, d) f32 CUDA; ids (B, K)
     int32 CUDA; prev (B, K) f32 CUDA, updated in place with the new local
     probabilities.  policy: None (MLP) or a constant probability (Never /
-    Always policies).  Returns a BatchResult of device tensors (no sync)."""
+    Always policies).  Returns a BatchResult of device tensors (no sync).
+
+    FAST mode certifies every decision against the reference's (DESIGN.md
+    3.1): rows it cannot certify are re-evaluated by the STRICT chain in a
+    follow-up launch of the same call, so ``fired`` is the reference's.
+    prev_err (B,) is the error bound carried with ``prev`` (default: attached
+    to the prev tensor, see prev_error); recheck the work list (default: one
+    per stream and B, see recheck_buffer).  certify=False turns it off."""
     B, d = hidden.shape
     K = ids.shape[1]
     dev = hidden.device
@@ -317,16 +375,19 @@ def evaluate_batch(model, weights, hidden, ids, prev, threshold=0.5, layer=0, ou
     a.norm_g, a.norm_b = N.ptr(model.final_g), N.ptr(model.final_b)
     a.head, a.head_dtype, a.head_bw = N.ptr(model.lm_head), model.spx_dtype, N.ptr(model.head_bw)
     a.ids, a.prev = N.ptr(ids), N.ptr(prev)
+    cert = None
     if policy is None:
         if isinstance(weights, PredictorBank):
             a.w1 = N._vp(weights.w1[layer].data_ptr())
             a.b1 = N._vp(weights.b1[layer].data_ptr())
             a.w2 = N._vp(weights.w2[layer].data_ptr())
             a.b2 = float(weights.b2[layer])
+            cert = weights.cert[layer]
             H = weights.hidden
         else:
             dw = _DeviceWeights.of(weights)
             a.w1, a.b1, a.w2, a.b2 = N.ptr(dw.w1), N.ptr(dw.b1), N.ptr(dw.w2), float(np.float32(weights.b2))
+            cert = dw.cert
             H = weights.hidden
         a.policy = N.SPX_POLICY_MLP
         a.z_cut = z_cut(threshold)
@@ -340,5 +401,13 @@ def evaluate_batch(model, weights, hidden, ids, prev, threshold=0.5, layer=0, ou
     a.pdl = 2 if (pdl == 2 and pdl is not True) else (1 if pdl else 0)
     a.err = N.ptr(out.err)
     a.B, a.d, a.V, a.K, a.H = B, d, model.config.vocab_size, K, H
+    if certify and a.mode == N.SPX_MODE_FAST:
+        out.recheck = recheck if recheck is not None else recheck_buffer(B)
+        a.head_wmax, a.cert = N.ptr(model.head_wmax), N.ptr(cert)
+        a.cert_kappa, a.cert_hnorm = model.cert_kappa, model.cert_hnorm
+        a.prev_err = N.ptr(prev_err if prev_err is not None else prev_error(prev))
+        a.recheck = N.ptr(out.recheck)
+    elif a.mode == N.SPX_MODE_STRICT:
+        a.prev_err = N.ptr(prev_err if prev_err is not None else prev_error(prev))
     N.check(N.lib().spx_predictor_eval(a, N.stream_ptr()), "spx_predictor_eval")
     return out

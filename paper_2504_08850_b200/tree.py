@@ -173,30 +173,6 @@ class TreeEngine:
         self.record_probs = False          # diagnostic: per-call (layer, prob) log
         self.prob_log = []
 
-    # -- draft proposals (speculation.py:62-84) with a per-step logits cache ----
-
-    def _draft_logits(self, context):
-        key = tuple(context)
-        lg = self._logit_cache.get(key)
-        if lg is None:
-            if self._dstate is None:
-                self._dstate = DecodeState(self.draft)
-            st = self._dstate
-            st.reset()
-            st.begin(list(context))
-            for l in range(self.draft.config.num_layers):
-                st.launch_layer(l)
-            lg = full_head_logits(self.draft, st.cur_hidden).clone()
-            self._logit_cache[key] = lg
-        return lg
-
-    def _propose(self, context, k):
-        if len(context) == 0:
-            raise ValueError("empty context")
-        if k > self.draft.config.vocab_size:
-            raise ValueError("k exceeds vocabulary size")
-        return speculative_set_from_logits(self._draft_logits(context), k)
-
     # -- reference API -------------------------------------------------------------
 
     def start(self, prompt):
@@ -216,7 +192,8 @@ class TreeEngine:
                 st.begin(prompt[:-1])
                 for l in range(m.config.num_layers):
                     st.launch_layer(l)
-        self.online.reset()
+        # the online window persists across generate() calls, as in the
+        # reference (tree.py:133-170 creates it once, start() keeps it)
         self.context = prompt
         self.policy.start(prompt)
 

@@ -226,11 +226,14 @@ def test_tiny_pipeline_trace_on_device(oracle):
         golden = [json.loads(line) for line in fh if line.strip()]
     out = []
     with numerics.using("strict"):
-        eng = E.ExitEngine(t, dm, E.PredictorPolicy(bank),
-                           E.EngineConfig(k=4, threshold=0.7, schedule_mode="two-level"), prof,
-                           spx.ScheduleConfig(5, 1, 4))
-        assert eng.device_resident()
+        pol = E.PredictorPolicy(bank)
         for prompt in prompts:
+            # one engine per prompt, as the reference pipeline does
+            # (pipeline.py:220-223): each starts with an empty online window
+            eng = E.ExitEngine(t, dm, pol,
+                               E.EngineConfig(k=4, threshold=0.7, schedule_mode="two-level"),
+                               prof, spx.ScheduleConfig(5, 1, 4))
+            assert eng.device_resident()
             base, _ = E.greedy_generate(t, prompt, 48)
             out.extend(eng.generate_forced(prompt, base))
     assert len(out) == len(golden) == 768
