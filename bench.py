@@ -317,6 +317,49 @@ def decode_bench(args, rank, ws, dev):
     ms_tok = float(ms.item()) / n
     # executed decoder layers = exit layer + 1; plus full-head GEMVs (262 MB)
     tok_bytes = (el + 1) * layer_bytes + heads * V * D * 2 + 2 * layer_bytes + V * D * 2
+    # injected-spec variant: generate_forced over the greedy
+    # stream with the target's final argmax put into the draft ids at 80% of
+    # the steps, so verification succeeds and exits actually happen
+    base, _ = E.greedy_generate(t, prompt, n)
+    flags = (rng.splitmix64(seed + 99, n) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53 < 0.8
+    dv = eng._dev
+
+    def forced_start():
+        eng.start(prompt)
+        dv.forced[:n].copy_(torch.as_tensor(np.asarray(base, np.int32)))
+        dv.inject[:n].copy_(torch.as_tensor(flags.astype(np.uint8)))
+
+    gi = dv.graph(True, True)
+    forced_start()
+    for _ in range(3):
+        gi.replay()
+    forced_start()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(n):
+        gi.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms_i = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(ms_i, op=dist.ReduceOp.MAX)
+    irecs = dv.records(n)
+    iel = float(np.mean([r.exit_layer for r in irecs]))
+    iheads = float(np.mean([r.full_head_count for r in irecs]))
+    ibytes = (iel + 1) * layer_bytes + iheads * V * D * 2 + 2 * layer_bytes + V * D * 2
+    injected = {"tok_s": ws * n / (float(ms_i.item()) / 1e3), "unit": "tokens/s",
+                "ms_per_token": float(ms_i.item()) / n, "p_inject": 0.8,
+                "avg_exit_layer": iel, "full_heads_per_token": iheads,
+                "fire_token_frac": float(np.mean([r.predictor_fired for r in irecs])),
+                "verified_frac": float(np.mean([r.verified for r in irecs])),
+                "hbm_bytes_per_token": ibytes,
+                "hbm_GBps": ibytes / (float(ms_i.item()) / n * 1e-3) / 1e9,
+                "tokens_match_greedy": [r.token for r in irecs] == list(base),
+                "config": "generate_forced over the greedy stream; at 80% of the steps "
+                          "(splitmix64 flags) the target's final argmax replaces the last "
+                          "draft id (injected-spec hook on _speculative_set)"}
     tree = None
     if not args.no_tree:
         # configs[2]: EAGLE-like token tree, context-aware merged mapping
@@ -324,6 +367,7 @@ def decode_bench(args, rank, ws, dev):
         import tree_bench
         tree = tree_bench.run(steps=3, seed=seed, models=(t, d))
     return {"tok_s": ws * n / (float(ms.item()) / 1e3), "unit": "tokens/s", "tree": tree,
+            "injected": injected,
             "ms_per_token": ms_tok, "streams": ws, "tokens_per_stream": n,
             "e2e_tok_s": ws * n / float(e2e_s.item()),
             "avg_exit_layer": el, "full_heads_per_token": heads,

@@ -319,6 +319,11 @@ int spx_or_flag(const uint8_t *src, uint8_t *dst, void *stream);
 /* generate_forced (engine.py:227-246): *next_in = forced[*step - 1] */
 int spx_force_next(const int32_t *forced, const int32_t *step, int32_t *next_in,
                    int64_t n_forced, void *stream);
+/* injected-spec hook on _speculative_set (engine.py:162-168):
+ * if flags[*step], forced[*step] (the target's final argmax under
+ * generate_forced) replaces spec_ids[K-1] unless already among the K ids */
+int spx_inject_spec(int32_t *spec_ids, int32_t K, const int32_t *forced, const int32_t *step,
+                    const uint8_t *flags, int64_t n, void *stream);
 
 /* numpy float32 exp restated on device (the exp of softmax_1d, model.py:151),
  * elementwise -- test hook for the bit-exactness of the softmax. */

@@ -567,11 +567,12 @@ class ExitEngineOracle:
             return list(range(L - 1))
         return active_layers(self.counts, self.online, self.sc)
 
-    def step(self, spec=None):
+    def step(self, spec=None, drafted_already=False):
         """engine.py:176-217 (``spec`` overrides the draft proposal: the
-        injected-spec hook of SURVEY.md §8d C2)."""
+        injected-spec hook of SURVEY.md §8d C2; drafted_already: the draft
+        forward of this step has run)."""
         L = self.tc.num_layers
-        drafted = self._spec()
+        drafted = None if drafted_already else self._spec()
         spec = drafted if spec is None else list(spec)
         active = self._active()
         aset = set(active)
@@ -620,12 +621,20 @@ class ExitEngineOracle:
         trace = [self.step() for _ in range(max_new)]
         return [r.token for r in trace], trace
 
-    def generate_forced(self, prompt, forced):
-        """engine.py:227-246."""
+    def generate_forced(self, prompt, forced, inject=None):
+        """engine.py:227-246.  inject: per-step flags of the injected-spec hook
+        (SURVEY.md §8d C2): at a flagged step the forced token replaces the
+        last drafted id unless it is already among them."""
         self.start(prompt)
         trace = []
-        for tok in forced:
-            trace.append(self.step())
+        for i, tok in enumerate(forced):
+            spec = None
+            if inject is not None and inject[i]:
+                drafted = self._spec()
+                if int(tok) not in drafted:
+                    drafted[-1] = int(tok)
+                spec = drafted
+            trace.append(self.step(spec, drafted_already=spec is not None))
             self.context[-1] = int(tok)
             self.next_in = int(tok)
         return trace

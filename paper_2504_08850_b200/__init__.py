@@ -26,3 +26,5 @@ from .engine import (AlwaysExitPolicy, EngineConfig, ExitEngine, ExitRecord,  # 
                      oracle_exit_layer, read_trace, verify_exit, write_trace)
 
 __version__ = "0.1.0"
+from .profiling import (LayerTraces, TrainingExample, collect_training_data,  # noqa: F401
+                        generation_layer_traces, profile_offline_device)

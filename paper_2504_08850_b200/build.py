@@ -30,6 +30,17 @@ def _stale():
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
+def _obj_stale(src, obj):
+    """An object is rebuilt when missing, older than its source, or older
+    than any shared header (.cuh / include/*.h)."""
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    hdrs.append(os.path.join(HERE, "..", "include", "specexit_b200.h"))
+    return any(os.path.getmtime(p) > t for p in [src] + hdrs if os.path.exists(p))
+
+
 def build(force=False, verbose=False):
     if not force and not _stale():
         return LIB
@@ -38,24 +49,28 @@ def build(force=False, verbose=False):
     srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
     procs = []
     for s in srcs:
+        src = os.path.join(CSRC, s)
         obj = os.path.join(LIB_DIR, s.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, s), "-o", obj]
-        procs.append((s, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
+        if not force and not _obj_stale(src, obj):
+            continue
+        cmd = [NVCC, *FLAGS, "-c", src, "-o", obj + ".tmp"]
+        procs.append((s, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE,
+                                               stderr=subprocess.STDOUT)))
     logs = []
-    for s, p in procs:
+    for s, obj, p in procs:
         out, _ = p.communicate()
         logs.append(out.decode())
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed on {s}:\n{out.decode()}")
-    with open(os.path.join(LIB_DIR, "ptxas.log"), "w") as fh:
-        fh.write("\n".join(logs))
+        os.replace(obj + ".tmp", obj)
+    if logs:
+        with open(os.path.join(LIB_DIR, "ptxas.log"), "w") as fh:
+            fh.write("\n".join(logs))
     tmp = LIB + ".tmp"
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
                            "-o", tmp, *objs, "-lcudart"])
     os.replace(tmp, LIB)
-    for o in objs:
-        os.remove(o)
     if verbose:
         print("\n".join(logs))
     return LIB

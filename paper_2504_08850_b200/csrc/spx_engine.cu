@@ -142,22 +142,45 @@ __global__ void force_next_kernel(const int32_t *forced, const int32_t *step, in
   if (s >= 0 && s < n_forced) *next_in = forced[s];
 }
 
+// Injected-spec hook (on the reference's _speculative_set,
+// engine.py:162-168): at a flagged step the target's final argmax -- the
+// forced token of generate_forced -- replaces the last draft id unless it is
+// already among the K ids.  One thread.
+__global__ void inject_spec_kernel(int32_t *spec, int K, const int32_t *forced,
+                                   const int32_t *step, const uint8_t *flags, int n) {
+  if (threadIdx.x != 0) return;
+  const int s = *step;
+  if (s < 0 || s >= n || !flags[s]) return;
+  const int tok = forced[s];
+  for (int k = 0; k < K; ++k)
+    if (spec[k] == tok) return;
+  spec[K - 1] = tok;
+}
+
 }  // namespace spx
 
 using namespace spx;
+
+extern "C" int spx_inject_spec(int32_t *spec_ids, int32_t K, const int32_t *forced,
+                               const int32_t *step, const uint8_t *flags, int64_t n,
+                               void *stream) {
+  if (!spec_ids || !forced || !step || !flags || K < 1 || K > 64 || n < 0) return SPX_EINVAL;
+  inject_spec_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(spec_ids, K, forced, step, flags, (int)n);
+  return spx_launch_status("spx_inject_spec");
+}
 
 extern "C" int spx_topk(const float *logits, int64_t n, int32_t K, int32_t *ids_out,
                         void *stream) {
   if (!logits || !ids_out || n <= 0 || K < 1 || K > 64 || K > n) return SPX_EINVAL;
   topk_kernel<<<1, TOPK_THREADS, 0, (cudaStream_t)stream>>>(logits, (int)n, K, ids_out);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_topk");
 }
 
 extern "C" int spx_token_begin(spx_token_state st, int32_t K, int32_t L, float inv_k,
                                void *stream) {
   if (!st.prev || !st.done || K < 1 || K > 64) return SPX_EINVAL;
   token_begin_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(st, K, L, inv_k);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_token_begin");
 }
 
 extern "C" int spx_token_end(spx_token_state st, spx_online_state os, int32_t L,
@@ -167,18 +190,18 @@ extern "C" int spx_token_end(spx_token_state st, spx_online_state os, int32_t L,
     return SPX_EINVAL;
   token_end_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(st, os, L, queue_len, radius,
                                                        (int)max_steps);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_token_end");
 }
 
 extern "C" int spx_force_next(const int32_t *forced, const int32_t *step, int32_t *next_in,
                               int64_t n_forced, void *stream) {
   if (!forced || !step || !next_in || n_forced < 0) return SPX_EINVAL;
   force_next_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(forced, step, next_in, (int)n_forced);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_force_next");
 }
 
 extern "C" int spx_or_flag(const uint8_t *src, uint8_t *dst, void *stream) {
   if (!src || !dst) return SPX_EINVAL;
   or_flag_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(src, dst);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_or_flag");
 }

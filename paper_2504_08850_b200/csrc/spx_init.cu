@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include "../../include/specexit_b200.h"
+#include "spx_common.cuh"
 
 namespace spx {
 
@@ -50,7 +51,7 @@ extern "C" int spx_init_uniform(void *out, int32_t out_f32, int64_t rows, int64_
   const double span = high - low;   // Python float arithmetic in the reference
   spx::init_uniform_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
       out, out_f32, rows, cols, transpose, seed, low, span);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_init_uniform");
 }
 
 extern "C" const char *spx_version(void) {

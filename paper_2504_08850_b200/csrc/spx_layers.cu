@@ -422,14 +422,19 @@ static void launch_layer(const LayerParams &p, cudaStream_t s) {
     int g = (nout + wpc - 1) / wpc;
     return g < sms ? g : sms;
   };
+  spx_debug_capture(s, "strict layer: entry");
   rows_kernel<<<1, LT, 0, s>>>(p);
+  spx_debug_capture(s, "strict layer: rows");
   qkv_kernel<TW><<<grid_for(3 * p.d), LT, ln_smem, s>>>(p);
+  spx_debug_capture(s, "strict layer: qkv");
   const size_t a_smem = (size_t)wpc * p.max_ctx * sizeof(float);
   attn_kernel<<<sms, LT, a_smem, s>>>(p);
+  spx_debug_capture(s, "strict layer: attn");
   wo_kernel<TW><<<grid_for(p.d), LT, ln_smem, s>>>(p);
   ffn1_kernel<TW><<<grid_for(p.ffn), LT, ln_smem, s>>>(p);
   ffn2_kernel<TW><<<grid_for(p.d), LT, f_smem, s>>>(p);
   finish_kernel<<<1, LT, 0, s>>>(p);
+  spx_debug_capture(s, "strict layer: exit");
 }
 
 extern "C" int spx_layer_forward(const spx_layer_args *a, void *stream) {
@@ -459,7 +464,7 @@ extern "C" int spx_layer_forward(const spx_layer_args *a, void *stream) {
   if (a->w_dtype == SPX_DTYPE_BF16) launch_layer<__nv_bfloat16>(p, s);
   else if (a->w_dtype == SPX_DTYPE_F32) launch_layer<float>(p, s);
   else return SPX_EINVAL;
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_layer_forward");
 }
 
 static int64_t tc_units(int64_t nout, int64_t kin) {
@@ -521,6 +526,7 @@ extern "C" int spx_embed(const void *embedding, int32_t w_dtype, const float *po
       !err || T <= 0 || d <= 0 || d % 4)
     return SPX_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
+  spx_debug_capture(s, "embed: entry");
   const int grid = (int)(T < 1024 ? T : 1024);
   if (w_dtype == SPX_DTYPE_BF16)
     embed_kernel<__nv_bfloat16><<<grid, 128, 0, s>>>((const __nv_bfloat16 *)embedding, pos_encoding,
@@ -534,5 +540,5 @@ extern "C" int spx_embed(const void *embedding, int32_t w_dtype, const float *po
   else
     return SPX_EINVAL;
   embed_commit_kernel<<<1, 1, 0, s>>>((int)T, n_ctx, new_row, (int)max_ctx);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_embed");
 }

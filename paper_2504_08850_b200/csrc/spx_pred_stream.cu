@@ -11,6 +11,6 @@ int launch_stream_bf16(const PredParams &p, const StreamPlan &sp, int grid, cuda
   if (p.d == 2048) L.template operator()<4>();
   else if (p.d == 4096) L.template operator()<8>();
   else L.template operator()<16>();
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_predictor_eval");
 }
 }  // namespace spx

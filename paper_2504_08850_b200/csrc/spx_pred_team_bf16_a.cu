@@ -8,7 +8,7 @@ template <typename TW, int CPL>
 int launch_team_cpl(const PredParams &p, const SmemPlan &sp, int grid, cudaStream_t stream,
                     int smem_optin) {
   FastLaunch<TW>{p, sp, grid, stream, smem_optin}.template operator()<CPL>();
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_predictor_eval");
 }
 template int launch_team_cpl<__nv_bfloat16, 1>(const PredParams &, const SmemPlan &, int, cudaStream_t, int);
 template int launch_team_cpl<__nv_bfloat16, 2>(const PredParams &, const SmemPlan &, int, cudaStream_t, int);

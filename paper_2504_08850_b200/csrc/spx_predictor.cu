@@ -258,7 +258,7 @@ static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cu
       cudaLaunchKernelEx(&cfg, predictor_recheck_kernel<TW>, p);
     }
   }
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_predictor_eval");
 }
 
 template <typename TW>
@@ -317,7 +317,7 @@ static int launch_fast(const PredParams &p0, const spx_predictor_args *a, cudaSt
     const int grid = (int)(need < g_sms ? need : g_sms);
     return launch_team<TW>(p, sp, grid > 0 ? grid : 1, stream, g_smem_optin);
   }
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_predictor_eval");
 }
 
 extern "C" int spx_predictor_eval(const spx_predictor_args *a, void *stream_) {
@@ -365,11 +365,11 @@ extern "C" int spx_extract_features(const float *logits, const float *prev, floa
   if (K > MAXK) {
     features_wide_kernel<<<(unsigned)B, 256, 0, (cudaStream_t)stream>>>(logits, prev, feats_out,
                                                                        err, (int)K);
-    return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+    return spx_launch_status("spx_extract_features");
   }
   features_kernel<<<(unsigned)B, 32, 0, (cudaStream_t)stream>>>(
       logits, const_cast<float *>(prev), feats_out, err, (int)B, (int)K);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_extract_features");
 }
 
 extern "C" int spx_predictor_mlp(const float *feats, const float *w1, const float *b1,
@@ -384,7 +384,7 @@ extern "C" int spx_predictor_mlp(const float *feats, const float *w1, const floa
   p.z_out = z_out; p.prob_out = prob_out; p.fired = fired_out;
   p.B = (int)B; p.K = (int)K; p.H = (int)H;
   mlp_kernel<<<(unsigned)B, 32, 0, (cudaStream_t)stream>>>(p, feats);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_predictor_mlp");
 }
 
 // Tree-node evaluation (tree.py:213-220): live node i's K merged logits (K6
@@ -423,7 +423,7 @@ extern "C" int spx_tree_node_eval(const float *logits, const int32_t *live_idx, 
   p.K = (int)K; p.H = policy == SPX_POLICY_MLP ? (int)H : 0;
   tree_node_eval_kernel<<<(unsigned)n_live, 32, 0, (cudaStream_t)stream>>>(p, logits, live_idx,
                                                                           (int)n_live);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_tree_node_eval");
 }
 
 extern "C" int spx_predictor_cert(const float *w1, const float *b1, const float *w2, int64_t K,
@@ -431,7 +431,7 @@ extern "C" int spx_predictor_cert(const float *w1, const float *b1, const float 
   if (!w1 || !b1 || !w2 || !cert || K < 1 || K > MAXK || H < 1 || H > MAXH) return SPX_EINVAL;
   predictor_cert_kernel<<<(unsigned)(3 * K + 2), 32, 0, (cudaStream_t)stream>>>(w1, b1, w2, (int)K,
                                                                                (int)H, cert);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_predictor_cert");
 }
 
 namespace spx {
@@ -465,5 +465,5 @@ extern "C" int spx_head_stats(const void *head, int32_t head_dtype, int64_t V, i
                                                   wmax);
   else
     return SPX_EINVAL;
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_head_stats");
 }

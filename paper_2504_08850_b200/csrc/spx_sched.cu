@@ -75,7 +75,7 @@ extern "C" int spx_sched_update(spx_online_state st, const int32_t *exit_layer,
   if (B == 0) return 0;
   sched_update_kernel<<<(unsigned)((B + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
       st, exit_layer, gate, (int)B, L, queue_len, radius, err);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_sched_update");
 }
 
 extern "C" int spx_sched_active(spx_online_state st, uint64_t offline_mask, int64_t B, int32_t L,
@@ -84,7 +84,7 @@ extern "C" int spx_sched_active(spx_online_state st, uint64_t offline_mask, int6
   if (B == 0) return 0;
   sched_active_kernel<<<(unsigned)((B + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
       st, offline_mask, (int)B, L, mode, active_out);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_sched_active");
 }
 
 extern "C" int spx_path_and(const uint8_t *node_fired, const int32_t *path_ptr,
@@ -94,7 +94,7 @@ extern "C" int spx_path_and(const uint8_t *node_fired, const int32_t *path_ptr,
   if (P == 0) return 0;
   path_and_kernel<<<(unsigned)((P + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
       node_fired, path_ptr, path_nodes, live, (int)P, path_fire);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_path_and");
 }
 
 // K7b: which rows need the full-head check after the path AND
@@ -122,7 +122,7 @@ extern "C" int spx_tree_gate(const uint8_t *path_fire, const int32_t *path_ptr,
     return SPX_EINVAL;
   spx::tree_gate_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(path_fire, path_ptr, path_nodes,
                                                              (int)P, (int)n_nodes, node_gate);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_tree_gate");
 }
 
 // Elementwise numpy-float32 exp (the softmax's exp, model.py:151), exposed so
@@ -140,5 +140,5 @@ extern "C" int spx_np_expf(const float *x, float *y, int64_t n, void *stream) {
   if (!x || !y || n < 0) return SPX_EINVAL;
   if (n == 0) return 0;
   spx::np_expf_kernel<<<148 * 4, 256, 0, (cudaStream_t)stream>>>(x, y, n);
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_np_expf");
 }

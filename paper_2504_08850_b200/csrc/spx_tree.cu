@@ -126,5 +126,5 @@ extern "C" int spx_tree_merged_logits(const float *xg, const float *r, int64_t N
   else
     return SPX_EINVAL;
   if (!ok) return SPX_EINVAL;
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_tree_merged_logits");
 }

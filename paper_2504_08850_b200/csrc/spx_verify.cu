@@ -346,7 +346,7 @@ static int launch_verify(const VerParams &p, int nchunk, int grid, size_t smem,
   else if (nchunk <= 8 * NPART) SPX_LAUNCH_VER(8);
   else return SPX_EINVAL;
 #undef SPX_LAUNCH_VER
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_verify");
 }
 
 extern "C" int spx_verify(const spx_verify_args *a, void *stream_) {
@@ -390,7 +390,7 @@ extern "C" int spx_final_norm(const float *hidden, int64_t hidden_stride, const 
   if (!dispatch_cpl((int)d, NormLaunch{hidden, st, g, b, hn, nullptr, (int)N, (int)d, mode, 1,
                                        err, grid, wpc * 32, stream}))
     return SPX_EINVAL;
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_final_norm");
 }
 
 extern "C" int spx_head_prep(const float *hidden, int64_t hidden_stride, const float *g,
@@ -405,7 +405,7 @@ extern "C" int spx_head_prep(const float *hidden, int64_t hidden_stride, const f
   if (!dispatch_cpl((int)d, NormLaunch{hidden, st, g, b, xg, r, (int)N, (int)d, mode, 0, err,
                                        grid, wpc * 32, stream}))
     return SPX_EINVAL;
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_head_prep");
 }
 
 extern "C" int spx_head_bias(const void *head, int32_t head_dtype, const float *b, int64_t V,
@@ -422,5 +422,5 @@ extern "C" int spx_head_bias(const void *head, int32_t head_dtype, const float *
   else
     return SPX_EINVAL;
   if (!ok) return SPX_EINVAL;
-  return cudaGetLastError() == cudaSuccess ? 0 : SPX_ECUDA;
+  return spx_launch_status("spx_head_bias");
 }

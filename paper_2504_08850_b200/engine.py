@@ -31,6 +31,7 @@ Any other policy (OraclePolicy, user policies, a bank with missing layers,
 spec_full_vocab) runs the reference's step loop on the host
 (``_host_step``), calling the same device operators one by one.
 """
+import gc
 import json
 from dataclasses import dataclass, field
 
@@ -188,6 +189,7 @@ class _DeviceStep:
         self.rec_fired, self.rec_verified = _u8(cap), _u8(cap)
         self.rec_active = torch.zeros(cap, dtype=torch.int64, device="cuda")
         self.forced = _i32(cap)
+        self.inject = _u8(cap)             # injected-spec flags (generate_forced)
         self.spec_ids = _i32(self.K)
         self.spec_ptr = torch.tensor([0, self.K], dtype=torch.int32, device="cuda")
         self.draft_logits = torch.zeros(dm.vocab_size, dtype=torch.float32, device="cuda")
@@ -239,7 +241,7 @@ class _DeviceStep:
                 a.cert = N._vp(pb.cert[l].data_ptr())
         return a
 
-    def enqueue(self, mode, forced: bool):
+    def enqueue(self, mode, forced: bool, inject: bool = False):
         """Enqueue one token step on the current stream (capturable)."""
         eng = self.eng
         lib = N.lib()
@@ -254,6 +256,10 @@ class _DeviceStep:
                                   mode=mode))
         N.check(lib.spx_topk(N.ptr(self.draft_logits), eng.draft.config.vocab_size, self.K,
                              N.ptr(self.spec_ids), s()), "spx_topk")
+        if inject:
+            N.check(lib.spx_inject_spec(N.ptr(self.spec_ids), self.K, N.ptr(self.forced),
+                                        N.ptr(self.step), N.ptr(self.inject), self.cap, s()),
+                    "spx_inject_spec")
         # schedule
         if eng.config.schedule_mode == "all":
             mask, m = 0, 0
@@ -290,16 +296,26 @@ class _DeviceStep:
             N.check(lib.spx_force_next(N.ptr(self.forced), N.ptr(self.step), N.ptr(self.next_in),
                                        self.cap, s()), "spx_force_next")
 
-    def graph(self, forced: bool):
+    def graph(self, forced: bool, inject: bool = False):
         mode = numerics.mode()
-        key = (mode, forced)
+        key = (mode, forced, inject)
         g = self.graphs.get(key)
         if g is None:
             # host-side preparation (weight packing, z_cut) before capture
             self._pargs = [self._pred_args(l, mode) for l in range(self.L - 1)]
+            # dead engines are reference cycles (engine <-> _DeviceStep) that
+            # may own CUDA graphs; collect them now -- a graph destroyed by a
+            # GC pass DURING capture invalidates the capture
+            gc.collect()
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self.enqueue(mode, forced)
+            was = gc.isenabled()
+            gc.disable()
+            try:
+                with torch.cuda.graph(g):
+                    self.enqueue(mode, forced, inject)
+            finally:
+                if was:
+                    gc.enable()
             self.graphs[key] = g
         return g
 
@@ -415,22 +431,18 @@ class ExitEngine:
             if st.n + n_steps > m.config.max_context:
                 raise ValueError("context overflow")
 
-    def _run_device(self, n, forced=None):
+    def _run_device(self, n, forced=None, inject=None):
         d = self._dev
         self._check_capacity(n)
         if forced is not None:
             d.forced[self._steps:self._steps + n].copy_(
                 torch.as_tensor(np.asarray(forced, np.int32)))
-        g = d.graph(forced is not None)
-        for _ in range(n):
-            g.replay()
-        torch.cuda.synchronize()
-        e = int(d.err.item()) | int(self.tstate.err.item()) | int(self.dstate.err.item())
-        N.raise_device_error(e)
-        recs = d.records(self._steps + n)[self._steps:]
-        for st in (self.tstate, self.dstate):
-            st.n += n
-        self._steps += n
+        if inject is not None:
+            d.inject[self._steps:self._steps + n].copy_(
+                torch.as_tensor(np.asarray(inject, np.uint8)))
+        self.replay_device(n, forced is not None, inject is not None)
+        self.sync_device()
+        recs = d.records(self._steps)[self._steps - n:]
         for r in recs:
             self.context.append(r.token)
         self.next_in = recs[-1].token
@@ -439,13 +451,36 @@ class ExitEngine:
             self.next_in = int(forced[-1])
         return recs
 
-    def _speculative_set(self):
+    def replay_device(self, n, forced: bool = False, inject: bool = False):
+        """Enqueue n token steps (graph replays) without synchronising; the
+        ExitRecord fields accumulate in the device record arrays."""
+        self._check_capacity(n)
+        g = self._dev.graph(forced, inject)
+        for _ in range(n):
+            g.replay()
+        for st in (self.tstate, self.dstate):
+            st.n += n
+        self._steps += n
+
+    def sync_device(self):
+        """Synchronise and raise the reference's error for any device error word."""
+        torch.cuda.synchronize()
+        d = self._dev
+        N.raise_device_error(int(d.err.item()) | int(self.tstate.err.item()) |
+                             int(self.dstate.err.item()))
+
+    def _speculative_set(self, inject_token=None):
         self.dstate.begin([self.next_in])
         for l in range(self.draft.config.num_layers):
             self.dstate.launch_layer(l)
         logits = full_head_logits(self.draft, self.dstate.cur_hidden)
         k = self.target.config.vocab_size if self.config.spec_full_vocab else self.config.k
-        return speculative_set_from_logits(logits, k)
+        spec = speculative_set_from_logits(logits, k)
+        if inject_token is not None and int(inject_token) not in spec.tokens:
+            toks = list(spec.tokens)
+            toks[-1] = int(inject_token)
+            spec = SpeculativeSet(tokens=tuple(toks), draft_probs=spec.draft_probs)
+        return spec
 
     def _active_layers(self):
         L = self.target.config.num_layers
@@ -453,10 +488,10 @@ class ExitEngine:
             return list(range(L - 1))
         return active_layers(self.profile, self.online, self.schedule_config)
 
-    def _host_step(self) -> ExitRecord:
+    def _host_step(self, inject_token=None) -> ExitRecord:
         """engine.py:176-217 with device operators and host decisions."""
         L = self.target.config.num_layers
-        spec = self._speculative_set()
+        spec = self._speculative_set(inject_token)
         active = self._active_layers()
         act = set(active)
         self.policy.observe(self.next_in)
@@ -509,18 +544,27 @@ class ExitEngine:
             trace = [self._host_step() for _ in range(max_new)]
         return [r.token for r in trace], trace
 
-    def generate_forced(self, prompt, forced_tokens):
+    def generate_forced(self, prompt, forced_tokens, inject=None):
         """engine.py:227-246: position-aligned evaluation over a given
-        continuation (normally the full model's greedy stream)."""
+        continuation (normally the full model's greedy stream).
+
+        inject (optional, one bool per step): the injected-spec hook of
+        SURVEY.md §8d C2 on _speculative_set (engine.py:162-168) -- at a
+        flagged step the forced token (the target's final argmax when the
+        continuation is the greedy stream) replaces the last draft id unless
+        it is already speculated.  Not part of the reference API; used to give
+        random-init models a realistic exit-depth distribution."""
         forced_tokens = [int(t) for t in forced_tokens]
         if len(forced_tokens) == 0:
             raise ValueError("empty forced continuation")
+        if inject is not None and len(inject) != len(forced_tokens):
+            raise ValueError("inject needs one flag per forced token")
         self.start(prompt)
         if self._dev is not None and self.device_resident():
-            return self._run_device(len(forced_tokens), forced_tokens)
+            return self._run_device(len(forced_tokens), forced_tokens, inject)
         trace = []
-        for tok in forced_tokens:
-            trace.append(self._host_step())
+        for i, tok in enumerate(forced_tokens):
+            trace.append(self._host_step(tok if inject is not None and inject[i] else None))
             self.context[-1] = tok
             self.next_in = tok
         return trace

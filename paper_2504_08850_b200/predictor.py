@@ -345,7 +345,8 @@ def prev_error(prev: torch.Tensor) -> torch.Tensor:
 
 def evaluate_batch(model, weights, hidden, ids, prev, threshold=0.5, layer=0, outputs=True, pdl=False,
                    row_layer_mask=None, row_done=None, evals=None, err=None, mode=None,
-                   policy=None, out=None, prev_err=None, recheck=None, certify=True):
+                   policy=None, out=None, prev_err=None, recheck=None, certify=True,
+                   feat_out=None):
     """K1+K2+K3 for B rows at one layer in ONE launch (spx_predictor_eval).
 
     model: TransformerModel (head + final norm used); weights: PredictorWeights
@@ -359,7 +360,8 @@ def evaluate_batch(model, weights, hidden, ids, prev, threshold=0.5, layer=0, ou
     follow-up launch of the same call, so ``fired`` is the reference's.
     prev_err (B,) is the error bound carried with ``prev`` (default: attached
     to the prev tensor, see prev_error); recheck the work list (default: one
-    per stream and B, see recheck_buffer).  certify=False turns it off."""
+    per stream and B, see recheck_buffer).  certify=False turns it off.
+    feat_out: optional (B, 3K) f32 tensor receiving the feature vectors."""
     B, d = hidden.shape
     K = ids.shape[1]
     dev = hidden.device
@@ -395,6 +397,7 @@ def evaluate_batch(model, weights, hidden, ids, prev, threshold=0.5, layer=0, ou
         a.policy, a.const_prob, a.threshold, H = N.SPX_POLICY_CONST, float(policy), float(threshold), 0
     a.logits_out, a.z_out, a.prob_out = N.ptr(out.logits), N.ptr(out.z), N.ptr(out.prob)
     a.fired = N.ptr(out.fired)
+    a.feat_out = N.ptr(feat_out)
     a.row_layer_mask, a.row_done, a.evals = N.ptr(row_layer_mask), N.ptr(row_done), N.ptr(evals)
     a.layer = layer
     a.mode = numerics.mode() if mode is None else mode

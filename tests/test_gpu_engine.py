@@ -254,3 +254,82 @@ def test_device_step_graph_replays_without_host_sync(golden):
     b, _ = eng.generate(PROMPT, 8)
     assert a == b
     assert eng._dev.graphs == g and len(g) == 1
+
+
+def _inject_flags(seed, n, p=0.8):
+    u = (spx.rng.splitmix64(seed, n) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    return [bool(x < p) for x in u]
+
+
+def _oracle_engine(oracle, eg_or_cfgs, bank, thr, mode, counts, sc, k=4):
+    tcfg, dcfg = eg_or_cfgs
+    t = oracle.init_model(tcfg, bf16=True)
+    d = oracle.init_model(dcfg, bf16=True)
+    ob = {l: oracle.PredictorWeights(w.w1, w.b1, w.w2, w.b2) for l, w in bank.items()}
+    return oracle.ExitEngineOracle(tcfg, t, dcfg, d, ob, k=k, threshold=thr, schedule_mode=mode,
+                                   exit_counts=counts,
+                                   schedule_config=oracle.ScheduleConfig(*sc))
+
+
+def _orec(r):
+    return (r.token, r.exit_layer, r.predictor_fired, r.verified, list(r.active),
+            r.full_head_count, r.predictor_evals)
+
+
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_injected_spec_forced_matches_oracle(golden, oracle, mode):
+    """The injected-spec hook (at 80% of the steps the
+    target's final argmax joins the draft ids) on the device graph vs the
+    oracle engine with the same hook, record for record."""
+    eg = golden.json("engine_tiny.json")
+    t, d = _engine_models(eg)
+    bank = {l: spx.init_predictor(4, 512, oracle.derive(eg["bank_seed"], l)) for l in range(5)}
+    counts = np.asarray(eg["exit_counts"])
+    prof = spx.OfflineProfile(6, counts, 0)
+    n = 20
+    with numerics.using(mode):
+        base, _ = E.greedy_generate(t, PROMPT, n)
+        flags = _inject_flags(31, n)
+        eng = E.ExitEngine(t, d, E.PredictorPolicy(bank),
+                           E.EngineConfig(k=4, threshold=0.5, schedule_mode="two-level"), prof,
+                           spx.ScheduleConfig(5, 1, 2))
+        got = eng.generate_forced(PROMPT, base, inject=flags)
+        host = E.ExitEngine(t, d, type("P", (E.PredictorPolicy,), {})(bank),
+                            E.EngineConfig(k=4, threshold=0.5, schedule_mode="two-level"), prof,
+                            spx.ScheduleConfig(5, 1, 2))
+        assert not host.device_resident()
+        got_host = host.generate_forced(PROMPT, base, inject=flags)
+    oe = _oracle_engine(oracle, (oracle.ModelConfig(num_layers=6, seed=eg["target_seed"]),
+                                 oracle.ModelConfig(num_layers=2, seed=eg["draft_seed"])),
+                        bank, 0.5, "two-level", counts, (5, 1, 2))
+    want = oe.generate_forced(PROMPT, base, inject=flags)
+    assert [_rec_tuple(r) for r in got] == [_orec(r) for r in want]
+    assert [_rec_tuple(r) for r in got_host] == [_orec(r) for r in want]
+
+
+@pytest.mark.slow
+def test_engine_7b_dims_fast_matches_oracle(oracle):
+    """A 4-layer target / 2-layer draft at Llama2-7B widths (d=4096,
+    ffn=11008, V=32000) in FAST mode (certified predictor decisions, the
+    persistent layer kernel) against the oracle engine: 8 tokens, two-level,
+    thr 0.5, every ExitRecord field equal."""
+    tc = spx.ModelConfig(32000, 4096, 4, 32, 11008, 64, 1234)
+    dc = spx.ModelConfig(32000, 4096, 2, 32, 11008, 64, 1235)
+    t, d = spx.init_model(tc, dtype="bf16"), spx.init_model(dc, dtype="bf16")
+    bank = {l: spx.init_predictor(4, 512, spx.rng.derive(1234, l)) for l in range(3)}
+    counts = np.asarray([5, 1, 3, 0], np.uint64)
+    prof = spx.OfflineProfile(4, counts, 0)
+    prompt = [int(x) % 32000 for x in spx.rng.splitmix64(1234, 6)]
+    with numerics.using("fast"):
+        eng = E.ExitEngine(t, d, E.PredictorPolicy(bank),
+                           E.EngineConfig(k=4, threshold=0.5, schedule_mode="two-level"), prof,
+                           spx.ScheduleConfig(5, 1, 2))
+        assert eng.device_resident()
+        toks, got = eng.generate(prompt, 8)
+    del t, d
+    torch.cuda.empty_cache()
+    oc = lambda c: oracle.ModelConfig(c.vocab_size, c.hidden_dim, c.num_layers,  # noqa: E731
+                                      c.num_heads, c.ffn_dim, c.max_context, c.seed)
+    oe = _oracle_engine(oracle, (oc(tc), oc(dc)), bank, 0.5, "two-level", counts, (5, 1, 2))
+    _, want = oe.generate(prompt, 8)
+    assert [_rec_tuple(r) for r in got] == [_orec(r) for r in want]
