@@ -15,6 +15,7 @@
 // writes the device exit flag.
 #include "spx_common.cuh"
 #include "../../include/specexit_b200.h"
+#include <type_traits>
 
 namespace spx {
 
@@ -268,6 +269,123 @@ verify_kernel(VerParams p) {
   if (threadIdx.x == 0) *p.counter = 0u;
 }
 
+// FAST K4 for ONE row (B == 1: the decode step's gated verify and final
+// argmax).  Same arithmetic as verify_kernel's FAST path (canonical CDOT,
+// folded LayerNorm), so the logits are bit-identical.  Differences are in the
+// schedule only: the gate is read first (a non-firing launch reads nothing
+// from the head); every warp then issues its first vocab row's loads BEFORE
+// the head-side LayerNorm, so the first HBM round trip overlaps the prologue;
+// and the loop keeps the next row's loads in flight behind the current row's
+// butterflies and argmax.  Two CTAs per SM.
+template <typename TW, int CPL>
+__global__ void __launch_bounds__(VER_THREADS, 2)
+verify1_kernel(VerParams p) {
+  const TW *head = reinterpret_cast<const TW *>(p.head);
+  extern __shared__ float hn[];           // d
+  __shared__ float s_r;
+  __shared__ int s_on;
+  __shared__ unsigned long long s_best[VER_THREADS / 32];
+  __shared__ bool s_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = VER_THREADS / 32;
+  if (threadIdx.x == 0) s_on = ver_row_on(p, 0) ? 1 : 0;
+  __syncthreads();
+  const bool on = s_on != 0;
+  const int nchunk = p.d / CHUNK;
+  const int gw = blockIdx.x * nwarps + warp, tw = gridDim.x * nwarps;
+  unsigned long long best = 0ull;
+  if (on) {
+    Chunk<TW> w[4][CPL];
+    float bwn = 0.f;
+    if (gw < p.V) {
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+#pragma unroll
+        for (int s = 0; s < CPL; ++s) {
+          const int c = 32 * g + lane + NPART * s;
+          if (c < nchunk) w[g][s].load(head + (size_t)gw * p.d + CHUNK * c);
+          else w[g][s].zero();
+        }
+      if (p.head_bw) bwn = __ldg(p.head_bw + gw);
+    }
+    if (warp == 0) {
+      int bad = 0;
+      float rr = 1.f;
+      warp_head_prep<CPL>(p.hidden, p.g, p.b, p.d, hn, lane, false, &rr, &bad);
+      if (lane == 0) s_r = rr;
+      if (bad && lane == 0) atomicOr(p.err, ERR_HIDDEN_NONFINITE);
+    }
+    __syncthreads();
+    const float rr = s_r;
+    for (int v = gw; v < p.V;) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};       // canonical partial groups
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+#pragma unroll
+        for (int s = 0; s < CPL; ++s) {
+          const int c = 32 * g + lane + NPART * s;
+          if (c < nchunk) {
+            float wf[4];
+            w[g][s].to_f32(wf);
+            const float4 h = *reinterpret_cast<const float4 *>(hn + CHUNK * c);
+            acc[g] = __fmaf_rn(h.x, wf[0], acc[g]);
+            acc[g] = __fmaf_rn(h.y, wf[1], acc[g]);
+            acc[g] = __fmaf_rn(h.z, wf[2], acc[g]);
+            acc[g] = __fmaf_rn(h.w, wf[3], acc[g]);
+          }
+        }
+      const float bw = bwn;
+      const int vn = v + tw;
+      if (vn < p.V) {                              // next row in flight during the reductions
+#pragma unroll
+        for (int g = 0; g < 4; ++g)
+#pragma unroll
+          for (int s = 0; s < CPL; ++s) {
+            const int c = 32 * g + lane + NPART * s;
+            if (c < nchunk) w[g][s].load(head + (size_t)vn * p.d + CHUNK * c);
+          }
+        if (p.head_bw) bwn = __ldg(p.head_bw + vn);
+      }
+      float gs[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) gs[g] = warp_butterfly_sum(acc[g]);
+      const float lg = __fadd_rn(__fmul_rn(rr, canon_combine(gs[0], gs[1], gs[2], gs[3])), bw);
+      const unsigned long long k = argmax_key(lg, (uint32_t)v);
+      best = k > best ? k : best;
+      if (p.logits_out && lane == 0) p.logits_out[v] = lg;
+      v = vn;
+    }
+    if (lane == 0) s_best[warp] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long b = 0ull;
+      for (int q = 0; q < nwarps; ++q) b = s_best[q] > b ? s_best[q] : b;
+      atomicMax(p.scratch, b);
+    }
+  }
+  // ---- last CTA resolves the argmax token, membership and the exit flag
+  __threadfence();
+  if (threadIdx.x == 0) s_last = (atomicAdd(p.counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  if (on) {
+    const unsigned long long k = atomicExch(p.scratch, 0ull);
+    const int tok = (int)(0xffffffffu - (uint32_t)(k & 0xffffffffull));
+    bool in = false;
+    if (p.spec_ptr)
+      for (int i = p.spec_ptr[0]; i < p.spec_ptr[1]; ++i) in |= (p.spec_ids[i] == tok);
+    p.token_out[0] = tok;
+    if (p.maxlogit_out) p.maxlogit_out[0] = f32_from_order_key((uint32_t)(k >> 32));
+    if (p.verified_out) p.verified_out[0] = in ? 1 : 0;
+    if (p.full_heads) p.full_heads[0] += 1;
+    if (in && p.done_out) {
+      p.done_out[0] = 1;
+      if (p.exit_layer_out) p.exit_layer_out[0] = p.layer;
+    }
+  }
+  *p.counter = 0u;
+}
+
 // Final LayerNorm of N rows into hn (FAST: canonical, STRICT: sequential).
 template <int CPL>
 __global__ void final_norm_kernel(const float *x, int64_t stride, const float *g, const float *b,
@@ -330,11 +448,27 @@ static int num_sms() {
   return g_num_sms;
 }
 
+template <typename TW, int CPL>
+static void launch_verify1(const VerParams &p, cudaStream_t stream) {
+  if constexpr (std::is_same<TW, __nv_bfloat16>::value) {
+    const size_t sm1 = (size_t)p.d * sizeof(float);
+    if (sm1 > 48 * 1024)
+      cudaFuncSetAttribute(verify1_kernel<TW, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sm1);
+    verify1_kernel<TW, CPL><<<2 * num_sms(), VER_THREADS, sm1, stream>>>(p);
+  }
+}
+
 template <typename TW>
 static int launch_verify(const VerParams &p, int nchunk, int grid, size_t smem,
                          cudaStream_t stream) {
+  const bool one = p.B == 1 && p.mode != SPX_MODE_STRICT && std::is_same<TW, __nv_bfloat16>::value;
 #define SPX_LAUNCH_VER(CPL)                                                                    \
   do {                                                                                         \
+    if (one) {                                                                                 \
+      launch_verify1<TW, CPL>(p, stream);                                                      \
+      break;                                                                                   \
+    }                                                                                          \
     if (smem > 48 * 1024)                                                                      \
       cudaFuncSetAttribute(verify_kernel<TW, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            (int)smem);                                                         \
