@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--no-tree", action="store_true")
     ap.add_argument("--decode-tokens", type=int, default=32)
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--fused", action="store_true",
+                    help="one fused K1-K3 launch per layer instead of the split gather/tail form")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU/gloo rehearsal of the N-rank plumbing (no kernels)")
     return ap.parse_args()
@@ -383,7 +385,7 @@ def decode_bench(args, rank, ws, dev):
 
 
 def parity_check(spx, model, bank, bank_w, hidden, ids_all, outs, stream, prev, prev0, B,
-                 rows=64):
+                 rows=64, inter=None):
     """Checker (untimed, rank 0): the decisions and probabilities of the
     benchmarked step against the oracle's reference chain (oracle/, the CPU
     restatement of model.py:298-314 + predictor.py:42-109) on a row sample,
@@ -413,11 +415,17 @@ def parity_check(spx, model, bank, bank_w, hidden, ids_all, outs, stream, prev, 
                 prev.copy_(prev0)
                 spx.prev_error(prev).zero_()
                 fs, ps = [], []
-                for l in range(PRED_LAYERS):
-                    o = spx.evaluate_batch(model, bank, hidden[l], torch.as_tensor(
-                        ids_all[l], device=hidden.device), prev, threshold=thr, layer=l)
-                    fs.append(o.fired)
-                    ps.append(o.prob)
+                ids_d = torch.as_tensor(ids_all, device=hidden.device)
+                if inter is not None:          # the benchmarked (pipelined) form
+                    os_ = spx.evaluate_chain(model, bank, hidden, ids_d, prev, inter,
+                                             list(range(PRED_LAYERS)), threshold=thr)
+                    fs, ps = [o.fired for o in os_], [o.prob for o in os_]
+                else:
+                    for l in range(PRED_LAYERS):
+                        o = spx.evaluate_batch(model, bank, hidden[l], ids_d[l], prev,
+                                               threshold=thr, layer=l)
+                        fs.append(o.fired)
+                        ps.append(o.prob)
             torch.cuda.synchronize()
             fired = torch.stack(fs).cpu().numpy()[:, sel]
             prob = torch.stack(ps).cpu().numpy()[:, sel]
@@ -523,12 +531,25 @@ def main():
     prev_err = spx.prev_error(prev)
     recheck = spx.recheck_buffer(B)
 
+    # PIPELINED split form (default when the shape allows): one
+    # launch per layer = that layer's LM-head gather (K1) + the previous
+    # layer's feature/MLP/decision tail (K2+K3, carries prev), programmatic
+    # dependent launches that never wait for the preceding gather; a final
+    # tail launch for the last layer.  --fused: one fused launch per layer.
+    split = (not args.fused and args.mode == "fast" and
+             spx.predictor.split_supported(model, bank, hidden[0], ids_l[0], prev))
+    inter = torch.zeros((PRED_LAYERS, B, 2 * K + 2), dtype=torch.float32, device=dev)
+
     def step():
         prev.copy_(prev0)                                  # token start: uniform prior
         prev_err.zero_()                                   # ... which is exact
-        for l in range(PRED_LAYERS):
-            spx.evaluate_batch(model, bank, hidden[l], ids_l[l], prev, threshold=THRESHOLD, layer=l,
-                               outputs=False, out=outs[l], pdl=PDL)
+        if not split:
+            for l in range(PRED_LAYERS):
+                spx.evaluate_batch(model, bank, hidden[l], ids_l[l], prev, threshold=THRESHOLD,
+                                   layer=l, outputs=False, out=outs[l], pdl=PDL)
+            return
+        spx.evaluate_chain(model, bank, hidden, ids_l, prev, inter, list(range(PRED_LAYERS)),
+                           threshold=THRESHOLD, outs=outs, recheck=recheck)
 
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
@@ -571,8 +592,8 @@ def main():
     ms_max = shard.max_over_ranks(ms, dev)                # device time, max over ranks
     evals_per_step = PRED_LAYERS * B * ws
     value = evals_per_step * args.steps / (ms_max / 1000.0)
-    launches = PRED_LAYERS * args.steps
-    t_launch = (ms / 1000.0) / launches
+    launches = (PRED_LAYERS + 1 if split else PRED_LAYERS) * args.steps
+    t_launch = (ms / 1000.0) / (PRED_LAYERS * args.steps)    # per layer (the dominant launch)
     bytes_launch = launch_bytes(B, U)
     peaks = {}
     try:
@@ -580,12 +601,19 @@ def main():
     except OSError:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = None                       # ncu dram bytes per launch (profiles/, one capture)
-    try:
-        ncu = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_summary.json")))
-        traffic = ncu["predictor_stream_kernel"]["traffic_bytes"]
-    except (OSError, KeyError, ValueError):
-        pass
+    # ncu dram bytes per launch of the dominant kernel (profiles/, one --set full capture)
+    kname = ("predictor_gather_kernel<d=4096, K=4, 1 team, 4 tail warps> (gather l + tail l-1)"
+             if split else "predictor_stream_kernel<bf16, d=4096, K=4, H=512>")
+    kkey = "predictor_gather_kernel" if split else "predictor_stream_kernel"
+    traffic, traffic_src = None, None
+    for fn in ("r02_ncu_summary.json", "r01_ncu_summary.json"):
+        try:
+            ncu = json.load(open(os.path.join(ROOT, "profiles", fn)))
+            traffic = ncu[kkey]["traffic_bytes"]
+            traffic_src = f"profiles/{fn} (ncu --set full, 1 launch)"
+            break
+        except (OSError, KeyError, ValueError):
+            pass
     achieved = bytes_launch / t_launch / 1e9
 
     fired = torch.stack([o.fired for o in outs]).float().mean().item()
@@ -685,9 +713,9 @@ def main():
                          f"{args.cpu_seconds:.0f}s on {P} forked single-core processes; "
                          f"strict kernel: {kind}"}
         del head_dv
-        if not args.no_parity:
-            parity = parity_check(spx, model, bank, bank_w, hidden, ids_all, outs, stream, prev,
-                                  prev0, B)
+    if rank == 0 and not args.no_parity:
+        parity = parity_check(spx, model, bank, bank_w, hidden, ids_all, outs, stream, prev,
+                              prev0, B, inter=inter if split else None)
 
     if rank == 0:
         line = {
@@ -697,18 +725,21 @@ def main():
             "data": "synthetic (reference splitmix64 init of the 7B head + predictors, bf16 head; "
                     "bf16-valued N(0,1) hidden rows; splitmix64 distinct ids)",
             "config": {"workload": f"predictor path step: {PRED_LAYERS} layers x {B} requests/GPU, "
-                                   f"one fused K1-K3 launch per layer, Llama2-7B head V={V} d={D}, "
+                                   + ("pipelined: per layer one launch = K1 gather of layer l + "
+                                      "K2-K3 tail of layer l-1 (+1 final tail launch)" if split else
+                                      "one fused K1-K3 launch per layer")
+                                   + f", Llama2-7B head V={V} d={D}, "
                                    f"K={K}, H={H}, thr={THRESHOLD}, mode={args.mode}",
                        "batch_per_gpu": B, "layers_per_step": PRED_LAYERS, "k": K,
                        "predictor_hidden": H, "unique_ids_per_launch": U,
                        "l2": "no flush: inputs exceed the 126 MB L2 (520 MB of hidden rows per step, "
                              "distinct speculative ids per layer launch over the 262 MB head)",
                        "parallelism": f"dp{ws} (request sharding, no hot-path collective)",
-                       "cuda_graph": True, "pdl": PDL},
+                       "cuda_graph": True, "pdl": 3 if split else PDL, "split": split},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
-                         "traffic_source": "profiles/r01_ncu_summary.json (ncu --set full, 1 launch)",
-                         "kernel": "predictor_stream_kernel<bf16, d=4096, K=4, H=512>",
+                         "traffic_source": traffic_src,
+                         "kernel": kname,
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "us_per_launch": t_launch * 1e6,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},

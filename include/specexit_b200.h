@@ -117,6 +117,32 @@ typedef struct {
 } spx_predictor_args;
 int spx_predictor_eval(const spx_predictor_args *args, void *stream);
 
+/* SPLIT form of spx_predictor_eval for large batches (FAST mode, bf16 head,
+ * K <= 8, d in {2048, 4096, 8192}; spx_predictor_split_ok tells): the same
+ * outputs, bit for bit, from two launches --
+ *   spx_predictor_gather: LayerNorm + K-row gather + local logits (K1) into
+ *     inter (B, 2K + 2) f32 = {local logits, wmax[id], lnf, flags}; reads neither
+ *     prev nor the predictor.  args->pdl = 3: the inputs are not written by
+ *     the preceding kernel, so consecutive gathers overlap (programmatic
+ *     dependent launch, no griddepcontrol.wait).
+ *   spx_predictor_tail: features + MLP + decision + certification (K2+K3)
+ *     from inter; carries prev.  May run on another stream, concurrently
+ *     with the next layer's gather.
+ * Replaces the same reference chain as spx_predictor_eval
+ * (src/specexit/model.py:298-314, src/specexit/predictor.py:42-109). */
+int spx_predictor_split_ok(const spx_predictor_args *args);
+int spx_predictor_gather(const spx_predictor_args *args, float *inter, void *stream);
+int spx_predictor_tail(const spx_predictor_args *args, const float *inter, void *stream);
+/* PIPELINED split form: ONE launch = the gather of `args` (layer l, into
+ * inter) + the tail of `tail_args` (layer l-1, from tail_inter), the tail
+ * warps starting once the preceding launch (layer l-1's gather) completes.
+ * A chain gather(0), gather_tail(1, 0), ..., gather_tail(L-1, L-2),
+ * tail(L-1) evaluates L layers with the prev chain carried and every gather
+ * overlapping its neighbours (always programmatic dependent launch). */
+int spx_predictor_gather_tail(const spx_predictor_args *args, float *inter,
+                              const spx_predictor_args *tail_args, const float *tail_inter,
+                              void *stream);
+
 /* Per-layer constants of the certification bound for one predictor:
  * cert[i] = sum_j |w2[j]| |w1[i][j]| (i < 3K), cert[3K] = sum_j |w2[j] b1[j]|,
  * cert[3K+1] = sum_j |w2[j]|. */

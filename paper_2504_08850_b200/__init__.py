@@ -9,7 +9,8 @@ from .model import (LN_EPS, ModelConfig, TransformerModel, final_norm, from_tens
                     full_head_logits, head_argmax, init_model, layer_norm, load_weights,
                     sliced_head_logits, tensor_specs)
 from .predictor import (FeatureVector, PredictorBank, PredictorWeights, decide_exit,  # noqa: F401
-                        evaluate_batch, extract_features, init_predictor, load_predictors,
+                        evaluate_batch, evaluate_batch_split, evaluate_chain, extract_features, init_predictor,
+                        load_predictors,
                         predictor_forward, predictor_param_count, prev_error,
                         recheck_buffer, recheck_stats, save_predictors, uniform_probs, z_cut)
 from .scheduler import (OfflineProfile, OnlineState, ScheduleConfig, active_layers,  # noqa: F401

@@ -126,6 +126,11 @@ def lib():
     L.spx_token_end.argtypes = [TokenStateC, OnlineStateC, _i32, _i32, _i32, _i64, _vp]
     L.spx_or_flag.argtypes = [_vp, _vp, _vp]
     L.spx_force_next.argtypes = [_vp, _vp, _vp, _i64, _vp]
+    L.spx_predictor_split_ok.argtypes = [ctypes.POINTER(PredictorArgs)]
+    L.spx_predictor_gather.argtypes = [ctypes.POINTER(PredictorArgs), _vp, _vp]
+    L.spx_predictor_tail.argtypes = [ctypes.POINTER(PredictorArgs), _vp, _vp]
+    L.spx_predictor_gather_tail.argtypes = [ctypes.POINTER(PredictorArgs), _vp,
+                                            ctypes.POINTER(PredictorArgs), _vp, _vp]
     L.spx_inject_spec.argtypes = [_vp, _i32, _vp, _vp, _vp, _i64, _vp]
     L.spx_predictor_cert.argtypes = [_vp, _vp, _vp, _i64, _i64, _vp, _vp]
     L.spx_head_stats.argtypes = [_vp, _i32, _i64, _i64, _vp, _vp]

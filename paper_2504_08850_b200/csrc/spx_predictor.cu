@@ -320,8 +320,7 @@ static int launch_fast(const PredParams &p0, const spx_predictor_args *a, cudaSt
   return spx_launch_status("spx_predictor_eval");
 }
 
-extern "C" int spx_predictor_eval(const spx_predictor_args *a, void *stream_) {
-  cudaStream_t stream = (cudaStream_t)stream_;
+static int params_from_args(const spx_predictor_args *a, PredParams &p) {
   if (!a) return SPX_EINVAL;
   if (a->B < 0 || a->d <= 0 || a->d % CHUNK || a->V <= 0 || a->K < 1 || a->K > MAXK ||
       (a->policy == SPX_POLICY_MLP && (a->H < 1 || a->H > MAXH)))
@@ -330,8 +329,7 @@ extern "C" int spx_predictor_eval(const spx_predictor_args *a, void *stream_) {
     return SPX_EINVAL;
   if (a->policy == SPX_POLICY_MLP && (!a->w1 || !a->b1 || !a->w2)) return SPX_EINVAL;
   if (a->hidden_stride % CHUNK) return SPX_EINVAL;
-  if (a->B == 0) return 0;
-  PredParams p;
+  p = PredParams{};
   p.hidden = a->hidden; p.hidden_stride = a->hidden_stride ? a->hidden_stride : a->d;
   p.norm_g = a->norm_g; p.norm_b = a->norm_b;
   p.head = a->head; p.head_bw = a->head_bw;
@@ -353,9 +351,74 @@ extern "C" int spx_predictor_eval(const spx_predictor_args *a, void *stream_) {
   if (p.recheck && (!a->head_wmax || !a->prev_err ||
                     (a->policy == SPX_POLICY_MLP && !a->cert)))
     return SPX_EINVAL;
+  return 0;
+}
+
+extern "C" int spx_predictor_eval(const spx_predictor_args *a, void *stream_) {
+  cudaStream_t stream = (cudaStream_t)stream_;
+  PredParams p;
+  const int rc = params_from_args(a, p);
+  if (rc) return rc;
+  if (a->B == 0) return 0;
   if (a->head_dtype == SPX_DTYPE_F32) return launch_predictor<float>(p, a, stream);
   if (a->head_dtype == SPX_DTYPE_BF16) return launch_predictor<__nv_bfloat16>(p, a, stream);
   return SPX_EINVAL;
+}
+
+// SPLIT path (spx_pred_split.cu): K1 gather -> inter, then K2+K3 tail.
+namespace spx {
+bool split_supported(const PredParams &p, int head_dtype);
+int launch_split_gather(const PredParams &p, float *inter, const PredParams *pt,
+                        const float *inter_t, cudaStream_t s);
+int launch_split_tail(const PredParams &p, const float *inter, cudaStream_t s);
+}  // namespace spx
+
+extern "C" int spx_predictor_split_ok(const spx_predictor_args *a) {
+  PredParams p;
+  if (params_from_args(a, p)) return 0;
+  return a->mode == SPX_MODE_FAST && split_supported(p, a->head_dtype) ? 1 : 0;
+}
+
+extern "C" int spx_predictor_gather(const spx_predictor_args *a, float *inter, void *stream) {
+  PredParams p;
+  const int rc = params_from_args(a, p);
+  if (rc) return rc;
+  if (!inter || a->mode != SPX_MODE_FAST || !split_supported(p, a->head_dtype)) return SPX_EINVAL;
+  if (a->B == 0) return 0;
+  p.pdl = a->pdl < 0 || a->pdl > 3 ? 0 : a->pdl;
+  const int r = launch_split_gather(p, inter, nullptr, nullptr, (cudaStream_t)stream);
+  if (r) return r;
+  return spx_launch_status("spx_predictor_gather");
+}
+
+extern "C" int spx_predictor_gather_tail(const spx_predictor_args *a, float *inter,
+                                         const spx_predictor_args *t, const float *inter_t,
+                                         void *stream) {
+  PredParams p, pt;
+  int rc = params_from_args(a, p);
+  if (rc) return rc;
+  rc = params_from_args(t, pt);
+  if (rc) return rc;
+  if (!inter || !inter_t || a->mode != SPX_MODE_FAST || t->mode != SPX_MODE_FAST ||
+      !split_supported(p, a->head_dtype) || !split_supported(pt, t->head_dtype) || p.B != pt.B)
+    return SPX_EINVAL;
+  if (a->B == 0) return 0;
+  p.pdl = 3;
+  const int r = launch_split_gather(p, inter, &pt, inter_t, (cudaStream_t)stream);
+  if (r) return r;
+  return spx_launch_status("spx_predictor_gather_tail");
+}
+
+extern "C" int spx_predictor_tail(const spx_predictor_args *a, const float *inter, void *stream) {
+  PredParams p;
+  const int rc = params_from_args(a, p);
+  if (rc) return rc;
+  if (!inter || a->mode != SPX_MODE_FAST || !split_supported(p, a->head_dtype)) return SPX_EINVAL;
+  if (a->B == 0) return 0;
+  p.pdl = 0;
+  const int r = launch_split_tail(p, inter, (cudaStream_t)stream);
+  if (r) return r;
+  return spx_launch_status("spx_predictor_tail");
 }
 
 extern "C" int spx_extract_features(const float *logits, const float *prev, float *feats_out,

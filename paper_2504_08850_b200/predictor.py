@@ -362,6 +362,15 @@ def evaluate_batch(model, weights, hidden, ids, prev, threshold=0.5, layer=0, ou
     to the prev tensor, see prev_error); recheck the work list (default: one
     per stream and B, see recheck_buffer).  certify=False turns it off.
     feat_out: optional (B, 3K) f32 tensor receiving the feature vectors."""
+    a, out = _batch_args(model, weights, hidden, ids, prev, threshold, layer, outputs, pdl,
+                         row_layer_mask, row_done, evals, err, mode, policy, out, prev_err,
+                         recheck, certify, feat_out)
+    N.check(N.lib().spx_predictor_eval(a, N.stream_ptr()), "spx_predictor_eval")
+    return out
+
+
+def _batch_args(model, weights, hidden, ids, prev, threshold, layer, outputs, pdl, row_layer_mask,
+                row_done, evals, err, mode, policy, out, prev_err, recheck, certify, feat_out):
     B, d = hidden.shape
     K = ids.shape[1]
     dev = hidden.device
@@ -412,5 +421,76 @@ def evaluate_batch(model, weights, hidden, ids, prev, threshold=0.5, layer=0, ou
         a.recheck = N.ptr(out.recheck)
     elif a.mode == N.SPX_MODE_STRICT:
         a.prev_err = N.ptr(prev_err if prev_err is not None else prev_error(prev))
-    N.check(N.lib().spx_predictor_eval(a, N.stream_ptr()), "spx_predictor_eval")
+    return a, out
+
+
+def split_supported(model, weights, hidden, ids, prev, policy=None, mode=None) -> bool:
+    """True when the SPLIT form (spx_predictor_gather + spx_predictor_tail)
+    serves this shape: FAST mode, bf16 head, K <= 8, d in {2048, 4096, 8192}."""
+    a, _ = _batch_args(model, weights, hidden, ids, prev, 0.5, 0, False, False, None, None, None,
+                       None, mode, policy, None, None, None, True, None)
+    return bool(N.lib().spx_predictor_split_ok(a))
+
+
+def evaluate_batch_split(model, weights, hidden, ids, prev, inter, threshold=0.5, layer=0,
+                         outputs=True, pdl=3, tail_stream=None, row_layer_mask=None,
+                         row_done=None, evals=None, err=None, policy=None, out=None,
+                         prev_err=None, recheck=None, certify=True, feat_out=None):
+    """evaluate_batch in its SPLIT form for large batches (same outputs, bit
+    for bit): K1 (LayerNorm + gather + local logits) into ``inter`` (B, 2K+2)
+    f32 on the current stream, then K2+K3 (features, MLP, decision,
+    certification; carries ``prev``) on ``tail_stream`` (default: the current
+    stream) after an event.  pdl=3: this layer's hidden rows and ids are not
+    written by the kernel launched just before (e.g. the previous layer's
+    gather), so consecutive gathers overlap.  No host sync; capturable."""
+    a, out = _batch_args(model, weights, hidden, ids, prev, threshold, layer, outputs, False,
+                         row_layer_mask, row_done, evals, err, N.SPX_MODE_FAST, policy, out,
+                         prev_err, recheck, certify, feat_out)
+    a.pdl = int(pdl)
+    lib = N.lib()
+    N.check(lib.spx_predictor_gather(a, N.ptr(inter), N.stream_ptr()), "spx_predictor_gather")
+    if tail_stream is None:
+        N.check(lib.spx_predictor_tail(a, N.ptr(inter), N.stream_ptr()), "spx_predictor_tail")
+        return out
+    ev = torch.cuda.Event()
+    ev.record()
+    tail_stream.wait_event(ev)
+    with torch.cuda.stream(tail_stream):
+        N.check(lib.spx_predictor_tail(a, N.ptr(inter), N.stream_ptr()), "spx_predictor_tail")
     return out
+
+
+def evaluate_chain(model, weights, hidden, ids, prev, inter, layers, threshold=0.5, outs=None,
+                   policy=None, prev_err=None, recheck=None, certify=True, feat_out=None):
+    """Several layers' predictor evaluations over the same B rows, ``prev``
+    carried from layer to layer (the token's layer loop of engine.py:192-207
+    for B independent requests whose hidden rows of every listed layer are
+    already resident), in the PIPELINED split form: gather(layers[0]), then
+    per further layer ONE launch = that layer's gather + the previous layer's
+    tail, then the last layer's tail -- so every LM-head gather overlaps its
+    neighbours and no per-row MLP tail sits on the bandwidth-bound path.
+    hidden[i] / ids[i] / inter[i] / outs[i] / feat_out[i] belong to
+    layers[i]; inter: (len(layers), B, 2K+2) f32.  FAST mode, shapes of
+    split_supported.  Same outputs, bit for bit, as evaluate_batch per layer.
+    No host sync; capturable."""
+    n = len(layers)
+    if outs is None:
+        outs = [None] * n
+    args = []
+    for i, l in enumerate(layers):
+        a, o = _batch_args(model, weights, hidden[i], ids[i], prev, threshold, l, outs[i] is None,
+                           False, None, None, None, None, N.SPX_MODE_FAST, policy, outs[i],
+                           prev_err, recheck, certify, None if feat_out is None else feat_out[i])
+        a.pdl = 3
+        args.append(a)
+        outs[i] = o
+    lib = N.lib()
+    st = N.stream_ptr()
+    N.check(lib.spx_predictor_gather(args[0], N.ptr(inter[0]), st), "spx_predictor_gather")
+    for i in range(1, n):
+        N.check(lib.spx_predictor_gather_tail(args[i], N.ptr(inter[i]), args[i - 1],
+                                              N.ptr(inter[i - 1]), st),
+                "spx_predictor_gather_tail")
+    args[-1].pdl = 0
+    N.check(lib.spx_predictor_tail(args[-1], N.ptr(inter[n - 1]), st), "spx_predictor_tail")
+    return outs

@@ -16,6 +16,7 @@
 #   layer       scripts/prof_layer.py --layers 4 --steps 16
 #   launches    ncu launch list of the predictor bench leg
 #   ncupred     ncu --set full of one predictor_stream launch (B=1024)
+#   ncugather   ncu --set full of one pipelined gather launch (B=1024)
 #   ncuverify   ncu --set full of one verify launch (1 row, 7B head)
 #   ncutree     ncu --set full of one tree-merged launch
 #   nculayer    ncu --set full of one layer_mega launch
@@ -48,6 +49,8 @@ for stage in "$@"; do
     launches) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 300 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-decode > gpurun_out/${TAG}_launches.log 2>&1; note launches $? ;;
     ncupred) B=1024 ITERS=8 timeout 600 ncu --set full --clock-control none --import-source on -k regex:predictor_stream -s 4 -c 1 -o gpurun_out/${TAG}_ncu_pred -f python scripts/prof_predictor.py > gpurun_out/${TAG}_ncu_pred.log 2>&1; note ncupred $?
              ncu_csv gpurun_out/${TAG}_ncu_pred.ncu-rep ;;
+    ncugather) CHAIN=1 B=1024 ITERS=6 timeout 600 ncu --set full --clock-control none --import-source on -k regex:predictor_gather -s 6 -c 1 -o gpurun_out/${TAG}_ncu_gather -f python scripts/prof_predictor.py > gpurun_out/${TAG}_ncu_gather.log 2>&1; note ncugather $?
+             ncu_csv gpurun_out/${TAG}_ncu_gather.ncu-rep ;;
     ncuverify) timeout 600 ncu --set full --clock-control none --import-source on -k regex:verify -s 3 -c 1 -o gpurun_out/${TAG}_ncu_verify -f python scripts/prof_kernels.py verify > gpurun_out/${TAG}_ncu_verify.log 2>&1; note ncuverify $?
                ncu_csv gpurun_out/${TAG}_ncu_verify.ncu-rep ;;
     ncutree) timeout 600 ncu --set full --clock-control none --import-source on -k regex:tree_merged -s 3 -c 1 -o gpurun_out/${TAG}_ncu_tree -f python scripts/prof_kernels.py tree > gpurun_out/${TAG}_ncu_tree.log 2>&1; note ncutree $?

@@ -16,9 +16,17 @@ bank = spx.PredictorBank({l: spx.init_predictor(K, 512, rng.derive(1234, 100 + l
 hidden = torch.randn((4, B, 4096), device="cuda").to(torch.bfloat16).float()
 ids = torch.randint(0, 32000, (B, K), device="cuda", dtype=torch.int32)
 prev = torch.full((B, K), 1.0 / K, device="cuda")
+inter = torch.zeros((4, B, 2 * K + 2), device="cuda")
+ids4 = torch.stack([torch.randperm(32000, device="cuda")[:B * K].reshape(B, K).int()
+                    for _ in range(4)])
 for it in range(int(os.environ.get("ITERS", "6"))):
     prev.fill_(1.0 / K)
-    out = spx.evaluate_batch(m, bank, hidden[it % 4], ids, prev, threshold=0.7, layer=it % 4,
-                             outputs=False)
+    if os.environ.get("CHAIN", "0") == "1":
+        # the pipelined chain of the bench (gather l + tail l-1 per launch)
+        out = spx.evaluate_chain(m, bank, hidden, ids4, prev, inter, [0, 1, 2, 3],
+                                 threshold=0.7)[-1]
+    else:
+        out = spx.evaluate_batch(m, bank, hidden[it % 4], ids, prev, threshold=0.7,
+                                 layer=it % 4, outputs=False)
 torch.cuda.synchronize()
 print("ok", out.err.item())
