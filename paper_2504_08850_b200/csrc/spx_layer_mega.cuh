@@ -43,7 +43,7 @@ constexpr int MG_CW = 16;                       // consumer warps
 constexpr int MG_T = 32 * (MG_CW + 1);          // + producer warp
 constexpr int MG_CT = 32 * MG_CW;               // consumer threads
 constexpr int MG_NRP = 2;                       // input rows per pass
-constexpr int MG_CPT = 3;                       // max 8-element chunks per thread (kin <= 12288)
+constexpr int MG_CPT = 4;                       // max 8-element chunks per thread (kin <= 16384: Llama2-13B ffn 13824)
 constexpr int MG_STAGE = 48 * 1024;             // max bytes per ring slot
 constexpr int MG_RMAX = 8;                      // max weight rows per stage
 constexpr int MG_SLOTS = 4;
@@ -625,7 +625,8 @@ static bool launch_layer_mega(const LayerParams &p, int sms, cudaStream_t s) {
   if (cd == 1 && cf == 2) return go(layer_mega_kernel<1, 2>);
   if (cd == 1 && cf == 3) return go(layer_mega_kernel<1, 3>);
   if (cd == 2 && cf == 2) return go(layer_mega_kernel<2, 2>);
-  return go(layer_mega_kernel<2, 3>);
+  if (cd == 2 && cf == 3) return go(layer_mega_kernel<2, 3>);
+  return go(layer_mega_kernel<2, 4>);                // Llama2-13B: d = 5120, ffn = 13824
 }
 
 extern "C" void spx_debug_mega_trace(void *host_out) {

@@ -410,11 +410,11 @@ static void launch_layer(const LayerParams &p, cudaStream_t s) {
   const size_t f_smem = (size_t)RMAX * (p.ffn > p.d ? p.ffn : p.d) * sizeof(float);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(qkv_kernel<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(wo_kernel<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(ffn1_kernel<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(ffn2_kernel<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(qkv_kernel<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
+    cudaFuncSetAttribute(wo_kernel<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
+    cudaFuncSetAttribute(ffn1_kernel<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
+    cudaFuncSetAttribute(ffn2_kernel<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
+    cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024);
     configured = true;
   }
   const int wpc = LT / 32;
@@ -444,8 +444,8 @@ extern "C" int spx_layer_forward(const spx_layer_args *a, void *stream) {
   if (a->d <= 0 || a->d % 8 || a->n_heads <= 0 || a->d % a->n_heads || (a->d / a->n_heads) % 4 ||
       a->ffn <= 0 || a->ffn % 4 || a->max_ctx <= 0)
     return SPX_EINVAL;
-  if ((size_t)RMAX * (a->ffn > a->d ? a->ffn : a->d) * 4 > 200 * 1024 ||
-      (size_t)(LT / 32) * a->max_ctx * 4 > 200 * 1024)
+  if ((size_t)RMAX * (a->ffn > a->d ? a->ffn : a->d) * 4 > 225 * 1024 ||
+      (size_t)(LT / 32) * a->max_ctx * 4 > 225 * 1024)
     return SPX_EINVAL;
   LayerParams p;
   p.ln1_g = a->ln1_g; p.ln1_b = a->ln1_b; p.ln2_g = a->ln2_g; p.ln2_b = a->ln2_b;

@@ -450,7 +450,7 @@ static int num_sms() {
 
 template <typename TW, int CPL>
 static void launch_verify1(const VerParams &p, cudaStream_t stream) {
-  if constexpr (std::is_same<TW, __nv_bfloat16>::value) {
+  if constexpr (std::is_same<TW, __nv_bfloat16>::value && CPL <= 8) {
     const size_t sm1 = (size_t)p.d * sizeof(float);
     if (sm1 > 48 * 1024)
       cudaFuncSetAttribute(verify1_kernel<TW, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -462,7 +462,8 @@ static void launch_verify1(const VerParams &p, cudaStream_t stream) {
 template <typename TW>
 static int launch_verify(const VerParams &p, int nchunk, int grid, size_t smem,
                          cudaStream_t stream) {
-  const bool one = p.B == 1 && p.mode != SPX_MODE_STRICT && std::is_same<TW, __nv_bfloat16>::value;
+  const bool one = p.B == 1 && p.mode != SPX_MODE_STRICT &&
+                   std::is_same<TW, __nv_bfloat16>::value && nchunk <= 8 * NPART;
 #define SPX_LAUNCH_VER(CPL)                                                                    \
   do {                                                                                         \
     if (one) {                                                                                 \
@@ -478,6 +479,7 @@ static int launch_verify(const VerParams &p, int nchunk, int grid, size_t smem,
   else if (nchunk <= 2 * NPART) SPX_LAUNCH_VER(2);
   else if (nchunk <= 4 * NPART) SPX_LAUNCH_VER(4);
   else if (nchunk <= 8 * NPART) SPX_LAUNCH_VER(8);
+  else if (nchunk <= 16 * NPART) SPX_LAUNCH_VER(16);     // d <= 8192 (e.g. Llama2-13B 5120)
   else return SPX_EINVAL;
 #undef SPX_LAUNCH_VER
   return spx_launch_status("spx_verify");

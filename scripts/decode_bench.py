@@ -13,6 +13,9 @@ from paper_2504_08850_b200 import engine as E
 from paper_2504_08850_b200 import numerics, rng
 
 
+SHAPES = {"7b": (4096, 11008, 32, 32), "13b": (5120, 13824, 40, 40)}   # d, ffn, heads, layers
+
+
 def c2_models(seed=1234, layers=32, draft_layers=2, d=4096, ffn=11008, heads=32, V=32000):
     tc = spx.ModelConfig(V, d, layers, heads, ffn, 512, seed)
     dc = spx.ModelConfig(V, d, draft_layers, heads, ffn, 512, seed + 1)
@@ -32,7 +35,8 @@ def c2_engine(t, d, seed=1234, thr=0.5, mode="two-level", k=4):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--model", default="7b", choices=sorted(SHAPES))
+    ap.add_argument("--layers", type=int, default=0, help="0: the model's own depth")
     ap.add_argument("--tokens", type=int, default=64)
     ap.add_argument("--thr", type=float, default=0.5)
     ap.add_argument("--mode", default="two-level")
@@ -40,7 +44,8 @@ def main():
     args = ap.parse_args()
     numerics.set_mode(args.numerics)
     t0 = time.time()
-    t, d = c2_models(layers=args.layers)
+    dd, ff, hh, ll = SHAPES[args.model]
+    t, d = c2_models(layers=args.layers or ll, d=dd, ffn=ff, heads=hh)
     eng = c2_engine(t, d, thr=args.thr, mode=args.mode)
     torch.cuda.synchronize()
     print(f"init {time.time() - t0:.1f}s", flush=True)
@@ -70,7 +75,8 @@ def main():
     print(json.dumps({"tok_s": args.tokens / (ms / 1e3), "ms_per_tok": ms / args.tokens,
                       "e2e_tok_s": e2e, "avg_exit_layer": float(el), "fire_tok_frac": float(fires),
                       "verified_frac": float(ver), "evals_per_tok": float(evals),
-                      "full_heads_per_tok": float(heads), "layers": args.layers}))
+                      "full_heads_per_tok": float(heads), "layers": t.config.num_layers,
+                      "model": args.model}))
 
 
 if __name__ == "__main__":

@@ -43,7 +43,7 @@ for stage in "$@"; do
     pred) timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --no-decode ${BENCH_ARGS:-} > gpurun_out/${TAG}_pred.json 2> gpurun_out/${TAG}_pred.err; note pred $? ;;
     sweep) timeout 1200 python scripts/predictor_sweep.py > gpurun_out/${TAG}_sweep.jsonl 2> gpurun_out/${TAG}_sweep.err; note sweep $? ;;
     decode) timeout 900 python scripts/decode_bench.py --tokens 64 > gpurun_out/${TAG}_decode.log 2>&1; note decode $?
-            timeout 900 python scripts/decode_bench.py --tokens 64 --inject 0.8 > gpurun_out/${TAG}_decode_inject.log 2>&1; note decode_inject $? ;;
+            timeout 900 python scripts/decode_bench.py --tokens 32 --model 13b > gpurun_out/${TAG}_decode_13b.log 2>&1; note decode_13b $? ;;
     tree) timeout 900 python scripts/tree_bench.py --steps 4 > gpurun_out/${TAG}_tree.log 2>&1; note tree $? ;;
     layer) timeout 600 python scripts/prof_layer.py --layers 4 --steps 16 > gpurun_out/${TAG}_layer.log 2>&1; note layer $? ;;
     launches) timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 300 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-decode > gpurun_out/${TAG}_launches.log 2>&1; note launches $? ;;

@@ -60,7 +60,8 @@ def test_decode_state_lazy_completion(oracle, mode):
         assert list(fr) == list(ref.frontier[:ref.n])
 
 
-@pytest.mark.parametrize("dims", [(1024, 2816, 8), (4096, 11008, 32), (512, 1376, 4)])
+@pytest.mark.parametrize("dims", [(1024, 2816, 8), (4096, 11008, 32), (512, 1376, 4),
+                                  (5120, 13824, 40)])
 def test_fast_layers_match_strict(dims):
     """The TMA-streamed FAST layer kernels (every contraction width class:
     1..3 chunks per thread) against the STRICT reference-order kernels, with
