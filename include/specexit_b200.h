@@ -226,6 +226,19 @@ int spx_tree_merged_logits(const float *xg, const float *r, int64_t N, const voi
                            const int32_t *uniq, int64_t U, const int32_t *uniq_ptr,
                            const int32_t *pair_node, const int32_t *pair_out, float *logits,
                            int32_t mode, int32_t *err, void *stream);
+/* K6 on the tensor cores (tcgen05.mma kind::f16, TMEM accumulators) for DENSE
+ * node x unique-id tiles: the same pairs / outputs as spx_tree_merged_logits
+ * (FAST mode; pair_uid[q] = the unique-id index of pair q, the CSR row), with xg split exactly into three bf16 parts so every product
+ * is exact; only the accumulation order differs from the CUDA-core CDOT.
+ * bf16 head, d % 64 == 0.  P = number of pairs; scratch: at least
+ * spx_tree_tc_scratch_bytes(N, d, U, P) bytes (no initialisation needed). */
+int64_t spx_tree_tc_scratch_bytes(int64_t N, int64_t d, int64_t U, int64_t P);
+int spx_tree_merged_logits_tc(const float *xg, const float *r, int64_t N, const void *head,
+                              int32_t head_dtype, const float *head_bw, int64_t V, int64_t d,
+                              const int32_t *uniq, int64_t U, const int32_t *uniq_ptr,
+                              const int32_t *pair_node, const int32_t *pair_out,
+                              const int32_t *pair_uid, int64_t P, float *logits, void *scratch,
+                              int32_t *err, void *stream);
 /* Head-side normalisation of N rows for K6: FAST -> xg = (x-mean)*g and
  * r = 1/sqrt(var+eps) per row (canonical order); STRICT -> xg = the
  * reference LayerNorm (model.py:140-146), r = 1. */

@@ -131,6 +131,10 @@ def lib():
     L.spx_predictor_tail.argtypes = [ctypes.POINTER(PredictorArgs), _vp, _vp]
     L.spx_predictor_gather_tail.argtypes = [ctypes.POINTER(PredictorArgs), _vp,
                                             ctypes.POINTER(PredictorArgs), _vp, _vp]
+    L.spx_tree_tc_scratch_bytes.argtypes = [_i64, _i64, _i64, _i64]
+    L.spx_tree_tc_scratch_bytes.restype = _i64
+    L.spx_tree_merged_logits_tc.argtypes = [_vp, _vp, _i64, _vp, _i32, _vp, _i64, _i64, _vp, _i64,
+                                            _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp]
     L.spx_inject_spec.argtypes = [_vp, _i32, _vp, _vp, _vp, _i64, _vp]
     L.spx_predictor_cert.argtypes = [_vp, _vp, _vp, _i64, _i64, _vp, _vp]
     L.spx_head_stats.argtypes = [_vp, _i32, _i64, _i64, _vp, _vp]

@@ -320,9 +320,33 @@ def head_prep(model: TransformerModel, hidden):
     return xg, r
 
 
-def merged_logits(model: TransformerModel, prep, id_lists) -> list:
+# K6 on the tensor cores when the merged node x unique-id tile is a real dense
+# contraction (north-star (e)): at least TC_MIN_ROWS nodes and TC_MIN_UNIQUE
+# unique ids with a requested fraction >= TC_MIN_DENSITY of the dense tile.
+TC_MIN_ROWS, TC_MIN_UNIQUE, TC_MIN_DENSITY = 64, 64, 0.25
+_TC_SCRATCH = {}
+
+
+def _tc_scratch(nbytes):
+    key = torch.cuda.current_device()
+    buf = _TC_SCRATCH.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device="cuda")
+        _TC_SCRATCH[key] = buf
+    return buf
+
+
+def use_tensor_cores(model, n_rows, n_unique, n_pairs) -> bool:
+    """The dispatch rule of K6 (FAST mode, bf16 head)."""
+    return (numerics.mode() == N.SPX_MODE_FAST and model.spx_dtype == N.SPX_DTYPE_BF16 and
+            model.config.hidden_dim % 64 == 0 and n_rows >= TC_MIN_ROWS and
+            n_unique >= TC_MIN_UNIQUE and n_pairs >= TC_MIN_DENSITY * n_rows * n_unique)
+
+
+def merged_logits(model: TransformerModel, prep, id_lists, tensor_cores=None) -> list:
     """K6: logits of node j for id_lists[j], one HBM read per unique id.
-    prep = head_prep(model, rows)."""
+    prep = head_prep(model, rows).  tensor_cores: None = the dispatch rule
+    (use_tensor_cores), True / False to force the tcgen05 / CUDA-core kernel."""
     xg, rr = prep
     flat = np.concatenate([np.asarray(ids, np.int64).reshape(-1) for ids in id_lists])
     sizes = [len(ids) for ids in id_lists]
@@ -339,6 +363,23 @@ def merged_logits(model: TransformerModel, prep, id_lists) -> list:
     d_node, d_out = dev(node[order]), dev(out_idx[order])
     logits = torch.empty(flat.size, dtype=torch.float32, device="cuda")
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    if tensor_cores is None:
+        tensor_cores = use_tensor_cores(model, xg.shape[0], uniq.size, flat.size)
+    if tensor_cores and flat.size:
+        lib = N.lib()
+        nb = lib.spx_tree_tc_scratch_bytes(xg.shape[0], model.config.hidden_dim, uniq.size,
+                                           flat.size)
+        scratch = _tc_scratch(nb)
+        d_uid = dev(inv[order])
+        N.check(lib.spx_tree_merged_logits_tc(
+            N.ptr(xg), N.ptr(rr), xg.shape[0], N.ptr(model.lm_head), model.spx_dtype,
+            N.ptr(model.head_bw), model.config.vocab_size, model.config.hidden_dim,
+            N.ptr(d_uniq), uniq.size, N.ptr(d_uptr), N.ptr(d_node), N.ptr(d_out), N.ptr(d_uid),
+            flat.size,
+            N.ptr(logits), N.ptr(scratch), N.ptr(err), N.stream_ptr()),
+            "spx_tree_merged_logits_tc")
+        N.raise_device_error(err.item())
+        return list(torch.split(logits, sizes))
     N.check(N.lib().spx_tree_merged_logits(N.ptr(xg), N.ptr(rr), xg.shape[0], N.ptr(model.lm_head),
                                            model.spx_dtype, N.ptr(model.head_bw),
                                            model.config.vocab_size,

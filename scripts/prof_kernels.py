@@ -26,14 +26,28 @@ if which == "verify":
         tok, _, _ = spx.head_argmax(m, h[it % 4])
 elif which == "tree":
     rows = int(os.environ.get("ROWS", "26"))
+    k = int(os.environ.get("K", "4"))
+    pool = int(os.environ.get("POOL", str(max(8, rows // 2))))
+    tc = {"1": True, "0": False}.get(os.environ.get("TC", ""), None)
     rs = np.random.default_rng(0)
     h = torch.randn((rows, 4096), device="cuda", generator=g).to(torch.bfloat16).float()
-    # tree-like id sets: siblings share most of their draft top-4
-    base = rs.choice(32000, size=max(8, rows // 2), replace=False)
-    ids = [rs.choice(base, 4, replace=False) for _ in range(rows)]
+    # tree-like id sets: siblings share most of their draft top-k
+    base = rs.choice(32000, size=pool, replace=False)
+    ids = [rs.choice(base, k, replace=False) for _ in range(rows)]
     prep = head_prep(m, h)
     for it in range(int(os.environ.get("ITERS", "6"))):
-        out = merged_logits(m, prep, ids)
+        out = merged_logits(m, prep, ids, tensor_cores=tc)
+    torch.cuda.synchronize()
+    if os.environ.get("TIME", "0") == "1":       # CUDA-event timing of both kernels
+        for mode in (False, True):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(20):
+                merged_logits(m, prep, ids, tensor_cores=mode)
+            e1.record()
+            torch.cuda.synchronize()
+            print(f"rows={rows} U<={pool} k={k} tensor_cores={mode}: "
+                  f"{e0.elapsed_time(e1) * 1000 / 20:.1f} us per call (incl. host CSR build)")
 else:
     raise SystemExit(f"unknown kernel {which}")
 torch.cuda.synchronize()

@@ -12,6 +12,7 @@ import os
 
 import numpy as np
 import pytest
+import torch
 
 import paper_2504_08850_b200 as spx
 from paper_2504_08850_b200 import engine as E
@@ -188,3 +189,27 @@ def test_tree_gate_and_node_eval_kernels():
                 exp[0] = 1
                 exp[paths[p]] = 1
         assert gate.cpu().numpy().tolist() == exp.tolist()
+
+
+@pytest.mark.parametrize("n_rows,n_ids,k", [(200, 300, 16), (64, 128, 64), (26, 40, 4), (300, 700, 8)])
+def test_tree_merged_tensor_cores_match_cuda_cores(n_rows, n_ids, k):
+    """K6 on tcgen05 (kind::f16, xg split exactly into three bf16 parts,
+    TMEM accumulators) vs the CUDA-core CDOT kernel on the same pairs: equal
+    within the f32 accumulation-order tolerance stated here (1e-5 of the
+    row's largest |logit| + 1e-6)."""
+    from paper_2504_08850_b200.model import head_prep, merged_logits
+    cfg = spx.ModelConfig(vocab_size=32000, hidden_dim=4096, num_layers=1, num_heads=32,
+                          ffn_dim=11008, max_context=64, seed=5)
+    m = spx.init_model(cfg, dtype="bf16", head_only=True)
+    g = torch.Generator(device="cuda").manual_seed(n_rows + n_ids)
+    h = torch.randn((n_rows, 4096), device="cuda", generator=g).to(torch.bfloat16).float()
+    r = np.random.default_rng(n_rows)
+    pool = r.choice(32000, n_ids, replace=False)
+    ids = [r.choice(pool, k, replace=False) for _ in range(n_rows)]
+    with numerics.using("fast"):
+        prep = head_prep(m, h)
+        a = merged_logits(m, prep, ids, tensor_cores=False)
+        b = merged_logits(m, prep, ids, tensor_cores=True)
+    for x, y in zip(a, b):
+        x, y = x.cpu().numpy(), y.cpu().numpy()
+        assert np.all(np.abs(x - y) <= 1e-5 * np.abs(x).max() + 1e-6)
