@@ -368,8 +368,16 @@ def decode_bench(args, rank, ws, dev):
         sys.path.insert(0, os.path.join(ROOT, "scripts"))
         import tree_bench
         tree = tree_bench.run(steps=3, seed=seed, models=(t, d))
+    cpu_dec = None
+    try:                     # reported CPU baseline of the same decode (one separate run)
+        cpu_dec = json.load(open(os.path.join(ROOT, "profiles", "r02_cpu_decode.json")))
+        cpu_dec = {"tok_s": cpu_dec["tok_s"], "cores": cpu_dec["cores"], "kind": "port",
+                   "source": "profiles/r02_cpu_decode.json (scripts/cpu_decode_baseline.py on "
+                             "the GPU box host: oracle ExitEngine, strict kernels, 3 tokens)"}
+    except (OSError, KeyError, ValueError):
+        pass
     return {"tok_s": ws * n / (float(ms.item()) / 1e3), "unit": "tokens/s", "tree": tree,
-            "injected": injected,
+            "injected": injected, "cpu_baseline": cpu_dec,
             "ms_per_token": ms_tok, "streams": ws, "tokens_per_stream": n,
             "e2e_tok_s": ws * n / float(e2e_s.item()),
             "avg_exit_layer": el, "full_heads_per_token": heads,

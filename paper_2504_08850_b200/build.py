@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIB_DIR, "libspecexit_b200.so")
 SOURCES = ["spx_predictor.cu", "spx_pred_stream.cu", "spx_pred_split.cu", "spx_pred_team_bf16_a.cu", "spx_pred_team_bf16_b.cu",
-           "spx_pred_team_bf16_c.cu", "spx_pred_team_f32.cu", "spx_verify.cu", "spx_sched.cu", "spx_tree.cu", "spx_tree_tc.cu", "spx_init.cu",
+           "spx_pred_team_bf16_c.cu", "spx_pred_team_bf16_w.cu", "spx_pred_team_f32.cu", "spx_verify.cu", "spx_sched.cu", "spx_tree.cu", "spx_tree_tc.cu", "spx_init.cu",
            "spx_layers.cu", "spx_engine.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

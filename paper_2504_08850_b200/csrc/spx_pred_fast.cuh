@@ -23,7 +23,10 @@
 
 #include <type_traits>
 
-constexpr int NTEAM = 4;
+#ifndef SPX_FAST_NTEAM
+#define SPX_FAST_NTEAM 4
+#endif
+constexpr int NTEAM = SPX_FAST_NTEAM;           // DOT teams (2 in the wide-row variant)
 constexpr int TEAM = 4;
 constexpr int NTAIL = 4;
 constexpr int HALF = 2;                        // LM-head rows per TMA unit

@@ -6,6 +6,11 @@ namespace spx {
 
 namespace spx {
 
+// the wide-row (2-team) variant, spx_pred_team_bf16_w.cu
+int launch_team_wide_bf16(const PredParams &p, int smem_optin, int sms, cudaStream_t stream,
+                          bool &inline_rc);
+bool team_wide_fits(int d, int K, int H, int smem_optin);
+
 // FAST kernel families, one translation unit each (spx_pred_stream.cu,
 // spx_pred_team.cu)
 int launch_stream_bf16(const PredParams &p, const StreamPlan &sp, int grid, cudaStream_t stream,
@@ -223,7 +228,10 @@ static int launch_predictor(const PredParams &p, const spx_predictor_args *a, cu
     // one CTA per request
     const bool stream_ok = std::is_same<TW, __nv_bfloat16>::value && p.K <= SKMAX &&
                            (p.d == 2048 || p.d == 4096 || p.d == 8192);
-    if (!stream_ok && plan_smem<TW>(p.d, p.K, p.H, g_smem_optin).bytes == 0) strict = true;
+    const bool wide_ok = std::is_same<TW, __nv_bfloat16>::value &&
+                         team_wide_fits(p.d, p.K, p.H, g_smem_optin);
+    if (!stream_ok && !wide_ok && plan_smem<TW>(p.d, p.K, p.H, g_smem_optin).bytes == 0)
+      strict = true;
   }
   if (strict) {
     const size_t smem = strict_smem_bytes(p.d, p.K);
@@ -310,7 +318,12 @@ static int launch_fast(const PredParams &p0, const spx_predictor_args *a, cudaSt
     static const int env_w1 = getenv("SPX_PRED_W1SMEM") ? atoi(getenv("SPX_PRED_W1SMEM")) : -1;
     static const int env_ring = getenv("SPX_PRED_RING") ? atoi(getenv("SPX_PRED_RING")) : -1;
     SmemPlan sp = plan_smem<TW>(p.d, p.K, p.H, g_smem_optin, env_w1, env_ring);
-    if (sp.bytes == 0) return SPX_EINVAL;
+    if (sp.bytes == 0) {
+      // rows too wide for the 4-team ring (d = 8192, K > 8): the 2-team variant
+      if constexpr (std::is_same<TW, __nv_bfloat16>::value)
+        return launch_team_wide_bf16(p, g_smem_optin, g_sms, stream, inline_rc);
+      return SPX_EINVAL;
+    }
     inline_rc = p.recheck && rscr <= sp.off_bar;
     p.recheck_inline = inline_rc ? 1 : 0;
     const long long need = (a->B + NTEAM - 1) / NTEAM;

@@ -22,7 +22,7 @@ def launch_bytes(B, U, K, d):
     return U * d * 2 + B * d * 4 + B * (3 * K * 4 + 5) + 2 * d * 4 + (3 * K * H + 2 * H + 1) * 4
 
 
-def one(model, V, d, K, B, peak):
+def one(model, V, d, K, B, peak, chain=False):
     bank = spx.PredictorBank({l: spx.init_predictor(K, H, rng.derive(3, l)) for l in range(NL)}, NL)
     g = torch.Generator(device="cuda")
     g.manual_seed(B * 131 + K)
@@ -34,8 +34,14 @@ def one(model, V, d, K, B, peak):
     prev0 = torch.full((B, K), float(np.float32(1.0 / K)), device="cuda")
     prev = prev0.clone()
 
+    inter = torch.zeros((NL, B, 2 * K + 2), device="cuda")
+
     def step():
         prev.copy_(prev0)
+        if chain:                          # pipelined split form (gather l + tail l-1)
+            spx.evaluate_chain(model, bank, hidden, ids, prev, inter, list(range(NL)),
+                               threshold=0.7)
+            return
         for l in range(NL):
             spx.evaluate_batch(model, bank, hidden[l], ids[l], prev, threshold=0.7, layer=l,
                                outputs=False, pdl=2)
@@ -60,8 +66,9 @@ def one(model, V, d, K, B, peak):
     e1.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / (reps * NL)
     by = launch_bytes(B, U, K, d)
-    kern = ("stream" if (K <= 8 and d in (2048, 4096, 8192)) else
-            "strict-fallback" if d * 2 * 2 * 4 * 2 > 227 * 1024 else "team")
+    kern = ("pipelined-chain" if chain else
+            "stream" if (K <= 8 and d in (2048, 4096, 8192)) else
+            "team-wide (2 teams)" if d * 2 * 2 * 4 * 2 > 227 * 1024 else "team")
     return {"V": V, "d": d, "K": K, "B": B, "U": U, "us_per_launch": us,
             "evals_per_s": B / (us * 1e-6), "GBps": by / (us * 1e-6) / 1e9,
             "frac": by / (us * 1e-6) / 1e9 / peak, "kernel": kern}
@@ -79,6 +86,8 @@ def main():
             for K in (1, 4, 16, 64):
                 for B in (1, 64, 1024):
                     print(json.dumps(one(model, V, d, K, B, peak)), flush=True)
+                    if K <= 8 and B >= 64:
+                        print(json.dumps(one(model, V, d, K, B, peak, chain=True)), flush=True)
             del model
             torch.cuda.empty_cache()
 
