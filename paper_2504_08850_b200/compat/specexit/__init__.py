@@ -14,9 +14,12 @@ to the production order.
 Out of scope (training, the offline pipeline, CLI, metrics): the training
 entry points raise NotImplementedError; use the reference package for them.
 """
+import os as _os
+
 from paper_2504_08850_b200 import numerics as _numerics
 
-_numerics.set_mode("strict")
+# SPECEXIT_B200_NUMERICS=fast selects the production order for the whole package
+_numerics.set_mode(_os.environ.get("SPECEXIT_B200_NUMERICS", "strict"))
 
 from . import engine, model, predictor, rng, scheduler, speculation, tree  # noqa: E402,F401
 

@@ -29,13 +29,15 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.skipif(not os.path.isdir(REF), reason="stage with scripts/stage_reference_tests.sh")
-def test_reference_suite_through_compat():
+@pytest.mark.parametrize("numerics", ["strict", "fast"])
+def test_reference_suite_through_compat(numerics):
     cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-c",
            os.path.join(REF, "pytest.ini"), "--rootdir", REF]
     for s in SKIP:
         cmd += ["--deselect", s]
     cmd += ["test_predictor.py", "test_scheduler.py", "test_engine.py", "test_tree.py"]
-    env = dict(os.environ, PYTHONPATH=ROOT + os.pathsep + os.environ.get("PYTHONPATH", ""))
+    env = dict(os.environ, PYTHONPATH=ROOT + os.pathsep + os.environ.get("PYTHONPATH", ""),
+               SPECEXIT_B200_NUMERICS=numerics)
     r = subprocess.run(cmd, cwd=REF, capture_output=True, text=True, timeout=1500, env=env)
     tail = (r.stdout + r.stderr)[-4000:]
     print(tail)
