@@ -142,6 +142,11 @@ int spx_predictor_tail(const spx_predictor_args *args, const float *inter, void 
 int spx_predictor_gather_tail(const spx_predictor_args *args, float *inter,
                               const spx_predictor_args *tail_args, const float *tail_inter,
                               void *stream);
+/* The chain's last step: the tail of `tail_args` by the pipelined kernel's
+ * tail warps with an empty gather (one warp per row across the grid), after
+ * the preceding launch completes. */
+int spx_predictor_tail_pipelined(const spx_predictor_args *tail_args, const float *tail_inter,
+                                 void *stream);
 
 /* Per-layer constants of the certification bound for one predictor:
  * cert[i] = sum_j |w2[j]| |w1[i][j]| (i < 3K), cert[3K] = sum_j |w2[j] b1[j]|,

@@ -129,6 +129,7 @@ def lib():
     L.spx_predictor_split_ok.argtypes = [ctypes.POINTER(PredictorArgs)]
     L.spx_predictor_gather.argtypes = [ctypes.POINTER(PredictorArgs), _vp, _vp]
     L.spx_predictor_tail.argtypes = [ctypes.POINTER(PredictorArgs), _vp, _vp]
+    L.spx_predictor_tail_pipelined.argtypes = [ctypes.POINTER(PredictorArgs), _vp, _vp]
     L.spx_predictor_gather_tail.argtypes = [ctypes.POINTER(PredictorArgs), _vp,
                                             ctypes.POINTER(PredictorArgs), _vp, _vp]
     L.spx_tree_tc_scratch_bytes.argtypes = [_i64, _i64, _i64, _i64]

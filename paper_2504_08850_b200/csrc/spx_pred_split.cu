@@ -887,7 +887,8 @@ int launch_split_gather(const PredParams &p, float *inter, const PredParams *pt,
   if (pt && pt->recheck && recheck_scratch_bytes(pt->d, pt->K) > (size_t)gp.S * gp.slot_bytes)
     return SPX_EINVAL;
   const long long cap = (long long)per_sm * g_split_sms;
-  const int grid = (int)(p.B < cap ? p.B : cap);
+  const int rows = p.B > 0 ? p.B : pt ? pt->B : 0;      // B = 0: tail warps only
+  const int grid = (int)(rows < cap ? rows : cap);
   PredParams none{};
   const PredParams &q = pt ? *pt : none;
   // SPX_SPLIT_PIPE (A/B): 1 = one compute team + 4 tail warps (default:

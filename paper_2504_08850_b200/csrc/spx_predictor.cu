@@ -422,6 +422,22 @@ extern "C" int spx_predictor_gather_tail(const spx_predictor_args *a, float *int
   return spx_launch_status("spx_predictor_gather_tail");
 }
 
+extern "C" int spx_predictor_tail_pipelined(const spx_predictor_args *t, const float *inter_t,
+                                            void *stream) {
+  PredParams pt;
+  const int rc = params_from_args(t, pt);
+  if (rc) return rc;
+  if (!inter_t || t->mode != SPX_MODE_FAST || !split_supported(pt, t->head_dtype))
+    return SPX_EINVAL;
+  if (t->B == 0) return 0;
+  PredParams p = pt;                 // an empty gather of the same shape: tail warps only
+  p.B = 0;
+  p.pdl = 3;
+  const int r = launch_split_gather(p, nullptr, &pt, inter_t, (cudaStream_t)stream);
+  if (r) return r;
+  return spx_launch_status("spx_predictor_tail_pipelined");
+}
+
 extern "C" int spx_predictor_tail(const spx_predictor_args *a, const float *inter, void *stream) {
   PredParams p;
   const int rc = params_from_args(a, p);

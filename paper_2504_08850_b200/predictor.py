@@ -469,6 +469,8 @@ def evaluate_chain(model, weights, hidden, ids, prev, inter, layers, threshold=0
     per further layer ONE launch = that layer's gather + the previous layer's
     tail, then the last layer's tail -- so every LM-head gather overlaps its
     neighbours and no per-row MLP tail sits on the bandwidth-bound path.
+    The last layer's tail runs on the same kernel's tail warps with an empty
+    gather (spx_predictor_tail_pipelined).
     hidden[i] / ids[i] / inter[i] / outs[i] / feat_out[i] belong to
     layers[i]; inter: (len(layers), B, 2K+2) f32.  FAST mode, shapes of
     split_supported.  Same outputs, bit for bit, as evaluate_batch per layer.
@@ -491,6 +493,6 @@ def evaluate_chain(model, weights, hidden, ids, prev, inter, layers, threshold=0
         N.check(lib.spx_predictor_gather_tail(args[i], N.ptr(inter[i]), args[i - 1],
                                               N.ptr(inter[i - 1]), st),
                 "spx_predictor_gather_tail")
-    args[-1].pdl = 0
-    N.check(lib.spx_predictor_tail(args[-1], N.ptr(inter[n - 1]), st), "spx_predictor_tail")
+    N.check(lib.spx_predictor_tail_pipelined(args[-1], N.ptr(inter[n - 1]), st),
+            "spx_predictor_tail_pipelined")
     return outs

@@ -85,8 +85,8 @@ def pipe():                          # pipelined: gather(l) + tail(l-1) per laun
     for l in range(1, L):
         N.check(N.lib().spx_predictor_gather_tail(A[l], N.ptr(inter[l]), A[l - 1],
                                                   N.ptr(inter[l - 1]), N.stream_ptr()), "gt")
-    A[L - 1].pdl = 0
-    N.check(N.lib().spx_predictor_tail(A[L - 1], N.ptr(inter[L - 1]), N.stream_ptr()), "tail")
+    N.check(N.lib().spx_predictor_tail_pipelined(A[L - 1], N.ptr(inter[L - 1]), N.stream_ptr()),
+            "tailp")
 
 
 def seq():                           # gather then tail, one stream
