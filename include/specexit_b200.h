@@ -114,6 +114,8 @@ typedef struct {
                              /* (cumulative), [4] rows whose STRICT decision   */
                              /* still sat inside the carried prev bound        */
                              /* (cumulative), [5..] row list                   */
+  uint8_t *fired_any;        /* (B) optional: fired_any[r] |= fired[r] (the    */
+                             /*     token's predictor_fired, engine.py:199)    */
 } spx_predictor_args;
 int spx_predictor_eval(const spx_predictor_args *args, void *stream);
 

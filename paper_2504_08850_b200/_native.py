@@ -41,7 +41,7 @@ class PredictorArgs(ctypes.Structure):
                 ("layer", _i32), ("mode", _i32), ("pdl", _i32), ("err", _vp),
                 ("B", _i64), ("d", _i64), ("V", _i64), ("K", _i64), ("H", _i64),
                 ("head_wmax", _vp), ("cert", _vp), ("cert_kappa", _f32), ("cert_hnorm", _f32),
-                ("prev_err", _vp), ("recheck", _vp)]
+                ("prev_err", _vp), ("recheck", _vp), ("fired_any", _vp)]
 
 
 class VerifyArgs(ctypes.Structure):

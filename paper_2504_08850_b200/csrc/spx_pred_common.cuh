@@ -79,7 +79,15 @@ struct PredParams {
   float *prev_err;                 // (B)
   int *recheck;                    // (5 + B): see spx_predictor_args.recheck
   int recheck_inline;              // the FAST kernel drains the list itself (epilogue)
+  uint8_t *fired_any;              // (B) optional: |= the decision (the token's "fired")
 };
+
+// the decision of a row: fired[row], and fired_any[row] |= it (ExitRecord's
+// predictor_fired accumulates over the token's layers, engine.py:199-200)
+__device__ __forceinline__ void write_fired(const PredParams &p, int row, bool f) {
+  if (p.fired) p.fired[row] = f ? 1 : 0;
+  if (f && p.fired_any) p.fired_any[row] = 1;
+}
 
 __device__ __forceinline__ bool row_skipped(const PredParams &p, int row) {
   if (p.row_done && p.row_done[row]) return true;
@@ -337,13 +345,13 @@ static __device__ float warp_row_tail(const PredParams &p, int row, float *feats
     if (lane == 0) {
       if (p.z_out) p.z_out[row] = z2;
       if (p.prob_out) p.prob_out[row] = sigmoid64(z2);
-      if (p.fired) p.fired[row] = (z2 >= p.z_cut) ? 1 : 0;
+      write_fired(p, row, z2 >= p.z_cut);
     }
     return z2;
   } else if (lane == 0) {
     if (p.prob_out) p.prob_out[row] = p.const_prob;
     if (p.z_out) p.z_out[row] = 0.0f;
-    if (p.fired) p.fired[row] = (p.const_prob > p.threshold) ? 1 : 0;
+    write_fired(p, row, p.const_prob > p.threshold);
   }
   return __int_as_float(0x7fc00000);
 }

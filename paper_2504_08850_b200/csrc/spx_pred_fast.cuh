@@ -344,12 +344,12 @@ predictor_fast_kernel(PredParams p, SmemPlan sp) {
           // the decision is exact (z2 >= z_cut); the reported probability is
           // the f32 sigmoid (|err| ~1e-7, tolerance 1e-3)
           if (p.prob_out) p.prob_out[row] = (double)sigmoid32(z2);
-          if (p.fired) p.fired[row] = (z2 >= p.z_cut) ? 1 : 0;
+          write_fired(p, row, z2 >= p.z_cut);
         }
       } else if (lane == 0) {
         if (p.prob_out) p.prob_out[row] = p.const_prob;
         if (p.z_out) p.z_out[row] = 0.0f;
-        if (p.fired) p.fired[row] = (p.const_prob > p.threshold) ? 1 : 0;
+        write_fired(p, row, p.const_prob > p.threshold);
       }
       if (p.trace && lane == 0) {
         p.trace[(size_t)row * 16 + 4] = gtimer();

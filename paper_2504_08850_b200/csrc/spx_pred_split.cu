@@ -173,12 +173,12 @@ __device__ void warp_tail_row(const PredParams &p, int row, const float *q, floa
     if (lane == 0) {
       if (p.z_out) p.z_out[row] = z2;
       if (p.prob_out) p.prob_out[row] = (double)sigmoid32(z2);
-      if (p.fired) p.fired[row] = (z2 >= p.z_cut) ? 1 : 0;
+      write_fired(p, row, z2 >= p.z_cut);
     }
   } else if (lane == 0) {
     if (p.prob_out) p.prob_out[row] = p.const_prob;
     if (p.z_out) p.z_out[row] = 0.0f;
-    if (p.fired) p.fired[row] = (p.const_prob > p.threshold) ? 1 : 0;
+    write_fired(p, row, p.const_prob > p.threshold);
   }
   __syncwarp();
 }
@@ -804,11 +804,11 @@ predictor_tail_lanes_kernel(PredParams p, const float *inter) {
         if (mlp) {
           if (p.z_out) p.z_out[row] = z2;
           if (p.prob_out) p.prob_out[row] = (double)sigmoid32(z2);
-          if (p.fired) p.fired[row] = (z2 >= p.z_cut) ? 1 : 0;
+          write_fired(p, row, z2 >= p.z_cut);
         } else {
           if (p.prob_out) p.prob_out[row] = p.const_prob;
           if (p.z_out) p.z_out[row] = 0.0f;
-          if (p.fired) p.fired[row] = (p.const_prob > p.threshold) ? 1 : 0;
+          write_fired(p, row, p.const_prob > p.threshold);
         }
       }
     }

@@ -329,12 +329,12 @@ predictor_stream_kernel(PredParams p, StreamPlan sp) {
         if (lane == 0) {
           if (p.z_out) p.z_out[row] = z2;
           if (p.prob_out) p.prob_out[row] = (double)sigmoid32(z2);
-          if (p.fired) p.fired[row] = (z2 >= p.z_cut) ? 1 : 0;
+          write_fired(p, row, z2 >= p.z_cut);
         }
       } else if (lane == 0) {
         if (p.prob_out) p.prob_out[row] = p.const_prob;
         if (p.z_out) p.z_out[row] = 0.0f;
-        if (p.fired) p.fired[row] = (p.const_prob > p.threshold) ? 1 : 0;
+        write_fired(p, row, p.const_prob > p.threshold);
       }
       if (p.trace && lane == 0) p.trace[(size_t)row * 16 + 4] = gtimer();
       __syncwarp();

@@ -186,7 +186,7 @@ __global__ void mlp_kernel(PredParams p, const float *feats_in) {
   if (lane == 0) {
     if (p.z_out) p.z_out[row] = z2;
     if (p.prob_out) p.prob_out[row] = sigmoid64(z2);
-    if (p.fired) p.fired[row] = (z2 >= p.z_cut) ? 1 : 0;
+    write_fired(p, row, z2 >= p.z_cut);
   }
 }
 
@@ -361,6 +361,7 @@ static int params_from_args(const spx_predictor_args *a, PredParams &p) {
   p.prev_err = a->prev_err;
   p.recheck = a->mode == SPX_MODE_FAST ? a->recheck : nullptr;
   p.recheck_inline = 0;
+  p.fired_any = a->fired_any;
   if (p.recheck && (!a->head_wmax || !a->prev_err ||
                     (a->policy == SPX_POLICY_MLP && !a->cert)))
     return SPX_EINVAL;

@@ -14,8 +14,8 @@ is captured once into a CUDA graph (``_DeviceStep``):
   spx_token_begin       (prev = f32(1/K), flags cleared, exit_layer = L-1)
   target: embed next_in; for l in 0..L-1:
          spx_layer_forward(l)        -- returns at once when done != 0
-         l <= L-2: spx_predictor_eval (row_layer_mask=active, row_done=done)
-                   spx_or_flag       (fired_any |= fired)
+         l <= L-2: spx_predictor_eval (row_layer_mask=active, row_done=done;
+                                      fired_any |= fired in-kernel)
                    spx_verify        (gate=fired, verify set = spec ids;
                                       on membership: done=1, exit_layer=l)
   spx_verify (row_done=done)         -- the final-layer argmax
@@ -230,6 +230,7 @@ class _DeviceStep:
             a.policy, a.const_prob = N.SPX_POLICY_CONST, float(pol.const_prob)
             a.threshold = float(eng.config.threshold)
         a.fired, a.row_layer_mask = N.ptr(self.fired), N.ptr(self.active)
+        a.fired_any = N.ptr(self.fired_any)      # the token's predictor_fired, in-kernel
         a.row_done, a.evals = N.ptr(self.done), N.ptr(self.evals)
         a.layer, a.mode, a.pdl, a.err = l, mode, 0, N.ptr(self.err)
         a.B, a.d, a.V, a.K, a.H = 1, m.config.hidden_dim, m.config.vocab_size, self.K, H
@@ -278,8 +279,6 @@ class _DeviceStep:
             if l <= self.L - 2:
                 pa = self._pargs[l]
                 N.check(lib.spx_predictor_eval(pa, s()), "spx_predictor_eval")
-                N.check(lib.spx_or_flag(N.ptr(self.fired), N.ptr(self.fired_any), s()),
-                        "spx_or_flag")
                 launch_verify(verify_args(tm, ts.cur_hidden, 1, self.exit_token, self.scratch,
                                           self.counter, self.err, gate=self.fired,
                                           row_done=self.done, spec_ptr=self.spec_ptr,
