@@ -50,6 +50,7 @@ extern "C" {
 #define SPX_ERR_LOGIT_NONFINITE 4
 #define SPX_ERR_PREV_SUM 8
 #define SPX_ERR_BAD_LAYER 16
+#define SPX_ERR_ROW_CAP 32        /* a layer call selected more rows than row_cap */
 
 /* K1+K2+K3 -- fused predictor evaluation for B rows at ONE layer.
  * Replaces, per row, the reference chain
@@ -326,6 +327,11 @@ typedef struct {
                                    /* unknown; > 2 selects the multi-row kernel     */
                                    /* chain (prefill, token trees) over the         */
                                    /* persistent single-launch decode layer         */
+  int32_t row_cap;                 /* max rows advanced by one call (shared-memory  */
+                                   /* row set); 0 = max_ctx.  Batched streams: the  */
+                                   /* new rows + lazily completed ones              */
+  int32_t att_cap;                 /* max attention-list length (keys per row); 0 = */
+                                   /* max_ctx.  Rows selecting more set SPX_ERR_ROW_CAP */
 } spx_layer_args;
 int spx_layer_forward(const spx_layer_args *args, void *stream);
 /* floats needed for s_part and int32s for s_flag at these dimensions */
@@ -354,6 +360,9 @@ typedef struct {
 /* stable top-K (value desc, lower id on ties) of n logits
  * (speculation.py:57-60 topk_from_logits). K <= 64. */
 int spx_topk(const float *logits, int64_t n, int32_t K, int32_t *ids_out, void *stream);
+/* spx_topk for `rows` independent rows of n logits (row-major), K ids each. */
+int spx_topk_rows(const float *logits, int64_t rows, int64_t n, int32_t K, int32_t *ids_out,
+                  void *stream);
 /* token start: prev = inv_k (= float32(1/K)), clear flags, exit_layer = L-1 */
 int spx_token_begin(spx_token_state st, int32_t K, int32_t L, float inv_k, void *stream);
 /* token end: pick verified exit token or the final argmax, record, next_in,

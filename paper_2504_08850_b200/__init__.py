@@ -29,3 +29,4 @@ from .engine import (AlwaysExitPolicy, EngineConfig, ExitEngine, ExitRecord,  # 
 __version__ = "0.1.0"
 from .profiling import (LayerTraces, TrainingExample, collect_training_data,  # noqa: F401
                         generation_layer_traces, profile_offline_device)
+from .batched import BatchedExitEngine  # noqa: F401,E402

@@ -16,6 +16,7 @@ SPX_MODE_FAST, SPX_MODE_STRICT = 0, 1
 SPX_DTYPE_BF16, SPX_DTYPE_F32 = 0, 1
 SPX_POLICY_MLP, SPX_POLICY_CONST = 0, 1
 ERR_ID_RANGE, ERR_HIDDEN_NONFINITE, ERR_LOGIT_NONFINITE, ERR_PREV_SUM, ERR_BAD_LAYER = 1, 2, 4, 8, 16
+ERR_ROW_CAP = 32
 
 # device error bits -> the reference's ValueError messages
 ERR_MESSAGES = [
@@ -24,6 +25,7 @@ ERR_MESSAGES = [
     (ERR_LOGIT_NONFINITE, "non-finite speculative logits"),       # predictor.py:47-48
     (ERR_PREV_SUM, "prev_local_probs must sum to 1"),             # predictor.py:49-50
     (ERR_BAD_LAYER, "exit layer out of range"),                   # scheduler.py:69-70
+    (ERR_ROW_CAP, "layer call selected more rows than its row capacity"),
 ]
 
 _vp = ctypes.c_void_p
@@ -70,7 +72,7 @@ class LayerArgs(ctypes.Structure):
                 ("s_part", _vp), ("s_flag", _vp),
                 ("layer", _i32), ("mode", _i32), ("err", _vp),
                 ("max_ctx", _i64), ("d", _i64), ("n_heads", _i64), ("ffn", _i64),
-                ("rows_hint", _i32)]
+                ("rows_hint", _i32), ("row_cap", _i32), ("att_cap", _i32)]
 
 
 class TokenStateC(ctypes.Structure):
@@ -122,6 +124,7 @@ def lib():
     L.spx_embed.argtypes = [_vp, _i32, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
                             _vp, _vp, _vp]
     L.spx_topk.argtypes = [_vp, _i64, _i32, _vp, _vp]
+    L.spx_topk_rows.argtypes = [_vp, _i64, _i64, _i32, _vp, _vp]
     L.spx_token_begin.argtypes = [TokenStateC, _i32, _i32, _f32, _vp]
     L.spx_token_end.argtypes = [TokenStateC, OnlineStateC, _i32, _i32, _i32, _i64, _vp]
     L.spx_or_flag.argtypes = [_vp, _vp, _vp]

@@ -34,6 +34,9 @@ __device__ __forceinline__ void topk_insert(unsigned long long (&l)[TK], unsigne
 
 __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(const float *logits, int n, int K,
                                                            int32_t *ids_out) {
+  // one CTA per row (gridDim.x rows of n logits, K ids each)
+  logits += (size_t)blockIdx.x * n;
+  ids_out += (size_t)blockIdx.x * K;
   __shared__ unsigned long long s_red[TOPK_THREADS / 32];
   __shared__ unsigned long long s_win;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -174,6 +177,15 @@ extern "C" int spx_topk(const float *logits, int64_t n, int32_t K, int32_t *ids_
   if (!logits || !ids_out || n <= 0 || K < 1 || K > 64 || K > n) return SPX_EINVAL;
   topk_kernel<<<1, TOPK_THREADS, 0, (cudaStream_t)stream>>>(logits, (int)n, K, ids_out);
   return spx_launch_status("spx_topk");
+}
+
+extern "C" int spx_topk_rows(const float *logits, int64_t rows, int64_t n, int32_t K,
+                             int32_t *ids_out, void *stream) {
+  if (!logits || !ids_out || rows < 0 || n <= 0 || K < 1 || K > 64 || K > n) return SPX_EINVAL;
+  if (rows == 0) return 0;
+  topk_kernel<<<(unsigned)rows, TOPK_THREADS, 0, (cudaStream_t)stream>>>(logits, (int)n, K,
+                                                                         ids_out);
+  return spx_launch_status("spx_topk_rows");
 }
 
 extern "C" int spx_token_begin(spx_token_state st, int32_t K, int32_t L, float inv_k,

@@ -367,8 +367,8 @@ static TcGeom tc_geom(int nout, int kin, int max_ctx, size_t &smem) {
 static bool tc_layer_supported(const LayerParams &p) {
   if (p.d % 32 || p.ffn % 32 || !p.s_part || !p.s_flag) return false;
   size_t smem;
-  return tc_geom(p.d, p.ffn, p.max_ctx, smem).maxr >= 1 &&
-         tc_geom(p.ffn, p.d, p.max_ctx, smem).maxr >= 1;
+  return tc_geom(p.d, p.ffn, p.row_cap, smem).maxr >= 1 &&
+         tc_geom(p.ffn, p.d, p.row_cap, smem).maxr >= 1;
 }
 
 // Multi-row calls (rows_hint > maxr: prefill, token trees) run one launch per
@@ -378,7 +378,7 @@ static bool tc_layer_supported(const LayerParams &p) {
 template <int EPI>
 static void launch_tc(const LayerParams &p, int nout, int kin, int sms, cudaStream_t s) {
   size_t smem;
-  TcGeom g = tc_geom(nout, kin, p.max_ctx, smem);
+  TcGeom g = tc_geom(nout, kin, p.row_cap, smem);
   cudaFuncSetAttribute(gemv_tc_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   int grid = g.units / TWARPS;

@@ -560,14 +560,14 @@ static size_t mega_smem(const LayerParams &p, int sms) {
   const size_t redf = (size_t)mx * MG_NRP * MG_CW > (size_t)MG_ATT_KEYS * MG_ATT_W
                           ? (size_t)mx * MG_NRP * MG_CW : (size_t)MG_ATT_KEYS * MG_ATT_W;
   return (size_t)MG_SLOTS * MG_STAGE + 2 * MG_SLOTS * 8 + redf * 4 +
-         MG_NRP * MG_CW * 4 + (size_t)p.max_ctx * 4 + 64;
+         MG_NRP * MG_CW * 4 + (size_t)p.row_cap * 4 + 64;
 }
 
 static bool mega_layer_supported(const LayerParams &p, int sms) {
   if (p.d % 8 || p.ffn % 8) return false;
   if (p.d > MG_CT * 8 * 2 || p.ffn > MG_CT * 8 * MG_CPT || p.ffn < p.d) return false;
   if ((size_t)p.ffn * 2 > MG_STAGE || (size_t)p.d * 2 > MG_STAGE) return false;   // >= 1 row/stage
-  if ((p.d / p.nh) > 256 || (p.d / p.nh) % 4 || p.max_ctx > MG_ATT_KEYS) return false;
+  if ((p.d / p.nh) > 256 || (p.d / p.nh) % 4 || p.att_cap > MG_ATT_KEYS) return false;
   if (!p.s_flag) return false;
   return sms > 0 && mega_smem(p, sms) <= 220 * 1024;
 }

@@ -42,6 +42,7 @@ struct LayerParams {
   int *err;
   int max_ctx, d, nh, ffn;
   int rows_hint;
+  int row_cap, att_cap;            // shared-memory row set / attention keys (<= max_ctx)
 };
 
 __device__ __forceinline__ bool exited(const LayerParams &p) { return p.done && *p.done; }
@@ -247,7 +248,7 @@ __global__ void __launch_bounds__(LT) attn_kernel(LayerParams p) {
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int tw = gridDim.x * (blockDim.x >> 5);
   extern __shared__ float sc[];                     // scores: (warps, max_ctx)
-  float *scores = sc + (size_t)(threadIdx.x >> 5) * p.max_ctx;
+  float *scores = sc + (size_t)(threadIdx.x >> 5) * p.att_cap;
   const float scale = __fdiv_rn(1.0f, __fsqrt_rn((float)dh)) ;
   // reference: np.float32(1.0 / math.sqrt(dh)) -- f64 then rounded
   const float scale_ref = (float)(1.0 / sqrt((double)dh));
@@ -427,7 +428,7 @@ static void launch_layer(const LayerParams &p, cudaStream_t s) {
   spx_debug_capture(s, "strict layer: rows");
   qkv_kernel<TW><<<grid_for(3 * p.d), LT, ln_smem, s>>>(p);
   spx_debug_capture(s, "strict layer: qkv");
-  const size_t a_smem = (size_t)wpc * p.max_ctx * sizeof(float);
+  const size_t a_smem = (size_t)wpc * p.att_cap * sizeof(float);
   attn_kernel<<<sms, LT, a_smem, s>>>(p);
   spx_debug_capture(s, "strict layer: attn");
   wo_kernel<TW><<<grid_for(p.d), LT, ln_smem, s>>>(p);
@@ -445,7 +446,8 @@ extern "C" int spx_layer_forward(const spx_layer_args *a, void *stream) {
       a->ffn <= 0 || a->ffn % 4 || a->max_ctx <= 0)
     return SPX_EINVAL;
   if ((size_t)RMAX * (a->ffn > a->d ? a->ffn : a->d) * 4 > 225 * 1024 ||
-      (size_t)(LT / 32) * a->max_ctx * 4 > 225 * 1024)
+      (size_t)(LT / 32) * (a->att_cap > 0 && a->att_cap < a->max_ctx ? a->att_cap : a->max_ctx) * 4 >
+          225 * 1024)
     return SPX_EINVAL;
   LayerParams p;
   p.ln1_g = a->ln1_g; p.ln1_b = a->ln1_b; p.ln2_g = a->ln2_g; p.ln2_b = a->ln2_b;
@@ -460,6 +462,8 @@ extern "C" int spx_layer_forward(const spx_layer_args *a, void *stream) {
   p.layer = a->layer; p.strict = a->mode == SPX_MODE_STRICT; p.err = a->err;
   p.max_ctx = (int)a->max_ctx; p.d = (int)a->d; p.nh = (int)a->n_heads; p.ffn = (int)a->ffn;
   p.rows_hint = a->rows_hint;
+  p.row_cap = a->row_cap > 0 && a->row_cap < p.max_ctx ? a->row_cap : p.max_ctx;
+  p.att_cap = a->att_cap > 0 && a->att_cap < p.max_ctx ? a->att_cap : p.max_ctx;
   cudaStream_t s = (cudaStream_t)stream;
   if (a->w_dtype == SPX_DTYPE_BF16) launch_layer<__nv_bfloat16>(p, s);
   else if (a->w_dtype == SPX_DTYPE_F32) launch_layer<float>(p, s);

@@ -79,12 +79,16 @@ __device__ int cta_row_set(const LayerParams &p, int *rows) {
     __syncthreads();
     int off = s_cnt;
     for (int j = 0; j < w; ++j) off += s_wc[j];
-    if (take) rows[off + __popc(m & ((1u << lane) - 1u))] = i;
+    if (take) {
+      const int slot = off + __popc(m & ((1u << lane) - 1u));
+      if (slot < p.row_cap) rows[slot] = i;
+      else atomicOr(p.err, ERR_ROW_CAP);
+    }
     __syncthreads();
     if (threadIdx.x == 0) for (int j = 0; j < nw; ++j) s_cnt += s_wc[j];
     __syncthreads();
   }
-  return s_cnt;
+  return s_cnt < p.row_cap ? s_cnt : p.row_cap;
 }
 
 // Sum of RP values over the CTA (fixed order -> identical in every CTA).
@@ -383,9 +387,9 @@ __global__ void __launch_bounds__(GT, 1) gemv_layer_kernel(LayerParams p, GemvGe
 constexpr int AT = 128;
 __global__ void __launch_bounds__(AT) attn_fast_kernel(LayerParams p) {
   extern __shared__ __align__(16) float asmem[];
-  float *scores = asmem;                            // max_ctx
-  float *qs = scores + p.max_ctx;                   // dh
-  int *rows = reinterpret_cast<int *>(qs + (p.d / p.nh));   // max_ctx
+  float *scores = asmem;                            // att_cap
+  float *qs = scores + p.att_cap;                   // dh
+  int *rows = reinterpret_cast<int *>(qs + (p.d / p.nh));   // row_cap
   __shared__ float s_red[AT / 32];
   __shared__ float s_bc;
   pdl_wait();
@@ -509,7 +513,7 @@ static bool fast_layer_supported(const LayerParams &p, size_t tw_size) {
     if (cpt > 4) return false;
     if ((size_t)k * tw_size > (size_t)GEMV_SMEM / 2) return false;   // >= 2 stages of one row
   }
-  return (size_t)p.max_ctx * 8 + 64 * 1024 < (size_t)GEMV_SMEM;
+  return (size_t)p.att_cap * 4 + (size_t)p.row_cap * 4 + 64 * 1024 < (size_t)GEMV_SMEM;
 }
 
 
@@ -517,7 +521,7 @@ template <typename TW, int EPI>
 static void launch_gemv(const LayerParams &p, int nout, int kin, int sms, cudaStream_t s) {
   int grid;
   size_t smem;
-  const GemvGeom g = gemv_geom<TW>(nout, kin, sms, p.max_ctx, grid, smem);
+  const GemvGeom g = gemv_geom<TW>(nout, kin, sms, p.row_cap, grid, smem);
   const int cpt = ((kin >> 3) + GT - 1) / GT;
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -541,7 +545,7 @@ static void launch_layer_fast(const LayerParams &p, int sms, cudaStream_t s) {
   static const int env_tc = getenv("SPX_LAYER_TC") ? atoi(getenv("SPX_LAYER_TC")) : 1;
   if (std::is_same<TW, __nv_bfloat16>::value && env_tc && tc_layer_supported(p)) {
     launch_tc<EPI_QKV>(p, 3 * p.d, p.d, sms, s);
-    const size_t ab = (size_t)p.max_ctx * 8 + (size_t)(p.d / p.nh) * 4;
+    const size_t ab = (size_t)(p.att_cap + p.row_cap) * 4 + (size_t)(p.d / p.nh) * 4;
     cudaFuncSetAttribute(attn_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);
     launch_pdl(attn_fast_kernel, 2 * sms, AT, ab, s, p);
     launch_tc<EPI_WO>(p, p.d, p.d, sms, s);
@@ -550,7 +554,7 @@ static void launch_layer_fast(const LayerParams &p, int sms, cudaStream_t s) {
     return;
   }
   launch_gemv<TW, EPI_QKV>(p, 3 * p.d, p.d, sms, s);
-  const size_t asm_bytes = (size_t)p.max_ctx * 8 + (size_t)(p.d / p.nh) * 4;
+  const size_t asm_bytes = (size_t)(p.att_cap + p.row_cap) * 4 + (size_t)(p.d / p.nh) * 4;
   cudaFuncSetAttribute(attn_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)asm_bytes);
   launch_pdl(attn_fast_kernel, 2 * sms, AT, asm_bytes, s, p);

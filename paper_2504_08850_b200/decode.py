@@ -20,12 +20,19 @@ from . import numerics
 class DecodeState:
     """KV cache plus lazy-completion bookkeeping for one generation stream."""
 
-    def __init__(self, model, done_flag: torch.Tensor = None):
+    def __init__(self, model, done_flag: torch.Tensor = None, max_context: int = None,
+                 row_cap: int = 0, att_cap: int = 0):
         cfg = model.config
         if model.head_only:
             raise ValueError("DecodeState needs a model with decoder layers")
         self.model = model
-        L, C, d, f = cfg.num_layers, cfg.max_context, cfg.hidden_dim, cfg.ffn_dim
+        # max_context: rows of this state (default: the model's context);
+        # row_cap / att_cap: per-call row-set and attention-list bounds for
+        # states holding many interleaved streams (BatchedExitEngine)
+        L, d, f = cfg.num_layers, cfg.hidden_dim, cfg.ffn_dim
+        C = cfg.max_context if max_context is None else int(max_context)
+        self.max_context = C
+        self.row_cap, self.att_cap = int(row_cap), int(att_cap)
         dev = "cuda"
         self.kcache = torch.zeros((L, C, d), dtype=torch.float32, device=dev)
         self.vcache = torch.zeros_like(self.kcache)
@@ -59,7 +66,7 @@ class DecodeState:
 
     @property
     def tokens_capacity_left(self):
-        return self.model.config.max_context - self.n
+        return self.max_context - self.n
 
     # -- begin (model.py:181-212) -----------------------------------------------
 
@@ -70,7 +77,7 @@ class DecodeState:
             raise ValueError("tokens must be a non-empty 1-D sequence")
         if toks.min() < 0 or toks.max() >= cfg.vocab_size:
             raise ValueError("token id out of range")
-        if self.n + toks.size > cfg.max_context:
+        if self.n + toks.size > self.max_context:
             raise ValueError("context overflow")
         rows = list(range(self.n, self.n + toks.size))
         self._tok_buf[:toks.size].copy_(torch.as_tensor(toks.astype(np.int32)))
@@ -93,12 +100,12 @@ class DecodeState:
         cfg = m.config
         N.check(N.lib().spx_embed(N.ptr(m.embedding), m.spx_dtype, N.ptr(m.pos_encoding),
                                   N.ptr(tokens), N.ptr(pos), T, cfg.hidden_dim, cfg.vocab_size,
-                                  cfg.max_context, N.ptr(self.pending), N.ptr(self.frontier),
+                                  self.max_context, N.ptr(self.pending), N.ptr(self.frontier),
                                   N.ptr(self.n_ctx), N.ptr(self.new_row), N.ptr(self.err),
                                   N.stream_ptr()), "spx_embed")
 
     def _set_attn(self, rows, attn_lists):
-        C = self.model.config.max_context
+        C = self.max_context
         if self.attn_ptr is None:
             self._attn_lists = {}
         for j, p in enumerate(rows):
@@ -116,6 +123,14 @@ class DecodeState:
         ptr[C] = len(flat)
         self.attn_ptr = torch.as_tensor(ptr, device="cuda")
         self.attn_idx = torch.as_tensor(np.asarray(flat or [0], np.int32), device="cuda")
+        self._largs = [self._layer_args(l) for l in range(self.model.config.num_layers)]
+
+    def set_attention_csr(self, attn_ptr: torch.Tensor, attn_idx: torch.Tensor):
+        """Static per-row attention lists (CSR over all max_context rows, each
+        list ascending and ending at the row itself): rows of several
+        interleaved streams attend only to their own stream's rows."""
+        self.attn_ptr, self.attn_idx = attn_ptr, attn_idx
+        self._attn_lists = None
         self._largs = [self._layer_args(l) for l in range(self.model.config.num_layers)]
 
     # -- run_layer (model.py:220-270) --------------------------------------------
@@ -143,7 +158,8 @@ class DecodeState:
         a.s_part, a.s_flag = N.ptr(self.s_part), N.ptr(self.s_flag)
         a.layer = l
         a.err = N.ptr(self.err)
-        a.max_ctx, a.d, a.n_heads, a.ffn = cfg.max_context, cfg.hidden_dim, cfg.num_heads, cfg.ffn_dim
+        a.max_ctx, a.d, a.n_heads, a.ffn = self.max_context, cfg.hidden_dim, cfg.num_heads, cfg.ffn_dim
+        a.row_cap, a.att_cap = self.row_cap, self.att_cap
         return a
 
     def launch_layer(self, l: int):
@@ -193,7 +209,7 @@ class DecodeState:
         self.frontier.zero_()
         self.frozen.zero_()
         self.new_rows = []
-        if self.attn_ptr is not None:
+        if self.attn_ptr is not None and getattr(self, "_attn_lists", {}) is not None:
             self.attn_ptr = self.attn_idx = None
             self._attn_lists = {}
             self._largs = [self._layer_args(l) for l in range(self.model.config.num_layers)]

@@ -346,7 +346,7 @@ def prev_error(prev: torch.Tensor) -> torch.Tensor:
 def evaluate_batch(model, weights, hidden, ids, prev, threshold=0.5, layer=0, outputs=True, pdl=False,
                    row_layer_mask=None, row_done=None, evals=None, err=None, mode=None,
                    policy=None, out=None, prev_err=None, recheck=None, certify=True,
-                   feat_out=None):
+                   feat_out=None, fired_any=None):
     """K1+K2+K3 for B rows at one layer in ONE launch (spx_predictor_eval).
 
     model: TransformerModel (head + final norm used); weights: PredictorWeights
@@ -361,10 +361,12 @@ def evaluate_batch(model, weights, hidden, ids, prev, threshold=0.5, layer=0, ou
     prev_err (B,) is the error bound carried with ``prev`` (default: attached
     to the prev tensor, see prev_error); recheck the work list (default: one
     per stream and B, see recheck_buffer).  certify=False turns it off.
-    feat_out: optional (B, 3K) f32 tensor receiving the feature vectors."""
+    feat_out: optional (B, 3K) f32 tensor receiving the feature vectors;
+    fired_any: optional (B) u8 tensor, |= the decision (a token's predictor_fired)."""
     a, out = _batch_args(model, weights, hidden, ids, prev, threshold, layer, outputs, pdl,
                          row_layer_mask, row_done, evals, err, mode, policy, out, prev_err,
                          recheck, certify, feat_out)
+    a.fired_any = N.ptr(fired_any)
     N.check(N.lib().spx_predictor_eval(a, N.stream_ptr()), "spx_predictor_eval")
     return out
 
