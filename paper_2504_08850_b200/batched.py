@@ -110,11 +110,12 @@ class BatchedExitEngine:
         self.P = P
         for st in (self.ts, self.ds):
             st.reset()
-        if P > 1:
-            toks = [prompts[b][q] for q in range(P - 1) for b in range(self.B)]
-            pos = [q for q in range(P - 1) for _ in range(self.B)]
+        # prefill position by position (B rows per call: the row set of a call
+        # stays within row_cap; rows attend only to earlier, complete rows)
+        for q in range(P - 1):
+            toks = [prompts[b][q] for b in range(self.B)]
             for st, m in ((self.ts, self.target), (self.ds, self.draft)):
-                st.begin(toks, pos_ids=pos)
+                st.begin(toks, pos_ids=[q] * self.B)
                 for l in range(m.config.num_layers):
                     st.launch_layer(l)
         self.next_in.copy_(torch.as_tensor([p[-1] for p in prompts], dtype=torch.int32))
