@@ -332,7 +332,13 @@ typedef struct {
                                    /* new rows + lazily completed ones              */
   int32_t att_cap;                 /* max attention-list length (keys per row); 0 = */
                                    /* max_ctx.  Rows selecting more set SPX_ERR_ROW_CAP */
+  void *tc_scratch;                /* optional: >= spx_layer_tc_scratch_bytes(d, ffn,  */
+                                   /* row_cap or max_ctx) bytes; enables the tcgen05  */
+                                   /* path for calls advancing >= 16 rows (FAST, bf16) */
 } spx_layer_args;
+/* scratch of the tensor-core multi-row layer path (three bf16 parts of the
+ * advanced rows) */
+int64_t spx_layer_tc_scratch_bytes(int64_t d, int64_t ffn, int64_t row_cap);
 int spx_layer_forward(const spx_layer_args *args, void *stream);
 /* floats needed for s_part and int32s for s_flag at these dimensions */
 int64_t spx_layer_part_floats(int64_t d, int64_t ffn);

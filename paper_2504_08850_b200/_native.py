@@ -72,7 +72,7 @@ class LayerArgs(ctypes.Structure):
                 ("s_part", _vp), ("s_flag", _vp),
                 ("layer", _i32), ("mode", _i32), ("err", _vp),
                 ("max_ctx", _i64), ("d", _i64), ("n_heads", _i64), ("ffn", _i64),
-                ("rows_hint", _i32), ("row_cap", _i32), ("att_cap", _i32)]
+                ("rows_hint", _i32), ("row_cap", _i32), ("att_cap", _i32), ("tc_scratch", _vp)]
 
 
 class TokenStateC(ctypes.Structure):
@@ -139,6 +139,8 @@ def lib():
     L.spx_tree_tc_scratch_bytes.restype = _i64
     L.spx_tree_merged_logits_tc.argtypes = [_vp, _vp, _i64, _vp, _i32, _vp, _i64, _i64, _vp, _i64,
                                             _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp]
+    L.spx_layer_tc_scratch_bytes.argtypes = [_i64, _i64, _i64]
+    L.spx_layer_tc_scratch_bytes.restype = _i64
     L.spx_inject_spec.argtypes = [_vp, _i32, _vp, _vp, _vp, _i64, _vp]
     L.spx_predictor_cert.argtypes = [_vp, _vp, _vp, _i64, _i64, _vp, _vp]
     L.spx_head_stats.argtypes = [_vp, _i32, _i64, _i64, _vp, _vp]

@@ -1,0 +1,258 @@
+// Multi-row decoder layers on the 5th-generation tensor cores (sm_100a):
+// batched streams (BatchedExitEngine), token trees, prefill -- every call
+// that advances >= 16 rows.  Included by spx_layers.cu after
+// spx_layers_fast.cuh.
+//
+// The 8-row mma.sync path (spx_gemv_tc.cuh) re-streams each weight matrix
+// once per 8-row slice; here every matrix is ONE weight-streaming GEMM per
+// call:
+//
+//   D[o][n] (TMEM f32, 128 lanes = 128 output features x <= 128 rows)
+//     += W[o0 .. o0+127][k-block] . X_part[n0 .. n0+127][k-block]^T
+//
+// for the three exact bf16 parts of the f32 input rows (hi + mid + lo = the
+// whole f32 mantissa; bf16 x bf16 products are exact in f32), so only the
+// accumulation order differs from the CUDA-core FAST kernels.  Per call:
+//
+//   tcl_rows      the row set (frontier == layer, not frozen), once
+//   per matrix:   tcl_prep  input rows -> LayerNorm (QKV, FFN1) -> 3 bf16 parts
+//                 tcl_gemm  grid (128-feature tiles, 128-row tiles); 16-byte
+//                           cp.async into 128B-swizzled K-major stages, one
+//                           thread issues tcgen05.mma kind::f16, tcgen05.commit
+//                           releases stages; epilogue tcgen05.ld -> the layer's
+//                           epilogue (Q/K/V scatter, residual adds, bias + ReLU)
+//   attention     attn_fast_kernel (unchanged)
+//   tcl_finish    frontier + newest-row copy
+//
+// The weights are read once per 128-row tile (once for <= 128 rows).
+#pragma once
+#include "spx_umma.cuh"
+
+namespace spx {
+
+constexpr int TL_M = 128;             // output features per tile (UMMA M)
+constexpr int TL_NT = 128;            // rows per tile (UMMA N)
+constexpr int TL_BK = 64;             // K elements per stage (one 128-byte swizzle atom)
+constexpr int TL_STAGES = 3;
+constexpr int TL_THREADS = 128;
+constexpr int TL_PARTS = 3;
+constexpr size_t TL_TILE_A = (size_t)TL_M * TL_BK * 2;
+constexpr size_t TL_TILE_B = (size_t)TL_NT * TL_BK * 2;
+constexpr size_t TL_STAGE = TL_TILE_A + TL_PARTS * TL_TILE_B;          // 64 KB
+
+inline int tl_npad(const LayerParams &p) { return (p.row_cap + 15) / 16 * 16; }
+
+// the row set once per call, into p.rows / *p.nrows (global)
+__global__ void __launch_bounds__(512) tcl_rows_kernel(LayerParams p) {
+  if (flag_set(p.done)) return;
+  extern __shared__ int trows[];
+  const int n = cta_row_set(p, trows);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p.rows[i] = trows[i];
+  if (threadIdx.x == 0) *p.nrows = n;
+}
+
+// input rows (row-set order) -> [LayerNorm] -> three bf16 parts (3, Npad, kin)
+template <int EPI>
+__global__ void __launch_bounds__(256) tcl_prep_kernel(LayerParams p, int kin, int Npad,
+                                                     __nv_bfloat16 *parts) {
+  if (flag_set(p.done)) return;
+  const int n = *reinterpret_cast<const volatile int32_t *>(p.nrows);
+  const bool ln = EPI == EPI_QKV || EPI == EPI_FFN1;
+  const float *src = ln ? p.pending : EPI == EPI_WO ? p.s_att : p.s_f;
+  const float *gg = EPI == EPI_QKV ? p.ln1_g : p.ln2_g;
+  const float *bb = EPI == EPI_QKV ? p.ln1_b : p.ln2_b;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const size_t plane = (size_t)Npad * kin;
+  for (int i = gw; i < n; i += nw) {
+    const float *x = src + (size_t)p.rows[i] * kin;
+    float mean = 0.f, den = 1.f;
+    if (ln) {
+      float s = 0.f;
+      for (int j = lane; j < kin; j += 32) s += __ldcg(x + j);
+      s = warp_butterfly_sum(s);
+      mean = s / (float)kin;
+      float v = 0.f;
+      for (int j = lane; j < kin; j += 32) {
+        const float c = __ldcg(x + j) - mean;
+        v = fmaf(c, c, v);
+      }
+      v = warp_butterfly_sum(v);
+      den = sqrtf(v / (float)kin + 1e-5f);
+    }
+    __nv_bfloat16 *o = parts + (size_t)i * kin;
+    for (int j = lane; j < kin; j += 32) {
+      float v = __ldcg(x + j);
+      if (ln) v = ln_elem(v - mean, den, gg[j], bb[j]);
+      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+      const float r1 = v - __bfloat162float(hi);
+      const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+      o[j] = hi;
+      o[plane + j] = mid;
+      o[2 * plane + j] = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+    }
+  }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, int nout, int kin,
+                                                                 int Npad,
+                                                                 const __nv_bfloat16 *parts) {
+  extern __shared__ __align__(1024) uint8_t tlsm[];
+  uint8_t *ring = reinterpret_cast<uint8_t *>(((uintptr_t)tlsm + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t mma_done[TL_STAGES];
+  __shared__ uint64_t all_done;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (flag_set(p.done)) return;
+  const int nrows = *reinterpret_cast<const volatile int32_t *>(p.nrows);
+  const int o0 = blockIdx.x * TL_M, n0 = blockIdx.y * TL_NT;
+  if (n0 >= nrows) return;
+  const int ntile = (nrows - n0 < TL_NT ? (nrows - n0 + 15) / 16 * 16 : TL_NT);
+  const int nkb = kin / TL_BK;
+  const __nv_bfloat16 *W = reinterpret_cast<const __nv_bfloat16 *>(gemv_weights<EPI>(p));
+  if (tid == 0) {
+    for (int s = 0; s < TL_STAGES; ++s) mbar_init(&mma_done[s], 1);
+    mbar_init(&all_done, 1);
+  }
+  fence_mbar_init();
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(&tmem_base)), "n"(TL_NT));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  const int my_o = o0 + tid;
+  const size_t plane = (size_t)Npad * kin;
+  auto load_stage = [&](int i) {
+    uint8_t *st = ring + (size_t)(i % TL_STAGES) * TL_STAGE;
+    const int k0 = i * TL_BK;
+    {
+      const __nv_bfloat16 *src = W + (size_t)(my_o < nout ? my_o : 0) * kin + k0;
+      uint8_t *dst = st + (size_t)tid * 128;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) cp_async16(dst + ((c ^ (tid & 7)) << 4), src + c * 8, my_o < nout);
+    }
+    for (int pp = 0; pp < TL_PARTS; ++pp) {
+      uint8_t *bt = st + TL_TILE_A + (size_t)pp * TL_TILE_B;
+      const __nv_bfloat16 *pb = parts + (size_t)pp * plane;
+      for (int q = tid; q < ntile * 8; q += TL_THREADS) {
+        const int n = q >> 3, c = q & 7;
+        cp_async16(bt + (size_t)n * 128 + ((c ^ (n & 7)) << 4),
+                   pb + (size_t)(n0 + n) * kin + k0 + c * 8, n0 + n < nrows);
+      }
+    }
+    cp_async_commit();
+  };
+  const uint32_t idesc = umma_idesc_bf16(TL_M, ntile);
+  for (int i = 0; i < TL_STAGES - 1; ++i) {
+    if (i < nkb) load_stage(i); else cp_async_commit();
+  }
+  for (int i = 0; i < nkb; ++i) {
+    const int nxt = i + TL_STAGES - 1;
+    if (nxt < nkb) {
+      if (i >= 1) mbar_wait(&mma_done[(i - 1) % TL_STAGES], ((i - 1) / TL_STAGES) & 1);
+      load_stage(nxt);
+    } else {
+      cp_async_commit();
+    }
+    cp_async_wait<TL_STAGES - 1>();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t sa = smem_u32(ring + (size_t)(i % TL_STAGES) * TL_STAGE);
+#pragma unroll
+      for (int k = 0; k < TL_BK / 16; ++k) {
+        const uint64_t ad = umma_desc_sw128(sa + k * 32);
+#pragma unroll
+        for (int pp = 0; pp < TL_PARTS; ++pp) {
+          const uint64_t bd = umma_desc_sw128(sa + (uint32_t)(TL_TILE_A + pp * TL_TILE_B) + k * 32);
+          umma_bf16(tmem, ad, bd, idesc, (i > 0 || k > 0 || pp > 0) ? 1u : 0u);
+        }
+      }
+      umma_commit(&mma_done[i % TL_STAGES]);
+      if (i == nkb - 1) umma_commit(&all_done);
+    }
+  }
+  mbar_wait(&all_done, 0);
+  tc_fence_after();
+  for (int c0 = 0; c0 < ntile; c0 += 32) {
+    uint32_t v[32];
+    tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c0, v);
+    if (my_o < nout) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int n = n0 + c0 + j;
+        if (c0 + j < ntile && n < nrows) gemv_epilogue<EPI>(p, p.rows[n], my_o, __uint_as_float(v[j]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TL_NT));
+}
+
+// frontier of the advanced rows, newest-row copy (model.py:269-270), reset
+__global__ void tcl_finish_kernel(LayerParams p) {
+  if (flag_set(p.done)) return;
+  const int n = *reinterpret_cast<const volatile int32_t *>(p.nrows);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) p.frontier[p.rows[i]] = p.layer + 1;
+  if (p.cur_hidden && p.new_row) {
+    const int nw = *p.new_row;
+    if (nw >= 0)
+      for (int j = threadIdx.x; j < p.d; j += blockDim.x)
+        p.cur_hidden[j] = __ldcg(p.pending + (size_t)nw * p.d + j);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *p.nrows = 0;
+}
+
+inline size_t tcl_scratch_bytes(int d, int ffn, int row_cap) {
+  const size_t npad = (size_t)(row_cap + 15) / 16 * 16;
+  return (size_t)TL_PARTS * npad * (size_t)(ffn > d ? ffn : d) * 2;
+}
+
+inline bool tcl_supported(const LayerParams &p) {
+  static const int env = getenv("SPX_LAYER_TCGEN05") ? atoi(getenv("SPX_LAYER_TCGEN05")) : 1;
+  return env && p.tc_scratch && p.rows_hint >= 16 && p.d % TL_BK == 0 && p.ffn % TL_BK == 0;
+}
+
+template <int EPI>
+static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sms,
+                       cudaStream_t s) {
+  __nv_bfloat16 *parts = reinterpret_cast<__nv_bfloat16 *>(p.tc_scratch);
+  const int pgrid = (p.row_cap * 32 + 255) / 256;
+  tcl_prep_kernel<EPI><<<pgrid < 4 * sms ? pgrid : 4 * sms, 256, 0, s>>>(p, kin, Npad, parts);
+  const size_t smem = (size_t)TL_STAGES * TL_STAGE + 1024;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(tcl_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured = true;
+  }
+  dim3 grid((unsigned)((nout + TL_M - 1) / TL_M), (unsigned)((Npad + TL_NT - 1) / TL_NT));
+  tcl_gemm_kernel<EPI><<<grid, TL_THREADS, smem, s>>>(p, nout, kin, Npad, parts);
+}
+
+static void launch_layer_tcgen05(const LayerParams &p, int sms, cudaStream_t s) {
+  const int Npad = tl_npad(p);
+  const size_t rsm = (size_t)p.row_cap * 4;
+  if (rsm > 48 * 1024)
+    cudaFuncSetAttribute(tcl_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+  tcl_rows_kernel<<<1, 512, rsm, s>>>(p);
+  tcl_matrix<EPI_QKV>(p, 3 * p.d, p.d, Npad, sms, s);
+  const size_t ab = (size_t)(p.att_cap + p.row_cap) * 4 + (size_t)(p.d / p.nh) * 4;
+  cudaFuncSetAttribute(attn_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);
+  launch_pdl(attn_fast_kernel, 2 * sms, AT, ab, s, p);
+  tcl_matrix<EPI_WO>(p, p.d, p.d, Npad, sms, s);
+  tcl_matrix<EPI_FFN1>(p, p.ffn, p.d, Npad, sms, s);
+  tcl_matrix<EPI_FFN2>(p, p.d, p.ffn, Npad, sms, s);
+  tcl_finish_kernel<<<1, 256, 0, s>>>(p);
+}
+
+}  // namespace spx

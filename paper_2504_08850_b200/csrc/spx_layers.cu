@@ -43,6 +43,7 @@ struct LayerParams {
   int max_ctx, d, nh, ffn;
   int rows_hint;
   int row_cap, att_cap;            // shared-memory row set / attention keys (<= max_ctx)
+  void *tc_scratch;                // tensor-core layer path: input parts (spx_layer_tc.cuh)
 };
 
 __device__ __forceinline__ bool exited(const LayerParams &p) { return p.done && *p.done; }
@@ -386,6 +387,7 @@ __global__ void finish_kernel(LayerParams p) {
 }  // namespace spx
 
 #include "spx_layers_fast.cuh"
+#include "spx_layer_tc.cuh"
 
 using namespace spx;
 
@@ -403,6 +405,12 @@ static int sm_count() {
 template <typename TW>
 static void launch_layer(const LayerParams &p, cudaStream_t s) {
   const int sms = sm_count();
+  if constexpr (std::is_same<TW, __nv_bfloat16>::value) {
+    if (!p.strict && tcl_supported(p) && fast_layer_supported(p, sizeof(TW))) {
+      launch_layer_tcgen05(p, sms, s);               // >= 16 rows: tcgen05 GEMMs
+      return;
+    }
+  }
   if (!p.strict && fast_layer_supported(p, sizeof(TW))) {
     launch_layer_fast<TW>(p, sms, s);
     return;
@@ -464,6 +472,7 @@ extern "C" int spx_layer_forward(const spx_layer_args *a, void *stream) {
   p.rows_hint = a->rows_hint;
   p.row_cap = a->row_cap > 0 && a->row_cap < p.max_ctx ? a->row_cap : p.max_ctx;
   p.att_cap = a->att_cap > 0 && a->att_cap < p.max_ctx ? a->att_cap : p.max_ctx;
+  p.tc_scratch = a->tc_scratch;
   cudaStream_t s = (cudaStream_t)stream;
   if (a->w_dtype == SPX_DTYPE_BF16) launch_layer<__nv_bfloat16>(p, s);
   else if (a->w_dtype == SPX_DTYPE_F32) launch_layer<float>(p, s);
@@ -480,6 +489,11 @@ extern "C" int64_t spx_layer_part_floats(int64_t d, int64_t ffn) {
   m = tc_units(d, ffn) > m ? tc_units(d, ffn) : m;
   return m * 64;
 }
+extern "C" int64_t spx_layer_tc_scratch_bytes(int64_t d, int64_t ffn, int64_t row_cap) {
+  if (d <= 0 || ffn <= 0 || row_cap <= 0) return -1;
+  return (int64_t)tcl_scratch_bytes((int)d, (int)ffn, (int)row_cap);
+}
+
 extern "C" int64_t spx_layer_flag_ints(int64_t d, int64_t ffn) {
   const int64_t n = 3 * d > ffn ? 3 * d : ffn;
   return (n + 7) / 8;

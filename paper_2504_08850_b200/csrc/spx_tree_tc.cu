@@ -26,6 +26,7 @@
 // (deterministic).
 #include "spx_common.cuh"
 #include "../../include/specexit_b200.h"
+#include "spx_umma.cuh"
 
 namespace spx {
 
@@ -38,59 +39,6 @@ constexpr int TC_PARTS = 3;          // hi / mid / lo
 constexpr size_t TC_TILE_A = (size_t)TC_M * TC_BK * 2;            // 16 KB
 constexpr size_t TC_TILE_B = (size_t)TC_NT * TC_BK * 2;           // 16 KB per part
 constexpr size_t TC_STAGE = TC_TILE_A + TC_PARTS * TC_TILE_B;     // 64 KB
-
-// ---- PTX wrappers (sm_100a) --------------------------------------------------
-__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc, bool valid) {
-  const uint32_t d = smem_u32(smem_dst);
-  const int n = valid ? 16 : 0;                     // zero-fill out-of-range rows
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gsrc), "r"(n)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// UMMA shared-memory descriptor: K-major, 128-byte swizzle, rows of 128 B,
-// 8-row groups 1024 B apart (SBO), version 1 (sm_100).
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);           // start address
-  d |= (uint64_t)1 << 16;                           // LBO (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;                 // SBO
-  d |= (uint64_t)1 << 46;                           // descriptor version (sm_100)
-  d |= (uint64_t)2 << 61;                           // SWIZZLE_128B
-  return d;
-}
-
-// Instruction descriptor: kind::f16, A = B = bf16, D = f32, both K-major.
-__host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
-  return (1u << 4)                    // D format f32
-         | (1u << 7)                  // A bf16
-         | (1u << 10)                 // B bf16
-         | ((uint32_t)(N >> 3) << 17) // N
-         | ((uint32_t)(M >> 4) << 24);// M
-}
-
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                          uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-__device__ __forceinline__ void umma_commit(uint64_t *mbar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-               ::"r"(smem_u32(mbar)) : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
 
 // ---- prep: xg (N, d) f32 -> three exact bf16 parts (3, Npad, d) -------------
 __global__ void tree_tc_split_kernel(const float *xg, int N, int Npad, int d,

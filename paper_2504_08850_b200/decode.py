@@ -53,6 +53,12 @@ class DecodeState:
         self.s_flag = torch.zeros(max(1, lib.spx_layer_flag_ints(d, f)), dtype=torch.int32,
                                   device=dev)
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        # tensor-core multi-row path (>= 16 rows per call, bf16 weights)
+        self.tc_scratch = None
+        if model.spx_dtype == N.SPX_DTYPE_BF16:
+            nb = lib.spx_layer_tc_scratch_bytes(d, f, self.row_cap or C)
+            if nb > 0:
+                self.tc_scratch = torch.empty(nb, dtype=torch.uint8, device=dev)
         self.attn_ptr = None
         self.attn_idx = None
         self.done = done_flag
@@ -160,6 +166,7 @@ class DecodeState:
         a.err = N.ptr(self.err)
         a.max_ctx, a.d, a.n_heads, a.ffn = self.max_context, cfg.hidden_dim, cfg.num_heads, cfg.ffn_dim
         a.row_cap, a.att_cap = self.row_cap, self.att_cap
+        a.tc_scratch = N.ptr(self.tc_scratch)
         return a
 
     def launch_layer(self, l: int):

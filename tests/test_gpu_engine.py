@@ -334,3 +334,30 @@ def test_engine_7b_dims_fast_matches_oracle(oracle):
     oe = _oracle_engine(oracle, (oc(tc), oc(dc)), bank, 0.5, "two-level", counts, (5, 1, 2))
     _, want = oe.generate(prompt, 8)
     assert [_rec_tuple(r) for r in got] == [_orec(r) for r in want]
+
+
+@pytest.mark.parametrize("dims", [(4096, 11008, 32), (1024, 2816, 8), (5120, 13824, 40)])
+def test_tcgen05_layers_match_strict(dims):
+    """Calls advancing >= 16 rows take the tensor-core layer path
+    (spx_layer_tc.cuh: tcgen05.mma GEMMs over exact bf16 parts of the rows):
+    a 40-row prefill, then single rows, vs the STRICT reference-order kernels
+    (FAST tolerance 1e-3 as for the other FAST layer kernels)."""
+    d, f, nh = dims
+    cfg = spx.ModelConfig(vocab_size=512, hidden_dim=d, num_layers=2, num_heads=nh, ffn_dim=f,
+                          max_context=64, seed=19)
+    m = spx.init_model(cfg, dtype="bf16")
+    outs = {}
+    for mode in ("strict", "fast"):
+        with numerics.using(mode):
+            st = DecodeState(m)
+            res = []
+            for toks, depth in [(list(range(3, 43)), 2), ([6], 1), (list(range(50, 70)), 2),
+                                ([7], 2)]:
+                st.begin(toks)
+                for l in range(depth):
+                    res.append(st.run_layer(l).cpu().numpy())
+            st.check()
+            res.append(st.pending[:st.n].cpu().numpy())
+            outs[mode] = res
+    for a, b in zip(outs["strict"], outs["fast"]):
+        np.testing.assert_allclose(b, a, rtol=1e-3, atol=1e-3 * np.abs(a).max())
