@@ -10,12 +10,13 @@
 //   D[o][n] (TMEM f32, 128 lanes = 128 output features x <= 128 rows)
 //     += W[o0 .. o0+127][k-block] . X_part[n0 .. n0+127][k-block]^T
 //
-// for the three exact bf16 parts of the f32 input rows (hi + mid + lo = the
-// whole f32 mantissa; bf16 x bf16 products are exact in f32), so only the
-// accumulation order differs from the CUDA-core FAST kernels.  Per call:
+// for the two bf16 parts of the f32 input rows (hi + lo: 16 mantissa bits,
+// relative representation error <= 2^-17, as the 8-row mma.sync path), with
+// exact bf16 x bf16 products and f32 accumulation -- FAST-mode tolerance.
+// Per call:
 //
 //   tcl_rows      the row set (frontier == layer, not frozen), once
-//   per matrix:   tcl_prep  input rows -> LayerNorm (QKV, FFN1) -> 3 bf16 parts
+//   per matrix:   tcl_prep  input rows -> LayerNorm (QKV, FFN1) -> 2 bf16 parts
 //                 tcl_gemm  grid (128-feature tiles, 128-row tiles); 16-byte
 //                           cp.async into 128B-swizzled K-major stages, one
 //                           thread issues tcgen05.mma kind::f16, tcgen05.commit
@@ -33,9 +34,11 @@ namespace spx {
 constexpr int TL_M = 128;             // output features per tile (UMMA M)
 constexpr int TL_NT = 128;            // rows per tile (UMMA N)
 constexpr int TL_BK = 64;             // K elements per stage (one 128-byte swizzle atom)
-constexpr int TL_STAGES = 3;
+constexpr int TL_STAGES = 4;
+constexpr int TL_AHEAD = 2;           // K-blocks loaded ahead; a slot is refilled TL_AHEAD
+                                      // iterations after its MMAs were issued
 constexpr int TL_THREADS = 128;
-constexpr int TL_PARTS = 3;
+constexpr int TL_PARTS = 2;           // hi + lo bf16: 16 mantissa bits of the f32 rows
 constexpr size_t TL_TILE_A = (size_t)TL_M * TL_BK * 2;
 constexpr size_t TL_TILE_B = (size_t)TL_NT * TL_BK * 2;
 constexpr size_t TL_STAGE = TL_TILE_A + TL_PARTS * TL_TILE_B;          // 64 KB
@@ -51,7 +54,8 @@ __global__ void __launch_bounds__(512) tcl_rows_kernel(LayerParams p) {
   if (threadIdx.x == 0) *p.nrows = n;
 }
 
-// input rows (row-set order) -> [LayerNorm] -> three bf16 parts (3, Npad, kin)
+// input rows (row-set order) -> [LayerNorm] -> two bf16 parts (2, Npad, kin);
+// one CTA per row, 4 elements per thread per step
 template <int EPI>
 __global__ void __launch_bounds__(256) tcl_prep_kernel(LayerParams p, int kin, int Npad,
                                                      __nv_bfloat16 *parts) {
@@ -61,35 +65,54 @@ __global__ void __launch_bounds__(256) tcl_prep_kernel(LayerParams p, int kin, i
   const float *src = ln ? p.pending : EPI == EPI_WO ? p.s_att : p.s_f;
   const float *gg = EPI == EPI_QKV ? p.ln1_g : p.ln2_g;
   const float *bb = EPI == EPI_QKV ? p.ln1_b : p.ln2_b;
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  __shared__ float s_red[8];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const size_t plane = (size_t)Npad * kin;
-  for (int i = gw; i < n; i += nw) {
-    const float *x = src + (size_t)p.rows[i] * kin;
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const float4 *x4 = reinterpret_cast<const float4 *>(src + (size_t)p.rows[i] * kin);
+    const int k4 = kin / 4;
     float mean = 0.f, den = 1.f;
     if (ln) {
-      float s = 0.f;
-      for (int j = lane; j < kin; j += 32) s += __ldcg(x + j);
-      s = warp_butterfly_sum(s);
-      mean = s / (float)kin;
-      float v = 0.f;
-      for (int j = lane; j < kin; j += 32) {
-        const float c = __ldcg(x + j) - mean;
-        v = fmaf(c, c, v);
+      float sm = 0.f;
+      for (int j = tid; j < k4; j += 256) {
+        const float4 v = __ldcg(x4 + j);
+        sm += (v.x + v.y) + (v.z + v.w);
       }
-      v = warp_butterfly_sum(v);
-      den = sqrtf(v / (float)kin + 1e-5f);
+      sm = warp_butterfly_sum(sm);
+      if (lane == 0) s_red[w] = sm;
+      __syncthreads();
+      sm = 0.f;
+      for (int q = 0; q < 8; ++q) sm += s_red[q];
+      mean = sm / (float)kin;
+      __syncthreads();
+      float v2 = 0.f;
+      for (int j = tid; j < k4; j += 256) {
+        const float4 v = __ldcg(x4 + j);
+        const float a0 = v.x - mean, a1 = v.y - mean, a2 = v.z - mean, a3 = v.w - mean;
+        v2 = fmaf(a0, a0, fmaf(a1, a1, fmaf(a2, a2, fmaf(a3, a3, v2))));
+      }
+      v2 = warp_butterfly_sum(v2);
+      if (lane == 0) s_red[w] = v2;
+      __syncthreads();
+      v2 = 0.f;
+      for (int q = 0; q < 8; ++q) v2 += s_red[q];
+      den = sqrtf(v2 / (float)kin + 1e-5f);
+      __syncthreads();
     }
     __nv_bfloat16 *o = parts + (size_t)i * kin;
-    for (int j = lane; j < kin; j += 32) {
-      float v = __ldcg(x + j);
-      if (ln) v = ln_elem(v - mean, den, gg[j], bb[j]);
-      const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-      const float r1 = v - __bfloat162float(hi);
-      const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-      o[j] = hi;
-      o[plane + j] = mid;
-      o[2 * plane + j] = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+    for (int j = tid; j < k4; j += 256) {
+      const float4 v4 = __ldcg(x4 + j);
+      float v[4] = {v4.x, v4.y, v4.z, v4.w};
+      __nv_bfloat16 h[4], m[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float x = v[e];
+        if (ln) x = ln_elem(x - mean, den, gg[4 * j + e], bb[4 * j + e]);
+        h[e] = __float2bfloat16_rn(x);
+        m[e] = __float2bfloat16_rn(x - __bfloat162float(h[e]));
+      }
+      *reinterpret_cast<uint2 *>(o + 4 * j) = *reinterpret_cast<uint2 *>(h);
+      *reinterpret_cast<uint2 *>(o + plane + 4 * j) = *reinterpret_cast<uint2 *>(m);
     }
   }
 }
@@ -97,7 +120,8 @@ __global__ void __launch_bounds__(256) tcl_prep_kernel(LayerParams p, int kin, i
 template <int EPI>
 __global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, int nout, int kin,
                                                                  int Npad,
-                                                                 const __nv_bfloat16 *parts) {
+                                                                 const __nv_bfloat16 *parts,
+                                                                 float *partial) {
   extern __shared__ __align__(1024) uint8_t tlsm[];
   uint8_t *ring = reinterpret_cast<uint8_t *>(((uintptr_t)tlsm + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t mma_done[TL_STAGES];
@@ -109,7 +133,10 @@ __global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, 
   const int o0 = blockIdx.x * TL_M, n0 = blockIdx.y * TL_NT;
   if (n0 >= nrows) return;
   const int ntile = (nrows - n0 < TL_NT ? (nrows - n0 + 15) / 16 * 16 : TL_NT);
-  const int nkb = kin / TL_BK;
+  // K split over blockIdx.z (partials reduced by tcl_reduce_kernel)
+  const int kbt = kin / TL_BK, ks = blockIdx.z, nks = gridDim.z;
+  const int kb0 = (int)((long long)ks * kbt / nks), kb1 = (int)((long long)(ks + 1) * kbt / nks);
+  const int nkb = kb1 - kb0;
   const __nv_bfloat16 *W = reinterpret_cast<const __nv_bfloat16 *>(gemv_weights<EPI>(p));
   if (tid == 0) {
     for (int s = 0; s < TL_STAGES; ++s) mbar_init(&mma_done[s], 1);
@@ -129,7 +156,7 @@ __global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, 
   const size_t plane = (size_t)Npad * kin;
   auto load_stage = [&](int i) {
     uint8_t *st = ring + (size_t)(i % TL_STAGES) * TL_STAGE;
-    const int k0 = i * TL_BK;
+    const int k0 = (kb0 + i) * TL_BK;
     {
       const __nv_bfloat16 *src = W + (size_t)(my_o < nout ? my_o : 0) * kin + k0;
       uint8_t *dst = st + (size_t)tid * 128;
@@ -148,18 +175,21 @@ __global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, 
     cp_async_commit();
   };
   const uint32_t idesc = umma_idesc_bf16(TL_M, ntile);
-  for (int i = 0; i < TL_STAGES - 1; ++i) {
+  for (int i = 0; i < TL_AHEAD; ++i) {
     if (i < nkb) load_stage(i); else cp_async_commit();
   }
   for (int i = 0; i < nkb; ++i) {
-    const int nxt = i + TL_STAGES - 1;
+    // block i + AHEAD goes into the slot block i + AHEAD - STAGES used, whose
+    // MMAs were issued STAGES - AHEAD iterations ago
+    const int nxt = i + TL_AHEAD;
     if (nxt < nkb) {
-      if (i >= 1) mbar_wait(&mma_done[(i - 1) % TL_STAGES], ((i - 1) / TL_STAGES) & 1);
+      const int old = nxt - TL_STAGES;
+      if (old >= 0) mbar_wait(&mma_done[old % TL_STAGES], (old / TL_STAGES) & 1);
       load_stage(nxt);
     } else {
       cp_async_commit();
     }
-    cp_async_wait<TL_STAGES - 1>();
+    cp_async_wait<TL_AHEAD>();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (tid == 0) {
@@ -187,7 +217,10 @@ __global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, 
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int n = n0 + c0 + j;
-        if (c0 + j < ntile && n < nrows) gemv_epilogue<EPI>(p, p.rows[n], my_o, __uint_as_float(v[j]));
+        if (c0 + j < ntile && n < nrows) {
+          if (nks == 1) gemv_epilogue<EPI>(p, p.rows[n], my_o, __uint_as_float(v[j]));
+          else partial[((size_t)ks * Npad + n) * nout + my_o] = __uint_as_float(v[j]);
+        }
       }
     }
   }
@@ -195,6 +228,22 @@ __global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, 
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TL_NT));
+}
+
+// the K-split partials of every (row, output) in split order -> the epilogue
+template <int EPI>
+__global__ void __launch_bounds__(256) tcl_reduce_kernel(LayerParams p, int nout, int Npad,
+                                                       int nks, const float *partial) {
+  if (flag_set(p.done)) return;
+  const int n = *reinterpret_cast<const volatile int32_t *>(p.nrows);
+  const long long total = (long long)n * nout;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / nout), o = (int)(e % nout);
+    float s = 0.f;
+    for (int k = 0; k < nks; ++k) s += __ldcg(partial + ((size_t)k * Npad + r) * nout + o);
+    gemv_epilogue<EPI>(p, p.rows[r], o, s);
+  }
 }
 
 // frontier of the advanced rows, newest-row copy (model.py:269-270), reset
@@ -212,9 +261,14 @@ __global__ void tcl_finish_kernel(LayerParams p) {
   if (threadIdx.x == 0) *p.nrows = 0;
 }
 
-inline size_t tcl_scratch_bytes(int d, int ffn, int row_cap) {
+constexpr size_t TL_PARTIAL_BYTES = 96ull << 20;      // K-split partial sums
+
+inline size_t tcl_parts_bytes(int d, int ffn, int row_cap) {
   const size_t npad = (size_t)(row_cap + 15) / 16 * 16;
-  return (size_t)TL_PARTS * npad * (size_t)(ffn > d ? ffn : d) * 2;
+  return ((size_t)TL_PARTS * npad * (size_t)(ffn > d ? ffn : d) * 2 + 255) / 256 * 256;
+}
+inline size_t tcl_scratch_bytes(int d, int ffn, int row_cap) {
+  return tcl_parts_bytes(d, ffn, row_cap) + TL_PARTIAL_BYTES;
 }
 
 inline bool tcl_supported(const LayerParams &p) {
@@ -226,8 +280,18 @@ template <int EPI>
 static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sms,
                        cudaStream_t s) {
   __nv_bfloat16 *parts = reinterpret_cast<__nv_bfloat16 *>(p.tc_scratch);
-  const int pgrid = (p.row_cap * 32 + 255) / 256;
-  tcl_prep_kernel<EPI><<<pgrid < 4 * sms ? pgrid : 4 * sms, 256, 0, s>>>(p, kin, Npad, parts);
+  float *partial = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(p.tc_scratch) +
+                                             tcl_parts_bytes(p.d, p.ffn, p.row_cap));
+  tcl_prep_kernel<EPI><<<p.row_cap < 2 * sms ? p.row_cap : 2 * sms, 256, 0, s>>>(p, kin, Npad,
+                                                                                parts);
+  // K split so that the live CTAs (expected row tiles) fill one wave
+  // (rows_hint), bounded by the partial buffer and >= 8 K-blocks per split
+  const int otiles = (nout + TL_M - 1) / TL_M;
+  const int nt_exp = (p.rows_hint + TL_NT - 1) / TL_NT;
+  int nks = sms / (otiles * (nt_exp > 0 ? nt_exp : 1));    // one wave (1 CTA per SM)
+  nks = nks < 1 ? 1 : nks > 8 ? 8 : nks;
+  while (nks > 1 && ((size_t)nks * Npad * nout * 4 > TL_PARTIAL_BYTES || kin / TL_BK / nks < 8))
+    --nks;
   const size_t smem = (size_t)TL_STAGES * TL_STAGE + 1024;
   static bool configured = false;
   if (!configured) {
@@ -235,8 +299,13 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
                          (int)smem);
     configured = true;
   }
-  dim3 grid((unsigned)((nout + TL_M - 1) / TL_M), (unsigned)((Npad + TL_NT - 1) / TL_NT));
-  tcl_gemm_kernel<EPI><<<grid, TL_THREADS, smem, s>>>(p, nout, kin, Npad, parts);
+  dim3 grid((unsigned)otiles, (unsigned)((Npad + TL_NT - 1) / TL_NT), (unsigned)nks);
+  tcl_gemm_kernel<EPI><<<grid, TL_THREADS, smem, s>>>(p, nout, kin, Npad, parts, partial);
+  if (nks > 1) {
+    const long long work = (long long)(p.rows_hint > 0 ? p.rows_hint : 1) * nout;
+    const int rg = (int)((work + 255) / 256 < 8 * sms ? (work + 255) / 256 : 8 * sms);
+    tcl_reduce_kernel<EPI><<<rg, 256, 0, s>>>(p, nout, Npad, nks, partial);
+  }
 }
 
 static void launch_layer_tcgen05(const LayerParams &p, int sms, cudaStream_t s) {
