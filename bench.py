@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--mode", default="fast", choices=["fast", "strict"])
     ap.add_argument("--no-decode", action="store_true")
     ap.add_argument("--no-tree", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the Llama2-13B batch sweep")
     ap.add_argument("--decode-tokens", type=int, default=32)
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--fused", action="store_true",
@@ -703,6 +704,19 @@ def main():
     decode = None
     if not args.no_decode:
         decode = decode_bench(args, rank, ws, dev)
+    # ---- configs[3]: Llama2-13B batch sweep (B requests per GPU) -----------
+    c4 = None
+    if not args.no_c4:
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        import batch_sweep
+        numerics.set_mode("fast")
+        c4 = {"per_gpu": batch_sweep.run([1, 16, 64, 256], steps=6, warmup=2),
+              "note": "BatchedExitEngine, B independent requests per GPU, 13B random-init "
+                      "bf16, 2-layer draft, K=4, thr 0.5, two-level; tok_s per GPU (device "
+                      "time); with N GPUs the requests shard (B per GPU, no collective)"}
+        for r in c4["per_gpu"]:
+            r["tok_s_all_gpus"] = r["tok_s"] * ws
+        numerics.set_mode(args.mode)
 
     # ---- CPU baseline (rank 0, N=1) ----------------------------------------
     cpu = None
@@ -756,6 +770,7 @@ def main():
             "gpu_launches": launches,
             "clocks": clocks,
             "decode": decode,
+            "c4_batch_sweep_13b": c4,
             "fire_rate": fired,
             "certified": certified,
             "parity": parity,

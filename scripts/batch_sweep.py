@@ -22,20 +22,14 @@ from paper_2504_08850_b200 import numerics, rng
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--batches", default="1,2,4,8,16,32,64,128,256")
-    ap.add_argument("--steps", type=int, default=8)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--layers", type=int, default=40)
-    ap.add_argument("--prompt", type=int, default=16)
-    args = ap.parse_args()
+def run(batches, steps=8, warmup=3, layers=40, prompt=16, emit=None):
+    """The sweep; returns one dict per batch size (emit(d) is called as each
+    finishes)."""
     numerics.set_mode("fast")
     seed = 1234
     V, d, ffn, nh = 32000, 5120, 13824, 40
-    L = args.layers
-    C = args.prompt + args.warmup + args.steps + 1
-    t0 = time.time()
+    L = layers
+    C = prompt + warmup + steps + 1
     t = spx.init_model(spx.ModelConfig(V, d, L, nh, ffn, 512, seed), dtype="bf16")
     dm = spx.init_model(spx.ModelConfig(V, d, 2, nh, ffn, 512, seed + 1), dtype="bf16")
     bank = {l: spx.init_predictor(4, 512, rng.derive(seed, l)) for l in range(L - 1)}
@@ -47,37 +41,50 @@ def main():
     except (OSError, KeyError, ValueError):
         pass
     layer_bytes = (4 * d * d + 2 * d * ffn) * 2
-    print(json.dumps({"init_s": round(time.time() - t0, 1)}), flush=True)
-    for B in [int(x) for x in args.batches.split(",")]:
+    out = []
+    for B in batches:
         eng = spx.BatchedExitEngine(t, dm, E.PredictorPolicy(bank),
                                     E.EngineConfig(k=4, threshold=0.5, schedule_mode="two-level"),
                                     prof, spx.ScheduleConfig(5, 2, 4), batch=B, context=C)
-        prompts = [[int(x) % V for x in rng.splitmix64(seed + 10 * b, args.prompt)]
-                   for b in range(B)]
+        prompts = [[int(x) % V for x in rng.splitmix64(seed + 10 * b, prompt)] for b in range(B)]
         eng.start(prompts)
-        eng.run(args.warmup)
+        eng.run(warmup)
         eng.sync()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        eng.run(args.steps)
+        eng.run(steps)
         e1.record()
         eng.sync()
         ms = e0.elapsed_time(e1)
         recs = eng.records()
-        el = float(np.mean([r.exit_layer for rs in recs for r in rs[args.warmup:]]))
-        heads = float(np.mean([r.full_head_count for rs in recs for r in rs[args.warmup:]]))
-        # every weight once per step: executed target layers (max over the
-        # batch: all 40 unless every stream exited), the draft, the full heads
+        el = float(np.mean([r.exit_layer for rs in recs for r in rs[warmup:]]))
+        heads = float(np.mean([r.full_head_count for rs in recs for r in rs[warmup:]]))
+        # every weight once per step: the target layers, the draft, the full heads
         step_bytes = (L + 2) * layer_bytes + (1 + heads) * V * d * 2
-        print(json.dumps({
-            "model": "Llama2-13B shape", "batch_per_gpu": B, "steps": args.steps,
-            "ms_per_step": ms / args.steps, "tok_s": B * args.steps / (ms / 1e3),
-            "avg_exit_layer": el, "full_heads_per_token": heads,
-            "weights_once_GBps": step_bytes / (ms / args.steps * 1e-3) / 1e9,
-            "weights_once_frac": step_bytes / (ms / args.steps * 1e-3) / 1e9 / peak,
-            "mem_GB": round(torch.cuda.max_memory_allocated() / 1e9, 1)}), flush=True)
+        res = {"model": "Llama2-13B shape", "batch_per_gpu": B, "steps": steps,
+               "ms_per_step": ms / steps, "tok_s": B * steps / (ms / 1e3),
+               "avg_exit_layer": el, "full_heads_per_token": heads,
+               "weights_once_GBps": step_bytes / (ms / steps * 1e-3) / 1e9,
+               "weights_once_frac": step_bytes / (ms / steps * 1e-3) / 1e9 / peak,
+               "mem_GB": round(torch.cuda.max_memory_allocated() / 1e9, 1)}
+        out.append(res)
+        if emit:
+            emit(res)
         del eng
         torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batches", default="1,2,4,8,16,32,64,128,256")
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--layers", type=int, default=40)
+    ap.add_argument("--prompt", type=int, default=16)
+    args = ap.parse_args()
+    run([int(x) for x in args.batches.split(",")], args.steps, args.warmup, args.layers,
+        args.prompt, emit=lambda r: print(json.dumps(r), flush=True))
 
 
 if __name__ == "__main__":
