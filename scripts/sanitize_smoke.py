@@ -51,5 +51,28 @@ st.begin([4])
 for l in range(2):
     st.run_layer(l)
 st.check()
+# round 2: the pipelined predictor chain, the tcgen05 K6 and the tcgen05
+# multi-row layers (20 rows), the batched engine
+L3 = 3
+hh = torch.randn((L3, B, 4096), device="cuda").to(torch.bfloat16).float()
+ids3 = torch.stack([ids, (ids + 7) % 2048, (ids + 13) % 2048])
+bank3 = spx.PredictorBank({l: spx.init_predictor(4, 512, l) for l in range(L3)}, L3)
+inter = torch.zeros((L3, B, 10), device="cuda")
+prev3 = torch.full((B, 4), 0.25, device="cuda")
+spx.evaluate_chain(m, bank3, hh, ids3, prev3, inter, [0, 1, 2], threshold=0.5)
+from paper_2504_08850_b200.model import head_prep, merged_logits  # noqa: E402
+rs = np.random.default_rng(0)
+pool = rs.choice(2048, 96, replace=False)
+rows_h = torch.randn((80, 4096), device="cuda")
+merged_logits(m, head_prep(m, rows_h), [rs.choice(pool, 16, replace=False) for _ in range(80)],
+              tensor_cores=True)
+st2 = spx.DecodeState(m2)
+st2.begin(list(range(1, 21)))
+for l in range(2):
+    st2.run_layer(l)
+st2.check()
+be = spx.BatchedExitEngine(t, d, E.PredictorPolicy(bank), E.EngineConfig(threshold=0.5),
+                           batch=17, context=16)
+be.generate([[84, 104, 101, 32]] * 17, 2)
 torch.cuda.synchronize()
 print("sanitize workload ok")
