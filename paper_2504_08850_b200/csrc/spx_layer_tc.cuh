@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(256) tcl_prep_kernel(LayerParams p, int kin, i
   }
 }
 
-template <int EPI>
+template <int EPI, int AHEAD>
 __global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, int nout, int kin,
                                                                  int Npad,
                                                                  const __nv_bfloat16 *parts,
@@ -143,9 +143,10 @@ __global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, 
     mbar_init(&all_done, 1);
   }
   fence_mbar_init();
+  // two accumulators (even / odd k-steps): two independent MMA chains
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 ::"r"(smem_u32(&tmem_base)), "n"(TL_NT));
+                 ::"r"(smem_u32(&tmem_base)), "n"(2 * TL_NT));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -175,13 +176,13 @@ __global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, 
     cp_async_commit();
   };
   const uint32_t idesc = umma_idesc_bf16(TL_M, ntile);
-  for (int i = 0; i < TL_AHEAD; ++i) {
+  for (int i = 0; i < AHEAD; ++i) {
     if (i < nkb) load_stage(i); else cp_async_commit();
   }
   for (int i = 0; i < nkb; ++i) {
     // block i + AHEAD goes into the slot block i + AHEAD - STAGES used, whose
     // MMAs were issued STAGES - AHEAD iterations ago
-    const int nxt = i + TL_AHEAD;
+    const int nxt = i + AHEAD;
     if (nxt < nkb) {
       const int old = nxt - TL_STAGES;
       if (old >= 0) mbar_wait(&mma_done[old % TL_STAGES], (old / TL_STAGES) & 1);
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, 
     } else {
       cp_async_commit();
     }
-    cp_async_wait<TL_AHEAD>();
+    cp_async_wait<AHEAD>();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (tid == 0) {
@@ -198,10 +199,11 @@ __global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, 
 #pragma unroll
       for (int k = 0; k < TL_BK / 16; ++k) {
         const uint64_t ad = umma_desc_sw128(sa + k * 32);
+        const uint32_t dt = tmem + (uint32_t)((k & 1) * TL_NT);
 #pragma unroll
         for (int pp = 0; pp < TL_PARTS; ++pp) {
           const uint64_t bd = umma_desc_sw128(sa + (uint32_t)(TL_TILE_A + pp * TL_TILE_B) + k * 32);
-          umma_bf16(tmem, ad, bd, idesc, (i > 0 || k > 0 || pp > 0) ? 1u : 0u);
+          umma_bf16(dt, ad, bd, idesc, (i > 0 || k > 1 || pp > 0) ? 1u : 0u);
         }
       }
       umma_commit(&mma_done[i % TL_STAGES]);
@@ -211,8 +213,11 @@ __global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, 
   mbar_wait(&all_done, 0);
   tc_fence_after();
   for (int c0 = 0; c0 < ntile; c0 += 32) {
-    uint32_t v[32];
+    uint32_t v[32], v1[32];
     tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c0, v);
+    tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(TL_NT + c0), v1);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(v1[j]));
     if (my_o < nout) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -227,7 +232,7 @@ __global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, 
   tc_fence_before();
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TL_NT));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * TL_NT));
 }
 
 // the K-split partials of every (row, output) in split order -> the epilogue
@@ -295,12 +300,20 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
   const size_t smem = (size_t)TL_STAGES * TL_STAGE + 1024;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(tcl_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(tcl_gemm_kernel<EPI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaFuncSetAttribute(tcl_gemm_kernel<EPI, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     configured = true;
   }
   dim3 grid((unsigned)otiles, (unsigned)((Npad + TL_NT - 1) / TL_NT), (unsigned)nks);
-  tcl_gemm_kernel<EPI><<<grid, TL_THREADS, smem, s>>>(p, nout, kin, Npad, parts, partial);
+  // SPX_TCL_AHEAD (A/B): K-blocks in flight ahead of the MMA (3 leaves one
+  // iteration of MMA slack per slot, 2 leaves two)
+  static const int env_ahead = getenv("SPX_TCL_AHEAD") ? atoi(getenv("SPX_TCL_AHEAD")) : 2;
+  if (env_ahead == 3)
+    tcl_gemm_kernel<EPI, 3><<<grid, TL_THREADS, smem, s>>>(p, nout, kin, Npad, parts, partial);
+  else
+    tcl_gemm_kernel<EPI, 2><<<grid, TL_THREADS, smem, s>>>(p, nout, kin, Npad, parts, partial);
   if (nks > 1) {
     const long long work = (long long)(p.rows_hint > 0 ? p.rows_hint : 1) * nout;
     const int rg = (int)((work + 255) / 256 < 8 * sms ? (work + 255) / 256 : 8 * sms);
