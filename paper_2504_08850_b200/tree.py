@@ -19,7 +19,8 @@ from .model import (TransformerModel, _VerifyScratch, full_head_logits, head_pre
 from .predictor import decide_exit, extract_features, z_cut
 from .scheduler import OfflineProfile, OnlineState, ScheduleConfig, active_layers, update_online
 from .speculation import (SpeculativeSet, TokenTree, TreeNode, build_token_tree,
-                          enumerate_paths, propose_topk, speculative_set_from_logits)
+                          enumerate_paths, propose_topk, speculative_set_from_logits,
+                          speculative_sets_from_rows)
 
 
 def grouped_speculative_logits(model: TransformerModel, hiddens, token_id_lists):
@@ -235,8 +236,9 @@ class TreeEngine:
             if depth == len(self.branching):
                 break
             nxt = []
-            for j in level:
-                spec = speculative_set_from_logits(logits[j], self.branching[depth])
+            sets = speculative_sets_from_rows(lg, self.branching[depth])    # one host read
+            for i, j in enumerate(level):
+                spec = sets[i]
                 for tok, pr in zip(spec.tokens, spec.draft_probs):
                     nodes.append(TreeNode(token=int(tok), parent=j, depth=depth + 1, prob=pr))
                     c = len(nodes) - 1
@@ -269,8 +271,18 @@ class TreeEngine:
         ctx_len = len(self.context)
         if K > self.draft.config.vocab_size:
             raise ValueError("k exceeds vocabulary size")
+        # every node's draft top-K at once (merge_paths' per-node feature / leaf
+        # verify sets, tree.py:64-73): one batched top-K + softmax, one host read
+        k_sets = {}
+        if 1 <= K <= 64:
+            order = sorted(node_logits)
+            batch = speculative_sets_from_rows(torch.stack([node_logits[j] for j in order]), K)
+            k_sets = {(j, K): s_ for j, s_ in zip(order, batch)}
+
         def propose(context, k):                  # node context -> that node's own logits
             j = self._node_of_context[tuple(context[ctx_len:])]
+            if (j, k) in k_sets:
+                return k_sets[(j, k)]
             return speculative_set_from_logits(node_logits[j], k)
         self._node_of_context = {}
         for j, n in enumerate(tree.nodes):
