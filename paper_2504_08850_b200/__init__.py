@@ -7,7 +7,7 @@ libspecexit_b200.so (C ABI: include/specexit_b200.h).  No CPU fallback.
 from . import numerics  # noqa: F401
 from .model import (LN_EPS, ModelConfig, TransformerModel, final_norm, from_tensors,  # noqa: F401
                     full_head_logits, head_argmax, init_model, layer_norm, load_weights,
-                    sliced_head_logits, tensor_specs)
+                    save_weights, sliced_head_logits, tensor_specs, to_tensors)
 from .predictor import (FeatureVector, PredictorBank, PredictorWeights, decide_exit,  # noqa: F401
                         evaluate_batch, evaluate_batch_split, evaluate_chain, extract_features, init_predictor,
                         load_predictors,

@@ -22,6 +22,11 @@ def load_weights(path):
     return _g.load_weights(path, dtype="f32")
 
 
+def save_weights(model, path):
+    """model.py:408-417."""
+    _m.save_weights(model, path)
+
+
 def full_head_logits(model, hidden):
     return host(_g.full_head_logits(model, hidden)).reshape(-1)
 

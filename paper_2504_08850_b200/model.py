@@ -281,6 +281,42 @@ def load_weights(path, dtype: str = "f32") -> TransformerModel:
     return from_tensors(ModelConfig(seed=seed, **fields), tensors, dtype)
 
 
+def to_tensors(model: TransformerModel) -> dict:
+    """Reference-layout float32 tensors of a device model (the inverse of
+    ``from_tensors``; bf16 weights widen exactly)."""
+    if model.head_only:
+        raise ValueError("head-only model has no decoder weights to export")
+    out = {}
+    for name, _, _ in tensor_specs(model.config):
+        src, transpose = model._target(name)
+        t = src.t() if transpose else src
+        out[name] = t.to(torch.float32).cpu().numpy().copy()
+    return out
+
+
+def save_weights(model: TransformerModel, path):
+    """SPXW writer (model.py:408-417): magic, u32 version 1, u32 count, the
+    "config" pseudo-tensor (config fields + the seed as four 16-bit limbs),
+    then every tensor in declaration order as u16 name length, name, u8 rank,
+    u32 dims, f32 LE data."""
+    cfg = model.config
+    vec = np.array([getattr(cfg, f) for f in CONFIG_FIELDS]
+                   + [(cfg.seed >> s) & 0xFFFF for s in (0, 16, 32, 48)], dtype=np.float32)
+    tensors = to_tensors(model)
+
+    def put(fh, name, arr):
+        nb = name.encode()
+        fh.write(len(nb).to_bytes(2, "little") + nb + arr.ndim.to_bytes(1, "little"))
+        fh.write(b"".join(int(s).to_bytes(4, "little") for s in arr.shape))
+        fh.write(np.ascontiguousarray(arr, dtype="<f4").tobytes())
+
+    with open(path, "wb") as fh:
+        fh.write(b"SPXW" + (1).to_bytes(4, "little") + (len(tensors) + 1).to_bytes(4, "little"))
+        put(fh, "config", vec)
+        for name, arr in tensors.items():
+            put(fh, name, arr)
+
+
 # --- head operators (the function-level drop-ins) --------------------------------
 
 
