@@ -201,8 +201,18 @@ typedef struct {
   int32_t mode;
   int32_t *err;
   int64_t B, d, V;
+  /* optional (FAST, bf16 head, d % 64 == 0, B >= SPX_VERIFY_TC_MIN_ROWS, no
+   * logits_out): the tensor-core form -- the head read once per 128 gated
+   * rows (UMMA over an exact three-part bf16 split of the normalised rows),
+   * candidates within a stated bound of the max re-evaluated in the CDOT
+   * order, so tokens / max logits / flags are bit-identical to the CUDA-core
+   * form.  tc_scratch >= spx_verify_tc_scratch_bytes(B, d, V) bytes. */
+  const float *head_wmax;     /* (V) spx_head_stats                           */
+  void *tc_scratch;
 } spx_verify_args;
+#define SPX_VERIFY_TC_MIN_ROWS 8
 int spx_verify(const spx_verify_args *args, void *stream);
+int64_t spx_verify_tc_scratch_bytes(int64_t B, int64_t d, int64_t V);
 
 /* K5 -- two-level scheduler on device (src/specexit/scheduler.py:49-102).
  * Per row: ring of the last `queue_len` exit layers + neighbour counts. */

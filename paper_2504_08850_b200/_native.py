@@ -15,6 +15,7 @@ from . import build as _build
 SPX_MODE_FAST, SPX_MODE_STRICT = 0, 1
 SPX_DTYPE_BF16, SPX_DTYPE_F32 = 0, 1
 SPX_POLICY_MLP, SPX_POLICY_CONST = 0, 1
+SPX_VERIFY_TC_MIN_ROWS = 8               # include/specexit_b200.h
 ERR_ID_RANGE, ERR_HIDDEN_NONFINITE, ERR_LOGIT_NONFINITE, ERR_PREV_SUM, ERR_BAD_LAYER = 1, 2, 4, 8, 16
 ERR_ROW_CAP = 32
 
@@ -54,7 +55,8 @@ class VerifyArgs(ctypes.Structure):
                 ("verified_out", _vp), ("maxlogit_out", _vp), ("logits_out", _vp),
                 ("done_out", _vp), ("exit_layer_out", _vp), ("full_heads", _vp),
                 ("layer", _i32), ("scratch", _vp), ("counter", _vp), ("mode", _i32),
-                ("err", _vp), ("B", _i64), ("d", _i64), ("V", _i64)]
+                ("err", _vp), ("B", _i64), ("d", _i64), ("V", _i64),
+                ("head_wmax", _vp), ("tc_scratch", _vp)]
 
 
 class OnlineStateC(ctypes.Structure):
@@ -135,6 +137,8 @@ def lib():
     L.spx_predictor_tail_pipelined.argtypes = [ctypes.POINTER(PredictorArgs), _vp, _vp]
     L.spx_predictor_gather_tail.argtypes = [ctypes.POINTER(PredictorArgs), _vp,
                                             ctypes.POINTER(PredictorArgs), _vp, _vp]
+    L.spx_verify_tc_scratch_bytes.argtypes = [_i64, _i64, _i64]
+    L.spx_verify_tc_scratch_bytes.restype = _i64
     L.spx_tree_tc_scratch_bytes.argtypes = [_i64, _i64, _i64, _i64]
     L.spx_tree_tc_scratch_bytes.restype = _i64
     L.spx_tree_merged_logits_tc.argtypes = [_vp, _vp, _i64, _vp, _i32, _vp, _i64, _i64, _vp, _i64,

@@ -27,6 +27,8 @@
 //
 // The weights are read once per 128-row tile (once for <= 128 rows).
 #pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include "spx_umma.cuh"
 
 namespace spx {
@@ -41,7 +43,7 @@ constexpr int TL_THREADS = 128;
 constexpr int TL_PARTS = 2;           // hi + lo bf16: 16 mantissa bits of the f32 rows
 constexpr size_t TL_TILE_A = (size_t)TL_M * TL_BK * 2;
 constexpr size_t TL_TILE_B = (size_t)TL_NT * TL_BK * 2;
-constexpr size_t TL_STAGE = TL_TILE_A + TL_PARTS * TL_TILE_B;          // 64 KB
+constexpr size_t TL_STAGE = TL_TILE_A + TL_PARTS * TL_TILE_B;          // 48 KB
 
 inline int tl_npad(const LayerParams &p) { return (p.row_cap + 15) / 16 * 16; }
 
@@ -235,6 +237,154 @@ __global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, 
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * TL_NT));
 }
 
+// ---------------------------------------------------------------------------
+// TMA-fed, warp-specialised form of the same GEMM (default).  Warps 0-3 are
+// the epilogue (thread = output feature = TMEM lane), warp 4 is the TMA
+// producer (one elected lane: a 2-D cp.async.bulk.tensor of the 128 x 64
+// weight block and of the two 64-wide row-part blocks per stage, 128-byte
+// swizzle done by the copy engine, completion on full[s]), warp 5 issues the
+// UMMAs (one lane) and releases stages with tcgen05.commit on empty[s].  No
+// CTA-wide barrier inside the K loop, and no per-thread copy instructions:
+// the ring is as deep as shared memory allows (4 stages at 128 rows, 7 at 64).
+// Same MMA sequence as tcl_gemm_kernel (even/odd k-step accumulators), so the
+// results are bit-identical to it.
+constexpr int TT_THREADS = 192;
+constexpr int TT_MAX_STAGES = 8;
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int x, int y,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y),
+        "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(TT_THREADS, 1) tcl_tma_kernel(
+    const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+    LayerParams p, int nout, int kin, int Npad, int nbox, int stages, float *partial) {
+  extern __shared__ __align__(1024) uint8_t tlsm[];
+  uint8_t *ring = reinterpret_cast<uint8_t *>(((uintptr_t)tlsm + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t full[TT_MAX_STAGES], empty[TT_MAX_STAGES];
+  __shared__ uint64_t all_done;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (flag_set(p.done)) return;
+  const int nrows = *reinterpret_cast<const volatile int32_t *>(p.nrows);
+  const int o0 = blockIdx.x * TL_M, n0 = blockIdx.y * nbox;
+  if (n0 >= nrows) return;
+  const int kbt = kin / TL_BK, ks = blockIdx.z, nks = gridDim.z;
+  const int kb0 = (int)((long long)ks * kbt / nks), kb1 = (int)((long long)(ks + 1) * kbt / nks);
+  const int nkb = kb1 - kb0;
+  const uint32_t tile_b = (uint32_t)nbox * 128u;
+  const uint32_t stage_bytes = (uint32_t)TL_TILE_A + TL_PARTS * tile_b;
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&all_done, 1);
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+  }
+  fence_mbar_init();
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(&tmem_base)), "n"(2 * TL_NT));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  if (warp == 4) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % stages;
+        if (i >= stages) mbar_wait(&empty[s], ((i / stages) - 1) & 1);
+        uint8_t *st = ring + (size_t)s * stage_bytes;
+        const int k0 = (kb0 + i) * TL_BK;
+        mbar_arrive_expect_tx(&full[s], stage_bytes);
+        tma_load_2d(st, &tmW, k0, o0, &full[s]);
+#pragma unroll
+        for (int pp = 0; pp < TL_PARTS; ++pp)
+          tma_load_2d(st + TL_TILE_A + pp * tile_b, &tmX, k0, pp * Npad + n0, &full[s]);
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_bf16(TL_M, nbox);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % stages;
+        mbar_wait(&full[s], (i / stages) & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(ring + (size_t)s * stage_bytes);
+#pragma unroll
+        for (int k = 0; k < TL_BK / 16; ++k) {
+          const uint64_t ad = umma_desc_sw128(sa + k * 32);
+          const uint32_t dt = tmem + (uint32_t)((k & 1) * TL_NT);
+#pragma unroll
+          for (int pp = 0; pp < TL_PARTS; ++pp) {
+            const uint64_t bd = umma_desc_sw128(sa + (uint32_t)TL_TILE_A + pp * tile_b + k * 32);
+            umma_bf16(dt, ad, bd, idesc, (i > 0 || k > 1 || pp > 0) ? 1u : 0u);
+          }
+        }
+        umma_commit(&empty[s]);
+        if (i == nkb - 1) umma_commit(&all_done);
+      }
+    }
+  } else {
+    const int my_o = o0 + tid;
+    mbar_wait(&all_done, 0);
+    tc_fence_after();
+    for (int c0 = 0; c0 < nbox; c0 += 32) {
+      uint32_t v[32], v1[32];
+      tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c0, v);
+      tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(TL_NT + c0), v1);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(v1[j]));
+      if (my_o < nout) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = n0 + c0 + j;
+          if (c0 + j < nbox && n < nrows) {
+            if (nks == 1) gemv_epilogue<EPI>(p, p.rows[n], my_o, __uint_as_float(v[j]));
+            else partial[((size_t)ks * Npad + n) * nout + my_o] = __uint_as_float(v[j]);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * TL_NT));
+}
+
+// 2-D bf16 tensor map, 64-element (128-byte) inner box, 128-byte swizzle
+static bool tl_tensor_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t cols,
+                          uint32_t box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void **>(&encode),
+                                cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      encode = nullptr;
+    if (!encode) return false;
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)TL_BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides,
+                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // the K-split partials of every (row, output) in split order -> the epilogue
 template <int EPI>
 __global__ void __launch_bounds__(256) tcl_reduce_kernel(LayerParams p, int nout, int Npad,
@@ -306,6 +456,21 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
                          (int)smem);
     configured = true;
   }
+  // SPX_TCL_TMA=0 (A/B): the cp.async form below
+  static const int env_tma = getenv("SPX_TCL_TMA") ? atoi(getenv("SPX_TCL_TMA")) : 1;
+  const int nbox = Npad < TL_NT ? Npad : TL_NT;
+  CUtensorMap tmW, tmX;
+  if (env_tma && tl_tensor_map(&tmW, gemv_weights_host<EPI>(p), (uint64_t)nout, (uint64_t)kin, TL_M) &&
+      tl_tensor_map(&tmX, parts, (uint64_t)TL_PARTS * Npad, (uint64_t)kin, (uint32_t)nbox)) {
+    const size_t stage = TL_TILE_A + (size_t)TL_PARTS * nbox * 128;
+    int stages = (int)((227 * 1024 - 1024) / stage);
+    stages = stages > TT_MAX_STAGES ? TT_MAX_STAGES : stages;
+    const size_t tsm = (size_t)stages * stage + 1024;
+    cudaFuncSetAttribute(tcl_tma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+    dim3 tgrid((unsigned)otiles, (unsigned)((Npad + nbox - 1) / nbox), (unsigned)nks);
+    tcl_tma_kernel<EPI><<<tgrid, TT_THREADS, tsm, s>>>(tmW, tmX, p, nout, kin, Npad, nbox, stages,
+                                                       partial);
+  } else {
   dim3 grid((unsigned)otiles, (unsigned)((Npad + TL_NT - 1) / TL_NT), (unsigned)nks);
   // SPX_TCL_AHEAD (A/B): K-blocks in flight ahead of the MMA (3 leaves one
   // iteration of MMA slack per slot, 2 leaves two)
@@ -314,6 +479,7 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
     tcl_gemm_kernel<EPI, 3><<<grid, TL_THREADS, smem, s>>>(p, nout, kin, Npad, parts, partial);
   else
     tcl_gemm_kernel<EPI, 2><<<grid, TL_THREADS, smem, s>>>(p, nout, kin, Npad, parts, partial);
+  }
   if (nks > 1) {
     const long long work = (long long)(p.rows_hint > 0 ? p.rows_hint : 1) * nout;
     const int rg = (int)((work + 255) / 256 < 8 * sms ? (work + 255) / 256 : 8 * sms);

@@ -151,6 +151,10 @@ template <int EPI>
 __device__ __forceinline__ const void *gemv_weights(const LayerParams &p) {
   return EPI == EPI_QKV ? p.wqkv : EPI == EPI_WO ? p.wo : EPI == EPI_FFN1 ? p.w1 : p.w2;
 }
+template <int EPI>
+inline const void *gemv_weights_host(const LayerParams &p) {
+  return EPI == EPI_QKV ? p.wqkv : EPI == EPI_WO ? p.wo : EPI == EPI_FFN1 ? p.w1 : p.w2;
+}
 
 template <int EPI>
 __device__ __forceinline__ void gemv_epilogue(const LayerParams &p, int row, int o, float v) {

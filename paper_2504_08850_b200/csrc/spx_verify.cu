@@ -16,6 +16,7 @@
 #include "spx_common.cuh"
 #include "../../include/specexit_b200.h"
 #include <type_traits>
+#include <cstdlib>
 
 namespace spx {
 
@@ -417,6 +418,17 @@ __global__ void head_bias_kernel(const TW *head, const float *b, int V, int d, f
   }
 }
 
+}  // namespace spx
+#include "spx_verify_tc.cuh"
+namespace spx {
+
+struct VerifyTcLaunch {
+  const VerParams *p; const float *wmax; uint8_t *scratch; cudaStream_t stream; bool *ok;
+  template <int CPL> void operator()() const {
+    *ok = launch_verify_tc<CPL>(*p, wmax, scratch, stream);
+  }
+};
+
 struct NormLaunch {
   const float *x; int64_t st; const float *g, *b; float *hn, *r; int N, d, mode, lno; int *err;
   unsigned grid; int threads; cudaStream_t stream;
@@ -501,6 +513,17 @@ extern "C" int spx_verify(const spx_verify_args *a, void *stream_) {
   p.logits_out = a->logits_out; p.done_out = a->done_out; p.exit_layer_out = a->exit_layer_out;
   p.full_heads = a->full_heads; p.layer = a->layer; p.scratch = a->scratch; p.counter = a->counter;
   p.mode = a->mode; p.err = a->err; p.B = (int)a->B; p.d = (int)a->d; p.V = (int)a->V;
+  // many gated rows, FAST, bf16 head: the tensor-core form (spx_verify_tc.cuh)
+  static const int env_tc = getenv("SPX_VERIFY_TC") ? atoi(getenv("SPX_VERIFY_TC")) : 1;
+  if (env_tc && a->tc_scratch && a->head_wmax && a->mode != SPX_MODE_STRICT &&
+      a->head_dtype == SPX_DTYPE_BF16 && !a->logits_out && a->d % TV_BK == 0 &&
+      a->B >= SPX_VERIFY_TC_MIN_ROWS && a->B <= 0x7fff) {
+    bool ok = false;
+    if (dispatch_cpl((int)a->d, VerifyTcLaunch{&p, a->head_wmax,
+                                               reinterpret_cast<uint8_t *>(a->tc_scratch), stream,
+                                               &ok}) && ok)
+      return spx_launch_status("spx_verify(tc)");
+  }
   const size_t smem = (size_t)VER_ROWS * a->d * sizeof(float);
   const int nchunk = (int)(a->d / CHUNK);
   const int warps_per_cta = VER_THREADS / 32;
@@ -512,6 +535,11 @@ extern "C" int spx_verify(const spx_verify_args *a, void *stream_) {
     return launch_verify<__nv_bfloat16>(p, nchunk, grid, smem, stream);
   if (a->head_dtype == SPX_DTYPE_F32) return launch_verify<float>(p, nchunk, grid, smem, stream);
   return SPX_EINVAL;
+}
+
+extern "C" int64_t spx_verify_tc_scratch_bytes(int64_t B, int64_t d, int64_t V) {
+  if (B <= 0 || d <= 0 || V <= 0) return 0;
+  return (int64_t)tv_layout((int)B, (int)d, (int)V).total;
 }
 
 extern "C" int spx_final_norm(const float *hidden, int64_t hidden_stride, const float *g,

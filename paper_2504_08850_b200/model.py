@@ -474,7 +474,26 @@ def verify_args(model: TransformerModel, hidden: torch.Tensor, B: int, token_out
     mode = kw.get("mode")
     a.mode, a.err = numerics.mode() if mode is None else mode, N.ptr(err)
     a.B, a.d, a.V = B, model.config.hidden_dim, model.config.vocab_size
+    # many rows, bf16 head: the tensor-core form of K4 (spx_verify_tc.cuh) --
+    # same tokens / flags; the library picks it only where it applies
+    if (kw.get("tensor_cores", True) and B >= N.SPX_VERIFY_TC_MIN_ROWS and model.dtype == "bf16"
+            and model.config.hidden_dim % 64 == 0 and kw.get("logits_out") is None):
+        a.head_wmax = N.ptr(model.head_wmax)
+        a.tc_scratch = N.ptr(_verify_tc_scratch(B, model.config.hidden_dim, model.config.vocab_size))
     return a
+
+
+_TC_VERIFY_SCRATCH = {}
+
+
+def _verify_tc_scratch(B, d, V):
+    key = (torch.cuda.current_device(), B, d, V)
+    t = _TC_VERIFY_SCRATCH.get(key)
+    if t is None:
+        t = torch.empty(int(N.lib().spx_verify_tc_scratch_bytes(B, d, V)), dtype=torch.uint8,
+                        device="cuda")
+        _TC_VERIFY_SCRATCH[key] = t
+    return t
 
 
 def launch_verify(args: N.VerifyArgs, mode: int = None):

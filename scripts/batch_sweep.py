@@ -22,14 +22,14 @@ from paper_2504_08850_b200 import numerics, rng
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def run(batches, steps=8, warmup=3, layers=40, prompt=16, emit=None):
+def run(batches, steps=8, warmup=3, layers=40, prompt=16, emit=None, profile=None):
     """The sweep; returns one dict per batch size (emit(d) is called as each
     finishes)."""
     numerics.set_mode("fast")
     seed = 1234
     V, d, ffn, nh = 32000, 5120, 13824, 40
     L = layers
-    C = prompt + warmup + steps + 1
+    C = prompt + warmup + steps + 2
     t = spx.init_model(spx.ModelConfig(V, d, L, nh, ffn, 512, seed), dtype="bf16")
     dm = spx.init_model(spx.ModelConfig(V, d, 2, nh, ffn, 512, seed + 1), dtype="bf16")
     bank = {l: spx.init_predictor(4, 512, rng.derive(seed, l)) for l in range(L - 1)}
@@ -56,6 +56,9 @@ def run(batches, steps=8, warmup=3, layers=40, prompt=16, emit=None):
         e1.record()
         eng.sync()
         ms = e0.elapsed_time(e1)
+        if profile:
+            from kernel_table import kernel_table
+            kernel_table(lambda: eng.run(1), f"{profile}_b{B}.txt")
         recs = eng.records()
         el = float(np.mean([r.exit_layer for rs in recs for r in rs[warmup:]]))
         heads = float(np.mean([r.full_head_count for rs in recs for r in rs[warmup:]]))
@@ -82,9 +85,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--layers", type=int, default=40)
     ap.add_argument("--prompt", type=int, default=16)
+    ap.add_argument("--profile", default=None, help="path prefix: per-kernel table of one step")
     args = ap.parse_args()
     run([int(x) for x in args.batches.split(",")], args.steps, args.warmup, args.layers,
-        args.prompt, emit=lambda r: print(json.dumps(r), flush=True))
+        args.prompt, emit=lambda r: print(json.dumps(r), flush=True), profile=args.profile)
 
 
 if __name__ == "__main__":

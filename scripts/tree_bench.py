@@ -18,7 +18,7 @@ from paper_2504_08850_b200 import numerics, rng  # noqa: E402
 from paper_2504_08850_b200 import tree as T  # noqa: E402
 
 
-def run(steps=4, branching=(5, 2, 1), seed=1234, layers=32, thr=0.5, models=None):
+def run(steps=4, branching=(5, 2, 1), seed=1234, layers=32, thr=0.5, models=None, profile=None):
     V, D = 32000, 4096
     if models is None:
         tc = spx.ModelConfig(V, D, layers, 32, 11008, 512, seed)
@@ -40,6 +40,10 @@ def run(steps=4, branching=(5, 2, 1), seed=1234, layers=32, thr=0.5, models=None
     res = [eng.step() for _ in range(steps)]
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
+    if profile:
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        from kernel_table import kernel_table
+        kernel_table(eng.step, profile)
     committed = sum(len(r.accepted_tokens) + 1 for r in res)
     return {"tok_s": committed / wall, "unit": "tokens/s", "ms_per_step": 1e3 * wall / steps,
             "steps": steps, "committed_tokens": committed, "branching": list(branching),
@@ -57,9 +61,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--profile", default=None, help="path: per-kernel table of one step")
     args = ap.parse_args()
     numerics.set_mode("fast")
-    print(json.dumps(run(args.steps, layers=args.layers)))
+    print(json.dumps(run(args.steps, layers=args.layers, profile=args.profile)))
 
 
 if __name__ == "__main__":
