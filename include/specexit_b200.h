@@ -209,6 +209,11 @@ typedef struct {
    * form.  tc_scratch >= spx_verify_tc_scratch_bytes(B, d, V) bytes. */
   const float *head_wmax;     /* (V) spx_head_stats                           */
   void *tc_scratch;
+  /* optional, tensor-core form only: the stable top-K ids (value desc, index
+   * asc; speculation.py:57-60) of each computed row's CDOT logits, (B, topk_k)
+   * row-major, 1 <= topk_k <= 64 -- the draft proposal without full logits. */
+  int32_t *topk_out;
+  int32_t topk_k;
 } spx_verify_args;
 #define SPX_VERIFY_TC_MIN_ROWS 8
 int spx_verify(const spx_verify_args *args, void *stream);

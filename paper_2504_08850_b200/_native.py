@@ -18,6 +18,7 @@ SPX_POLICY_MLP, SPX_POLICY_CONST = 0, 1
 SPX_VERIFY_TC_MIN_ROWS = 8               # include/specexit_b200.h
 ERR_ID_RANGE, ERR_HIDDEN_NONFINITE, ERR_LOGIT_NONFINITE, ERR_PREV_SUM, ERR_BAD_LAYER = 1, 2, 4, 8, 16
 ERR_ROW_CAP = 32
+ERR_CAND_OVERFLOW = 64
 
 # device error bits -> the reference's ValueError messages
 ERR_MESSAGES = [
@@ -27,6 +28,7 @@ ERR_MESSAGES = [
     (ERR_PREV_SUM, "prev_local_probs must sum to 1"),             # predictor.py:49-50
     (ERR_BAD_LAYER, "exit layer out of range"),                   # scheduler.py:69-70
     (ERR_ROW_CAP, "layer call selected more rows than its row capacity"),
+    (ERR_CAND_OVERFLOW, "tensor-core verify: too many near-maximal logits to re-evaluate"),
 ]
 
 _vp = ctypes.c_void_p
@@ -56,7 +58,7 @@ class VerifyArgs(ctypes.Structure):
                 ("done_out", _vp), ("exit_layer_out", _vp), ("full_heads", _vp),
                 ("layer", _i32), ("scratch", _vp), ("counter", _vp), ("mode", _i32),
                 ("err", _vp), ("B", _i64), ("d", _i64), ("V", _i64),
-                ("head_wmax", _vp), ("tc_scratch", _vp)]
+                ("head_wmax", _vp), ("tc_scratch", _vp), ("topk_out", _vp), ("topk_k", _i32)]
 
 
 class OnlineStateC(ctypes.Structure):

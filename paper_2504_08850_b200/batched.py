@@ -138,10 +138,17 @@ class BatchedExitEngine:
         for l in range(self.draft.config.num_layers):
             ds.launch_layer(l)
         dh = ds.pending[n0:n0 + B]
-        launch_verify(verify_args(self.draft, dh, B, self.dtok, scratch, counter, self.err,
-                                  logits_out=self.dlogits, mode=mode))
-        N.check(lib.spx_topk_rows(N.ptr(self.dlogits), B, self.draft.config.vocab_size, K,
-                                  N.ptr(self.spec), s()), "spx_topk_rows")
+        # the K draft ids straight from K4 (tensor-core form: stable top-K of
+        # the CDOT logits, no full-logit round trip), else full logits + top-K
+        a = verify_args(self.draft, dh, B, self.dtok, scratch, counter, self.err, mode=mode,
+                        topk_out=self.spec, topk_k=K)
+        if a.tc_scratch and mode != N.SPX_MODE_STRICT:
+            launch_verify(a)
+        else:
+            launch_verify(verify_args(self.draft, dh, B, self.dtok, scratch, counter, self.err,
+                                      logits_out=self.dlogits, mode=mode))
+            N.check(lib.spx_topk_rows(N.ptr(self.dlogits), B, self.draft.config.vocab_size, K,
+                                      N.ptr(self.spec), s()), "spx_topk_rows")
         # schedule (scheduler.py:95-102), all streams
         if self.config.schedule_mode == "all":
             mask, m = 0, 0

@@ -36,6 +36,7 @@ struct VerParams {
   unsigned long long *scratch; unsigned int *counter;
   int mode; int *err;
   int B, d, V;
+  int32_t *topk_out; int topk_k;
 };
 
 __device__ __forceinline__ bool ver_row_on(const VerParams &p, int r) {
@@ -513,17 +514,21 @@ extern "C" int spx_verify(const spx_verify_args *a, void *stream_) {
   p.logits_out = a->logits_out; p.done_out = a->done_out; p.exit_layer_out = a->exit_layer_out;
   p.full_heads = a->full_heads; p.layer = a->layer; p.scratch = a->scratch; p.counter = a->counter;
   p.mode = a->mode; p.err = a->err; p.B = (int)a->B; p.d = (int)a->d; p.V = (int)a->V;
+  p.topk_out = nullptr; p.topk_k = 0;
   // many gated rows, FAST, bf16 head: the tensor-core form (spx_verify_tc.cuh)
   static const int env_tc = getenv("SPX_VERIFY_TC") ? atoi(getenv("SPX_VERIFY_TC")) : 1;
   if (env_tc && a->tc_scratch && a->head_wmax && a->mode != SPX_MODE_STRICT &&
       a->head_dtype == SPX_DTYPE_BF16 && !a->logits_out && a->d % TV_BK == 0 &&
       a->B >= SPX_VERIFY_TC_MIN_ROWS && a->B <= 0x7fff) {
+    if (a->topk_out && (a->topk_k < 1 || a->topk_k > 64 || a->topk_k > a->V)) return SPX_EINVAL;
+    p.topk_out = a->topk_out; p.topk_k = a->topk_out ? a->topk_k : 0;
     bool ok = false;
     if (dispatch_cpl((int)a->d, VerifyTcLaunch{&p, a->head_wmax,
                                                reinterpret_cast<uint8_t *>(a->tc_scratch), stream,
                                                &ok}) && ok)
       return spx_launch_status("spx_verify(tc)");
   }
+  if (a->topk_out) return SPX_EINVAL;               // top-K only in the tensor-core form
   const size_t smem = (size_t)VER_ROWS * a->d * sizeof(float);
   const int nchunk = (int)(a->d / CHUNK);
   const int warps_per_cta = VER_THREADS / 32;

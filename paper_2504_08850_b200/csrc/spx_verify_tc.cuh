@@ -222,24 +222,32 @@ __global__ void __launch_bounds__(TV_THREADS, 1) tcv_gemm_kernel(
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * TV_NT));
 }
 
-// one CTA per compacted row: the tensor-core max, the candidates, their exact
-// CDOT logits, the argmax and verify_kernel's row finalisation
+// one CTA per compacted row: the tensor-core top keys, the candidates, their
+// exact CDOT logits, the argmax (and the stable top-K when topk_k > 0) and
+// verify_kernel's row finalisation.  With Kt = max(topk_k, 1) tensor-core
+// winners, T = the Kt-th largest tensor-core logit and E = the largest bound
+// e_v among the winners, every member of the exact top-Kt has tl_v + e_v >=
+// T - E (Kt elements have exact logits >= T - E), so it is a candidate.
+constexpr int TV_CAND = 1024;
 template <typename TW, int CPL>
 __global__ void __launch_bounds__(VER_THREADS) tcv_select_kernel(VerParams p,
                                                                  const float *head_wmax,
                                                                  const uint8_t *scratch) {
   extern __shared__ float hn[];
   __shared__ unsigned long long s_key[VER_THREADS / 32];
-  __shared__ float s_e;
+  __shared__ unsigned long long s_cand[TV_CAND];
+  __shared__ int s_nc;
+  __shared__ float s_thr;
   const TvLayout L = tv_layout(p.B, p.d, p.V);
   const int nrows = *reinterpret_cast<const volatile int32_t *>(scratch);
   const int i = blockIdx.x;
   if (i >= nrows) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = VER_THREADS / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = VER_THREADS / 32;
   const int row = reinterpret_cast<const int32_t *>(scratch + L.rows)[i];
   const float S = reinterpret_cast<const float *>(scratch + L.s)[i];
   const float *tl = reinterpret_cast<const float *>(scratch + L.tl) + (size_t)i * p.V;
   const TW *head = reinterpret_cast<const TW *>(p.head);
+  const int Kt = p.topk_k > 0 ? p.topk_k : 1;
   if (warp == 0) {
     int bad = 0;
     float rr = 1.f;
@@ -247,43 +255,50 @@ __global__ void __launch_bounds__(VER_THREADS) tcv_select_kernel(VerParams p,
                         &rr, &bad);
     if (lane == 0) hn[p.d] = rr;
   }
-  // tensor-core argmax (value, lowest index)
-  unsigned long long best = 0ull;
-  for (int v = threadIdx.x; v < p.V; v += VER_THREADS) {
-    const unsigned long long k = argmax_key(tl[v], (uint32_t)v);
-    best = k > best ? k : best;
-  }
-#pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) {
-    const unsigned long long o = __shfl_xor_sync(0xffffffffu, best, m);
-    best = o > best ? o : best;
-  }
-  if (lane == 0) s_key[warp] = best;
+  if (tid == 0) s_nc = 0;
   __syncthreads();
   const float r = hn[p.d];
   const float du = 4.f * (float)p.d * 5.9604645e-8f;          // 4 d u
   const float u4 = 4.f * 5.9604645e-8f;
-  if (threadIdx.x == 0) {
+  auto bound = [&](int v, float t) {
+    const float bwv = p.head_bw ? p.head_bw[v] : 0.f;
+    return r * du * head_wmax[v] * S + u4 * (fabsf(t) + fabsf(bwv));
+  };
+  auto block_max = [&](unsigned long long k) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(0xffffffffu, k, m);
+      k = o > k ? o : k;
+    }
+    if (lane == 0) s_key[warp] = k;
+    __syncthreads();
     unsigned long long b = 0ull;
     for (int w = 0; w < nw; ++w) b = s_key[w] > b ? s_key[w] : b;
-    const int vh = (int)(0xffffffffu - (uint32_t)(b & 0xffffffffull));
-    const float M = f32_from_order_key((uint32_t)(b >> 32));
-    const float bwh = p.head_bw ? p.head_bw[vh] : 0.f;
-    const float eh = r * du * head_wmax[vh] * S + u4 * (fabsf(M) + fabsf(bwh));
-    s_e = M - eh;                                              // threshold before e_v
+    __syncthreads();
+    return b;
+  };
+  // the Kt largest tensor-core keys, one block max per round
+  unsigned long long below = ~0ull, last = 0ull;
+  float E = 0.f;
+  for (int q = 0; q < Kt; ++q) {
+    unsigned long long best = 0ull;
+    for (int v = tid; v < p.V; v += VER_THREADS) {
+      const unsigned long long k = argmax_key(tl[v], (uint32_t)v);
+      if (k < below && k > best) best = k;
+    }
+    last = block_max(best);
+    below = last;
+    const int vw = (int)(0xffffffffu - (uint32_t)(last & 0xffffffffull));
+    E = fmaxf(E, bound(vw, f32_from_order_key((uint32_t)(last >> 32))));
   }
-  __syncthreads();
-  const float thr = s_e;
-  // candidates: tl_v + e_v >= M - e_vhat, re-evaluated exactly (warp per candidate)
-  best = 0ull;
+  const float thr = f32_from_order_key((uint32_t)(last >> 32)) - E;
+  // candidates, re-evaluated exactly (warp per candidate), keys into s_cand
   for (int base = warp * 32; base < p.V; base += nw * 32) {
     const int v = base + lane;
     bool cand = false;
     if (v < p.V) {
       const float t = tl[v];
-      const float bwv = p.head_bw ? p.head_bw[v] : 0.f;
-      const float ev = r * du * head_wmax[v] * S + u4 * (fabsf(t) + fabsf(bwv));
-      cand = t + ev >= thr || !(t == t);
+      cand = t + bound(v, t) >= thr || !(t == t);
     }
     unsigned m = __ballot_sync(0xffffffffu, cand);
     while (m) {
@@ -293,17 +308,31 @@ __global__ void __launch_bounds__(VER_THREADS) tcv_select_kernel(VerParams p,
       warp_cdot<TW, 1, CPL>(head + (size_t)vc * p.d, hn, p.d, 1, lane, &lg);
       const float bw = p.head_bw ? p.head_bw[vc] : 0.f;
       lg = __fadd_rn(__fmul_rn(r, lg), bw);
-      const unsigned long long k = argmax_key(lg, (uint32_t)vc);
-      best = k > best ? k : best;
+      if (lane == 0) {
+        const int slot = atomicAdd(&s_nc, 1);
+        if (slot < TV_CAND) s_cand[slot] = argmax_key(lg, (uint32_t)vc);
+      }
     }
   }
-  if (lane == 0) s_key[warp] = best;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long k = 0ull;
-    for (int w = 0; w < nw; ++w) k = s_key[w] > k ? s_key[w] : k;
-    const int tok = (int)(0xffffffffu - (uint32_t)(k & 0xffffffffull));
-    const float mx = f32_from_order_key((uint32_t)(k >> 32));
+  const int nc = s_nc < TV_CAND ? s_nc : TV_CAND;
+  if (s_nc > TV_CAND && tid == 0) atomicOr(p.err, ERR_CAND_OVERFLOW);
+  // exact top-Kt of the candidates (stable: value desc, index asc)
+  below = ~0ull;
+  unsigned long long top = 0ull;
+  for (int q = 0; q < Kt; ++q) {
+    unsigned long long best = 0ull;
+    for (int c = tid; c < nc; c += VER_THREADS)
+      if (s_cand[c] < below && s_cand[c] > best) best = s_cand[c];
+    const unsigned long long k = block_max(best);
+    if (q == 0) top = k;
+    below = k;
+    if (p.topk_out && tid == 0)
+      p.topk_out[(size_t)row * p.topk_k + q] = (int32_t)(0xffffffffu - (uint32_t)(k & 0xffffffffull));
+  }
+  if (tid == 0) {
+    const int tok = (int)(0xffffffffu - (uint32_t)(top & 0xffffffffull));
+    const float mx = f32_from_order_key((uint32_t)(top >> 32));
     bool in = false;
     if (p.spec_ptr)
       for (int j = p.spec_ptr[row]; j < p.spec_ptr[row + 1]; ++j) in |= (p.spec_ids[j] == tok);

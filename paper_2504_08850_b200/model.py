@@ -480,6 +480,8 @@ def verify_args(model: TransformerModel, hidden: torch.Tensor, B: int, token_out
             and model.config.hidden_dim % 64 == 0 and kw.get("logits_out") is None):
         a.head_wmax = N.ptr(model.head_wmax)
         a.tc_scratch = N.ptr(_verify_tc_scratch(B, model.config.hidden_dim, model.config.vocab_size))
+        if kw.get("topk_out") is not None:
+            a.topk_out, a.topk_k = N.ptr(kw["topk_out"]), int(kw["topk_k"])
     return a
 
 

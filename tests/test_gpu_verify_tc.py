@@ -96,3 +96,40 @@ def test_verify_tc_exact_ties_and_near_ties():
     for k in a:
         assert np.array_equal(a[k], b[k]), k
     assert (a["tok"] == np.arange(B)).all() and (a["ver"] == 1).all()
+
+
+@pytest.mark.parametrize("V,d,B,K", [(32000, 5120, 64, 4), (32000, 4096, 16, 16),
+                                     (8192, 4096, 24, 64)])
+def test_verify_tc_topk_equals_full_logits_topk(V, d, B, K):
+    """The draft proposal's top-K from K4's tensor-core form equals the stable
+    top-K (speculation.py:57-60) of the CUDA-core full logits, id for id."""
+    m = _head(V, d, 3)
+    g = torch.Generator(device="cuda").manual_seed(B * K)
+    h = torch.randn((B, d), device="cuda", generator=g)
+    if K == 64:                                   # exact ties inside the top-K
+        m = spx.init_model(spx.ModelConfig(V, d, 1, 8, 64, 16, 9), dtype="bf16", head_only=True)
+        m.lm_head[V - 64:] = m.lm_head[:64]
+        m.finalize()
+        h = m.lm_head[:B].float() * 30 + 0.01 * torch.randn((B, d), device="cuda", generator=g)
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    scratch, counter = _VerifyScratch.get(B)
+    logits = torch.empty((B, V), dtype=torch.float32, device="cuda")
+    tok_a = torch.empty(B, dtype=torch.int32, device="cuda")
+    tok_b = torch.empty(B, dtype=torch.int32, device="cuda")
+    ids_a = torch.empty((B, K), dtype=torch.int32, device="cuda")
+    ids_b = torch.full((B, K), -1, dtype=torch.int32, device="cuda")
+    with numerics.using("fast"):
+        launch_verify(verify_args(m, h, B, tok_a, scratch, counter, err, logits_out=logits))
+        N.check(N.lib().spx_topk_rows(N.ptr(logits), B, V, K, N.ptr(ids_a), N.stream_ptr()),
+                "spx_topk_rows")
+        a = verify_args(m, h, B, tok_b, scratch, counter, err, topk_out=ids_b, topk_k=K)
+        assert a.tc_scratch
+        launch_verify(a)
+    torch.cuda.synchronize()
+    assert err.item() == 0
+    ia, ib = ids_a.cpu().numpy(), ids_b.cpu().numpy()
+    assert np.array_equal(ia, ib)
+    assert np.array_equal(tok_a.cpu().numpy(), tok_b.cpu().numpy())
+    assert np.array_equal(ia[:, 0], tok_b.cpu().numpy())
+    ref = np.argsort(-logits.cpu().numpy(), axis=1, kind="stable")[:, :K]
+    assert np.array_equal(ref, ia)
