@@ -494,9 +494,7 @@ static void launch_layer_tcgen05(const LayerParams &p, int sms, cudaStream_t s) 
     cudaFuncSetAttribute(tcl_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
   tcl_rows_kernel<<<1, 512, rsm, s>>>(p);
   tcl_matrix<EPI_QKV>(p, 3 * p.d, p.d, Npad, sms, s);
-  const size_t ab = (size_t)(p.att_cap + p.row_cap) * 4 + (size_t)(p.d / p.nh) * 4;
-  cudaFuncSetAttribute(attn_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);
-  launch_pdl(attn_fast_kernel, 2 * sms, AT, ab, s, p);
+  launch_attn_fast(p, sms, s, true);
   tcl_matrix<EPI_WO>(p, p.d, p.d, Npad, sms, s);
   tcl_matrix<EPI_FFN1>(p, p.ffn, p.d, Npad, sms, s);
   tcl_matrix<EPI_FFN2>(p, p.d, p.ffn, Npad, sms, s);

@@ -467,6 +467,124 @@ __global__ void __launch_bounds__(AT) attn_fast_kernel(LayerParams p) {
   }
 }
 
+// Head dim 128 (Llama2-7B / 13B): the same attention with the key loops
+// latency-hidden -- each warp takes 4 keys per iteration (4 independent
+// 512-byte K/V row loads in flight instead of one dependent chain), lane =
+// 4 consecutive head dims, the P.V partials of the 4 warps summed in shared
+// memory.  GROWS: the row set comes from tcl_rows_kernel (p.rows / *p.nrows)
+// instead of a per-CTA frontier scan.
+template <bool GROWS>
+__global__ void __launch_bounds__(AT) attn_fast128_kernel(LayerParams p) {
+  constexpr int DH = 128, NW = AT / 32;
+  extern __shared__ __align__(16) float asmem[];
+  float *scores = asmem;                            // att_cap
+  float *red = scores + (p.att_cap + 3) / 4 * 4;    // NW * DH
+  int *rows = reinterpret_cast<int *>(red + NW * DH);   // row_cap (!GROWS)
+  __shared__ float s_red[NW];
+  __shared__ float s_bc;
+  pdl_wait();
+  if (flag_set(p.done)) return;
+  pdl_trigger();
+  int nrows;
+  const int *rowp;
+  if (GROWS) {
+    nrows = *reinterpret_cast<const volatile int32_t *>(p.nrows);
+    rowp = p.rows;
+  } else {
+    nrows = cta_row_set(p, rows);
+    rowp = rows;
+  }
+  const int d = p.d, nh = p.nh;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const float scale = (float)(1.0 / sqrt((double)DH));
+  for (int item = blockIdx.x; item < nrows * nh; item += gridDim.x) {
+    const int row = rowp[item / nh], h = item % nh;
+    const float4 q = __ldcg(reinterpret_cast<const float4 *>(p.s_q + (size_t)row * d + h * DH) + lane);
+    const int *ctx = nullptr;
+    int nctx = row + 1;
+    if (p.attn_ptr && p.attn_ptr[row + 1] > p.attn_ptr[row]) {
+      ctx = p.attn_idx + p.attn_ptr[row];
+      nctx = p.attn_ptr[row + 1] - p.attn_ptr[row];
+    }
+    float mloc = -INFINITY;
+    for (int j0 = 4 * w; j0 < nctx; j0 += 4 * NW) {
+      float4 kv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int jj = j0 + u < nctx ? j0 + u : j0;
+        const int pos = ctx ? ctx[jj] : jj;
+        kv[u] = __ldcg(reinterpret_cast<const float4 *>(p.kc + (size_t)pos * d + h * DH) + lane);
+      }
+      float acc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        acc[u] = fmaf(kv[u].x, q.x, fmaf(kv[u].y, q.y, fmaf(kv[u].z, q.z, kv[u].w * q.w)));
+#pragma unroll
+      for (int m = 16; m; m >>= 1)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], m);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (j0 + u < nctx) {
+          const float sc = acc[u] * scale;
+          if (lane == 0) scores[j0 + u] = sc;
+          mloc = fmaxf(mloc, sc);
+        }
+    }
+    if (lane == 0) s_red[w] = mloc;
+    __syncthreads();
+    if (tid == 0) {
+      float m = s_red[0];
+      for (int j = 1; j < NW; ++j) m = fmaxf(m, s_red[j]);
+      s_bc = m;
+    }
+    __syncthreads();
+    const float m = s_bc;
+    float sl = 0.f;
+    for (int jj = tid; jj < nctx; jj += AT) {
+      const float e = np_expf(scores[jj] - m);
+      scores[jj] = e;
+      sl += e;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sl += __shfl_xor_sync(0xffffffffu, sl, o);
+    __syncthreads();
+    if (lane == 0) s_red[w] = sl;
+    // P.V: warp w takes keys w, w + NW, ... four at a time
+    float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j0 = w; j0 < nctx; j0 += 4 * NW) {
+      float4 vv[4];
+      float sc[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int jj = j0 + u * NW;
+        const int js = jj < nctx ? jj : j0;
+        const int pos = ctx ? ctx[js] : js;
+        vv[u] = __ldcg(reinterpret_cast<const float4 *>(p.vc + (size_t)pos * d + h * DH) + lane);
+        sc[u] = jj < nctx ? scores[jj] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        o4.x = fmaf(sc[u], vv[u].x, o4.x);
+        o4.y = fmaf(sc[u], vv[u].y, o4.y);
+        o4.z = fmaf(sc[u], vv[u].z, o4.z);
+        o4.w = fmaf(sc[u], vv[u].w, o4.w);
+      }
+    }
+    reinterpret_cast<float4 *>(red + w * DH)[lane] = o4;
+    __syncthreads();
+    const float inv = 1.0f / (((s_red[0] + s_red[1]) + s_red[2]) + s_red[3]);
+    if (tid < DH) {
+      const float a = ((red[tid] + red[DH + tid]) + red[2 * DH + tid]) + red[3 * DH + tid];
+      p.s_att[(size_t)row * d + h * DH + tid] = a * inv;
+    }
+    __syncthreads();
+  }
+}
+
+// attention launch for the fast layer paths (dh == 128: attn_fast128_kernel)
+static void launch_attn_fast(const LayerParams &p, int sms, cudaStream_t s, bool grows);
+
 template <typename K, typename... Args>
 static void launch_pdl(K kern, int grid, int block, size_t smem, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -549,22 +667,36 @@ static void launch_layer_fast(const LayerParams &p, int sms, cudaStream_t s) {
   static const int env_tc = getenv("SPX_LAYER_TC") ? atoi(getenv("SPX_LAYER_TC")) : 1;
   if (std::is_same<TW, __nv_bfloat16>::value && env_tc && tc_layer_supported(p)) {
     launch_tc<EPI_QKV>(p, 3 * p.d, p.d, sms, s);
-    const size_t ab = (size_t)(p.att_cap + p.row_cap) * 4 + (size_t)(p.d / p.nh) * 4;
-    cudaFuncSetAttribute(attn_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);
-    launch_pdl(attn_fast_kernel, 2 * sms, AT, ab, s, p);
+    launch_attn_fast(p, sms, s, false);
     launch_tc<EPI_WO>(p, p.d, p.d, sms, s);
     launch_tc<EPI_FFN1>(p, p.ffn, p.d, sms, s);
     launch_tc<EPI_FFN2>(p, p.d, p.ffn, sms, s);
     return;
   }
   launch_gemv<TW, EPI_QKV>(p, 3 * p.d, p.d, sms, s);
-  const size_t asm_bytes = (size_t)(p.att_cap + p.row_cap) * 4 + (size_t)(p.d / p.nh) * 4;
-  cudaFuncSetAttribute(attn_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)asm_bytes);
-  launch_pdl(attn_fast_kernel, 2 * sms, AT, asm_bytes, s, p);
+  launch_attn_fast(p, sms, s, false);
   launch_gemv<TW, EPI_WO>(p, p.d, p.d, sms, s);
   launch_gemv<TW, EPI_FFN1>(p, p.ffn, p.d, sms, s);
   launch_gemv<TW, EPI_FFN2>(p, p.d, p.ffn, sms, s);
+}
+
+static void launch_attn_fast(const LayerParams &p, int sms, cudaStream_t s, bool grows) {
+  static const int env = getenv("SPX_ATTN128") ? atoi(getenv("SPX_ATTN128")) : 1;
+  if (env && p.d / p.nh == 128 && p.d % p.nh == 0) {
+    const size_t ab = (size_t)((p.att_cap + 3) / 4 * 4) * 4 + (size_t)(AT / 32) * 128 * 4 +
+                      (grows ? 0 : (size_t)p.row_cap * 4);
+    if (grows) {
+      cudaFuncSetAttribute(attn_fast128_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);
+      launch_pdl(attn_fast128_kernel<true>, 2 * sms, AT, ab, s, p);
+    } else {
+      cudaFuncSetAttribute(attn_fast128_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);
+      launch_pdl(attn_fast128_kernel<false>, 2 * sms, AT, ab, s, p);
+    }
+    return;
+  }
+  const size_t ab = (size_t)(p.att_cap + p.row_cap) * 4 + (size_t)(p.d / p.nh) * 4;
+  cudaFuncSetAttribute(attn_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);
+  launch_pdl(attn_fast_kernel, 2 * sms, AT, ab, s, p);
 }
 
 }  // namespace spx
