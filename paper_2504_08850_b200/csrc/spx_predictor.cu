@@ -156,7 +156,13 @@ __global__ void features_wide_kernel(const float *logits, const float *prev, flo
     }
     __syncthreads();
   }
-  const float psum = tid == 0 ? np_pairwise_sum(0, K, [&](int i) { return pv[i]; }) : 0.f;
+  constexpr int MAXLEAF = 2560;                 // K <= ~150k without the serial fallback
+  __shared__ int2 s_leaf[MAXLEAF];
+  __shared__ float s_lsum[MAXLEAF];
+  __shared__ int s_nleaf;
+  __shared__ float s_psum;
+  const float psum = np_pairwise_sum_cta(0, K, [&](int i) { return pv[i]; }, s_leaf, s_lsum,
+                                         MAXLEAF, &s_nleaf, &s_psum);
   if (tid == 0) {
     int e = 0;
     if (s_bad) e |= ERR_LOGIT_NONFINITE;

@@ -1,0 +1,39 @@
+"""extract_features for wide speculative sets (K > 64: the spec_full_vocab
+ablation and the tree's full-vocabulary draft probabilities, engine.py:166-168,
+predictor.py:42-52) against the oracle, bit for bit: the softmax with the
+strict denominator chain and numpy's pairwise prev-sum check (now summed by
+the whole CTA, leaf blocks in parallel) -- including the uniform prior at
+V = 32000 / 128000 that a sequential sum would wrongly reject."""
+import numpy as np
+import pytest
+
+import paper_2504_08850_b200 as spx
+from paper_2504_08850_b200 import numerics
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("K", [65, 1000, 32000, 128000])
+def test_wide_features_bit_exact(oracle, K):
+    rs = np.random.default_rng(K)
+    lg = (rs.standard_normal(K) * 3).astype(np.float32)
+    prev = np.full(K, np.float32(1.0 / K), np.float32)            # uniform prior
+    ref = oracle.extract_features(lg, prev)
+    with numerics.using("strict"):
+        fv = spx.extract_features(lg, prev)
+    assert np.array_equal(fv.local_probs.cpu().numpy(), ref.local_probs)
+    assert np.array_equal(fv.prob_variation.cpu().numpy(), ref.prob_variation)
+    # a random prior summing to 1 in numpy's pairwise order
+    p = rs.random(K).astype(np.float32)
+    p /= p.sum(dtype=np.float32)
+    if abs(float(p.sum()) - 1.0) <= 1e-5:
+        ref = oracle.extract_features(lg, p)
+        fv = spx.extract_features(lg, p)
+        assert np.array_equal(fv.prob_variation.cpu().numpy(), ref.prob_variation)
+    # off by more than the reference tolerance -> the reference's ValueError
+    bad = prev.copy()
+    bad[0] += np.float32(3e-5)
+    with pytest.raises(ValueError, match="sum to 1"):
+        oracle.extract_features(lg, bad)
+    with pytest.raises(ValueError, match="sum to 1"):
+        spx.extract_features(lg, bad)
