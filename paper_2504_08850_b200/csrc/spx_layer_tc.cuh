@@ -262,7 +262,7 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
 }
 
 template <int EPI>
-__global__ void __launch_bounds__(TT_THREADS, 1) tcl_tma_kernel(
+__global__ void __launch_bounds__(TT_THREADS, 2) tcl_tma_kernel(
     const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
     LayerParams p, int nout, int kin, int Npad, int nbox, int stages, float *partial) {
   extern __shared__ __align__(1024) uint8_t tlsm[];
@@ -443,7 +443,7 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
   // (rows_hint), bounded by the partial buffer and >= 8 K-blocks per split
   const int otiles = (nout + TL_M - 1) / TL_M;
   const int nt_exp = (p.rows_hint + TL_NT - 1) / TL_NT;
-  int nks = sms / (otiles * (nt_exp > 0 ? nt_exp : 1));    // one wave (1 CTA per SM)
+  int nks = sms / (otiles * (nt_exp > 0 ? nt_exp : 1));    // one wave (1 CTA per SM; cp.async form)
   nks = nks < 1 ? 1 : nks > 8 ? 8 : nks;
   while (nks > 1 && ((size_t)nks * Npad * nout * 4 > TL_PARTIAL_BYTES || kin / TL_BK / nks < 8))
     --nks;
@@ -458,13 +458,37 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
   }
   // SPX_TCL_TMA=0 (A/B): the cp.async form below
   static const int env_tma = getenv("SPX_TCL_TMA") ? atoi(getenv("SPX_TCL_TMA")) : 1;
-  const int nbox = Npad < TL_NT ? Npad : TL_NT;
+  // row tile sized by the rows this call expects (rows_hint), not the state's
+  // capacity: the B operand (two parts) is loaded box-sized per stage
+  const int rows_exp = p.rows_hint > 16 ? (p.rows_hint + 15) / 16 * 16 : 16;
+  int nbox = Npad < TL_NT ? Npad : TL_NT;
+  nbox = rows_exp < nbox ? rows_exp : nbox;
   CUtensorMap tmW, tmX;
   if (env_tma && tl_tensor_map(&tmW, gemv_weights_host<EPI>(p), (uint64_t)nout, (uint64_t)kin, TL_M) &&
       tl_tensor_map(&tmX, parts, (uint64_t)TL_PARTS * Npad, (uint64_t)kin, (uint32_t)nbox)) {
     const size_t stage = TL_TILE_A + (size_t)TL_PARTS * nbox * 128;
-    int stages = (int)((227 * 1024 - 1024) / stage);
+    // two CTAs per SM (two independent TMA -> UMMA pipelines per SM, and a
+    // K split that fills one wave of 2 x 148 CTAs) when at least 2 stages fit
+    // in half the shared memory (measured: 2 x 2 stages beat 1 x 4 stages at
+    // 128-row tiles, 78 vs 113 us for the 13B QKV at 256 rows), else one
+    // CTA per SM with a deep ring
+    const int nt0 = (rows_exp + nbox - 1) / nbox;
+    int per_sm = 2;
+    int stages = (int)((113 * 1024 - 1024) / stage);
+    static const int env_min2 = getenv("SPX_TCL_MIN2") ? atoi(getenv("SPX_TCL_MIN2")) : 2;
+    (void)nt0;
+    const int min_stages = env_min2;
+    if (stages < min_stages) {
+      per_sm = 1;
+      stages = (int)((227 * 1024 - 1024) / stage);
+    }
     stages = stages > TT_MAX_STAGES ? TT_MAX_STAGES : stages;
+    // K split: the expected live CTAs fill one wave of per_sm CTAs per SM
+    const int nt = (rows_exp + nbox - 1) / nbox;
+    nks = per_sm * sms / (otiles * nt);
+    nks = nks < 1 ? 1 : nks > 8 ? 8 : nks;
+    while (nks > 1 && ((size_t)nks * Npad * nout * 4 > TL_PARTIAL_BYTES || kin / TL_BK / nks < 8))
+      --nks;
     const size_t tsm = (size_t)stages * stage + 1024;
     cudaFuncSetAttribute(tcl_tma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
     dim3 tgrid((unsigned)otiles, (unsigned)((Npad + nbox - 1) / nbox), (unsigned)nks);

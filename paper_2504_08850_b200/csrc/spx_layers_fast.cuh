@@ -467,21 +467,18 @@ __global__ void __launch_bounds__(AT) attn_fast_kernel(LayerParams p) {
   }
 }
 
-// Head dim 128 (Llama2-7B / 13B): the same attention with the key loops
-// latency-hidden -- each warp takes 4 keys per iteration (4 independent
-// 512-byte K/V row loads in flight instead of one dependent chain), lane =
-// 4 consecutive head dims, the P.V partials of the 4 warps summed in shared
-// memory.  GROWS: the row set comes from tcl_rows_kernel (p.rows / *p.nrows)
-// instead of a per-CTA frontier scan.
+// Head dim 128 (Llama2-7B / 13B): the same attention, one WARP per
+// (row, head) item (no CTA barrier per item; 4 items in flight per CTA), the
+// key loops latency-hidden -- 4 keys per iteration (4 independent 512-byte
+// K/V row loads in flight), lane = 4 consecutive head dims.  GROWS: the row
+// set comes from tcl_rows_kernel (p.rows / *p.nrows) instead of a per-CTA
+// frontier scan.
 template <bool GROWS>
 __global__ void __launch_bounds__(AT) attn_fast128_kernel(LayerParams p) {
   constexpr int DH = 128, NW = AT / 32;
   extern __shared__ __align__(16) float asmem[];
-  float *scores = asmem;                            // att_cap
-  float *red = scores + (p.att_cap + 3) / 4 * 4;    // NW * DH
-  int *rows = reinterpret_cast<int *>(red + NW * DH);   // row_cap (!GROWS)
-  __shared__ float s_red[NW];
-  __shared__ float s_bc;
+  const int sstride = (p.att_cap + 3) / 4 * 4;
+  int *rows = reinterpret_cast<int *>(asmem + NW * sstride);   // row_cap (!GROWS)
   pdl_wait();
   if (flag_set(p.done)) return;
   pdl_trigger();
@@ -495,9 +492,10 @@ __global__ void __launch_bounds__(AT) attn_fast128_kernel(LayerParams p) {
     rowp = rows;
   }
   const int d = p.d, nh = p.nh;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float *scores = asmem + w * sstride;
   const float scale = (float)(1.0 / sqrt((double)DH));
-  for (int item = blockIdx.x; item < nrows * nh; item += gridDim.x) {
+  for (int item = blockIdx.x * NW + w; item < nrows * nh; item += gridDim.x * NW) {
     const int row = rowp[item / nh], h = item % nh;
     const float4 q = __ldcg(reinterpret_cast<const float4 *>(p.s_q + (size_t)row * d + h * DH) + lane);
     const int *ctx = nullptr;
@@ -506,8 +504,8 @@ __global__ void __launch_bounds__(AT) attn_fast128_kernel(LayerParams p) {
       ctx = p.attn_idx + p.attn_ptr[row];
       nctx = p.attn_ptr[row + 1] - p.attn_ptr[row];
     }
-    float mloc = -INFINITY;
-    for (int j0 = 4 * w; j0 < nctx; j0 += 4 * NW) {
+    float m = -INFINITY;
+    for (int j0 = 0; j0 < nctx; j0 += 4) {
       float4 kv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -520,44 +518,34 @@ __global__ void __launch_bounds__(AT) attn_fast128_kernel(LayerParams p) {
       for (int u = 0; u < 4; ++u)
         acc[u] = fmaf(kv[u].x, q.x, fmaf(kv[u].y, q.y, fmaf(kv[u].z, q.z, kv[u].w * q.w)));
 #pragma unroll
-      for (int m = 16; m; m >>= 1)
+      for (int o = 16; o; o >>= 1)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], m);
+        for (int u = 0; u < 4; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         if (j0 + u < nctx) {
           const float sc = acc[u] * scale;
           if (lane == 0) scores[j0 + u] = sc;
-          mloc = fmaxf(mloc, sc);
+          m = fmaxf(m, sc);
         }
     }
-    if (lane == 0) s_red[w] = mloc;
-    __syncthreads();
-    if (tid == 0) {
-      float m = s_red[0];
-      for (int j = 1; j < NW; ++j) m = fmaxf(m, s_red[j]);
-      s_bc = m;
-    }
-    __syncthreads();
-    const float m = s_bc;
+    __syncwarp();
     float sl = 0.f;
-    for (int jj = tid; jj < nctx; jj += AT) {
+    for (int jj = lane; jj < nctx; jj += 32) {
       const float e = np_expf(scores[jj] - m);
       scores[jj] = e;
       sl += e;
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) sl += __shfl_xor_sync(0xffffffffu, sl, o);
-    __syncthreads();
-    if (lane == 0) s_red[w] = sl;
-    // P.V: warp w takes keys w, w + NW, ... four at a time
+    __syncwarp();
     float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int j0 = w; j0 < nctx; j0 += 4 * NW) {
+    for (int j0 = 0; j0 < nctx; j0 += 4) {
       float4 vv[4];
       float sc[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int jj = j0 + u * NW;
+        const int jj = j0 + u;
         const int js = jj < nctx ? jj : j0;
         const int pos = ctx ? ctx[js] : js;
         vv[u] = __ldcg(reinterpret_cast<const float4 *>(p.vc + (size_t)pos * d + h * DH) + lane);
@@ -571,14 +559,10 @@ __global__ void __launch_bounds__(AT) attn_fast128_kernel(LayerParams p) {
         o4.w = fmaf(sc[u], vv[u].w, o4.w);
       }
     }
-    reinterpret_cast<float4 *>(red + w * DH)[lane] = o4;
-    __syncthreads();
-    const float inv = 1.0f / (((s_red[0] + s_red[1]) + s_red[2]) + s_red[3]);
-    if (tid < DH) {
-      const float a = ((red[tid] + red[DH + tid]) + red[2 * DH + tid]) + red[3 * DH + tid];
-      p.s_att[(size_t)row * d + h * DH + tid] = a * inv;
-    }
-    __syncthreads();
+    const float inv = 1.0f / sl;
+    o4.x *= inv; o4.y *= inv; o4.z *= inv; o4.w *= inv;
+    reinterpret_cast<float4 *>(p.s_att + (size_t)row * d + h * DH)[lane] = o4;
+    __syncwarp();
   }
 }
 
@@ -683,11 +667,11 @@ static void launch_layer_fast(const LayerParams &p, int sms, cudaStream_t s) {
 static void launch_attn_fast(const LayerParams &p, int sms, cudaStream_t s, bool grows) {
   static const int env = getenv("SPX_ATTN128") ? atoi(getenv("SPX_ATTN128")) : 1;
   if (env && p.d / p.nh == 128 && p.d % p.nh == 0) {
-    const size_t ab = (size_t)((p.att_cap + 3) / 4 * 4) * 4 + (size_t)(AT / 32) * 128 * 4 +
+    const size_t ab = (size_t)(AT / 32) * ((p.att_cap + 3) / 4 * 4) * 4 +
                       (grows ? 0 : (size_t)p.row_cap * 4);
     if (grows) {
       cudaFuncSetAttribute(attn_fast128_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);
-      launch_pdl(attn_fast128_kernel<true>, 2 * sms, AT, ab, s, p);
+      launch_pdl(attn_fast128_kernel<true>, 8 * sms, AT, ab, s, p);
     } else {
       cudaFuncSetAttribute(attn_fast128_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);
       launch_pdl(attn_fast128_kernel<false>, 2 * sms, AT, ab, s, p);
