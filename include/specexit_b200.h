@@ -381,6 +381,12 @@ typedef struct {
 /* stable top-K (value desc, lower id on ties) of n logits
  * (speculation.py:57-60 topk_from_logits). K <= 64. */
 int spx_topk(const float *logits, int64_t n, int32_t K, int32_t *ids_out, void *stream);
+/* softmax_1d (src/specexit/model.py:149-152) of each of `rows` rows of n
+ * logits, evaluated at the K ids ids[r*K + j] (speculation.py:80-84
+ * draft_probs): bit-identical to extract_features' local probabilities with
+ * the strict denominator chain.  Non-finite logits set ERR bit 4. */
+int spx_softmax_pick(const float *logits, int64_t rows, int64_t n, const int32_t *ids,
+                     int32_t K, float *probs_out, int32_t *err, void *stream);
 /* spx_topk for `rows` independent rows of n logits (row-major), K ids each. */
 int spx_topk_rows(const float *logits, int64_t rows, int64_t n, int32_t K, int32_t *ids_out,
                   void *stream);

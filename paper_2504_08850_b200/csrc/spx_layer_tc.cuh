@@ -428,7 +428,11 @@ inline size_t tcl_scratch_bytes(int d, int ffn, int row_cap) {
 
 inline bool tcl_supported(const LayerParams &p) {
   static const int env = getenv("SPX_LAYER_TCGEN05") ? atoi(getenv("SPX_LAYER_TCGEN05")) : 1;
-  return env && p.tc_scratch && p.rows_hint >= 16 && p.d % TL_BK == 0 && p.ffn % TL_BK == 0;
+  // SPX_TCL_MIN_ROWS: smallest row count routed here (the 8-row mma.sync
+  // slices below it re-stream nothing for <= 8 rows but run ~2x slower per
+  // byte than the TMA-fed UMMA GEMM)
+  static const int min_rows = getenv("SPX_TCL_MIN_ROWS") ? atoi(getenv("SPX_TCL_MIN_ROWS")) : 3;
+  return env && p.tc_scratch && p.rows_hint >= min_rows && p.d % TL_BK == 0 && p.ffn % TL_BK == 0;
 }
 
 template <int EPI>

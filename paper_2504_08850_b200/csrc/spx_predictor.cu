@@ -180,6 +180,64 @@ __global__ void features_wide_kernel(const float *logits, const float *prev, flo
   }
 }
 
+// softmax_1d (model.py:149-152) of each row of n logits, evaluated only at K
+// requested ids (the draft proposal's probabilities, speculation.py:80-84):
+// the same max, np_expf and strict left-to-right denominator as
+// features_wide_kernel -- bit-identical probabilities -- without the
+// prev-sum check and the 3n feature writes.  The chain runs on thread 0 over
+// shared-memory chunks that warps 1.. fill one chunk ahead.
+__global__ void __launch_bounds__(256) softmax_pick_kernel(const float *logits, int n,
+                                                           const int32_t *ids, int K,
+                                                           float *probs_out, int *err) {
+  constexpr int WCH = 2048;
+  __shared__ float s_e[2][WCH];
+  __shared__ float s_red[8];
+  __shared__ int s_bad;
+  __shared__ float s_sum;
+  const int row = blockIdx.x, tid = threadIdx.x;
+  const float *x = logits + (size_t)row * n;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  float m = -INFINITY;
+  for (int i = tid; i < n; i += blockDim.x) {
+    const float v = x[i];
+    if (!is_finite(v)) s_bad = 1;
+    m = fmaxf(m, v);
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((tid & 31) == 0) s_red[tid >> 5] = m;
+  __syncthreads();
+  m = s_red[0];
+  for (int w = 1; w < 8; ++w) m = fmaxf(m, s_red[w]);
+  const int nch = (n + WCH - 1) / WCH;
+  for (int i = tid; i < (n < WCH ? n : WCH); i += blockDim.x) s_e[0][i] = np_expf(__fsub_rn(x[i], m));
+  __syncthreads();
+  float esum = 0.f;
+  for (int c = 0; c < nch; ++c) {
+    if (tid == 0) {
+      const int len = n - c * WCH < WCH ? n - c * WCH : WCH;
+      const float *e = s_e[c & 1];
+#pragma unroll 8
+      for (int j = 0; j < len; ++j) esum = __fadd_rn(esum, e[j]);
+    } else if (tid >= 32 && c + 1 < nch) {
+      const int b = (c + 1) * WCH, len = n - b < WCH ? n - b : WCH;
+      for (int j = tid - 32; j < len; j += blockDim.x - 32)
+        s_e[(c + 1) & 1][j] = np_expf(__fsub_rn(x[b + j], m));
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    s_sum = esum;
+    if (s_bad) atomicOr(err, ERR_LOGIT_NONFINITE);
+  }
+  __syncthreads();
+  for (int j = tid; j < K; j += blockDim.x) {
+    const int id = ids[(size_t)row * K + j];
+    probs_out[(size_t)row * K + j] = __fdiv_rn(np_expf(__fsub_rn(x[id], m)), s_sum);
+  }
+}
+
 __global__ void mlp_kernel(PredParams p, const float *feats_in) {
   const int row = blockIdx.x;
   if (row >= p.B) return;
@@ -469,6 +527,17 @@ extern "C" int spx_extract_features(const float *logits, const float *prev, floa
   features_kernel<<<(unsigned)B, 32, 0, (cudaStream_t)stream>>>(
       logits, const_cast<float *>(prev), feats_out, err, (int)B, (int)K);
   return spx_launch_status("spx_extract_features");
+}
+
+extern "C" int spx_softmax_pick(const float *logits, int64_t rows, int64_t n,
+                                const int32_t *ids, int32_t K, float *probs_out, int32_t *err,
+                                void *stream) {
+  if (!logits || !ids || !probs_out || !err || rows < 0 || n < 1 || n > (1 << 30) || K < 1)
+    return SPX_EINVAL;
+  if (rows == 0) return 0;
+  softmax_pick_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>(logits, (int)n, ids, K,
+                                                                         probs_out, err);
+  return spx_launch_status("spx_softmax_pick");
 }
 
 extern "C" int spx_predictor_mlp(const float *feats, const float *w1, const float *b1,

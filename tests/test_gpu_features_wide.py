@@ -37,3 +37,23 @@ def test_wide_features_bit_exact(oracle, K):
         oracle.extract_features(lg, bad)
     with pytest.raises(ValueError, match="sum to 1"):
         spx.extract_features(lg, bad)
+
+
+@pytest.mark.parametrize("n,V,K", [(1, 1000, 4), (10, 32000, 8), (3, 128000, 64)])
+def test_softmax_pick_equals_feature_probs(n, V, K):
+    """spx_softmax_pick (the draft proposal's probabilities) == the feature
+    kernel's softmax (softmax_device, one-hot prior) at the same ids, bit for bit."""
+    import torch
+    from paper_2504_08850_b200 import _native as N
+    from paper_2504_08850_b200.speculation import softmax_device
+    rs = np.random.default_rng(V + n)
+    lg = torch.as_tensor((rs.standard_normal((n, V)) * 4).astype(np.float32), device="cuda")
+    ids = torch.as_tensor(rs.integers(0, V, size=(n, K)).astype(np.int32), device="cuda")
+    out = torch.empty((n, K), dtype=torch.float32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.check(N.lib().spx_softmax_pick(N.ptr(lg), n, V, N.ptr(ids), K, N.ptr(out), N.ptr(err),
+                                     N.stream_ptr()), "spx_softmax_pick")
+    assert err.item() == 0
+    for r in range(n):
+        full = softmax_device(lg[r].contiguous())
+        assert torch.equal(out[r], full[ids[r].long()])
