@@ -49,6 +49,8 @@ inline int tl_npad(const LayerParams &p) { return (p.row_cap + 15) / 16 * 16; }
 
 // the row set once per call, into p.rows / *p.nrows (global)
 __global__ void __launch_bounds__(512) tcl_rows_kernel(LayerParams p) {
+  pdl_wait();
+  pdl_trigger();
   if (flag_set(p.done)) return;
   extern __shared__ int trows[];
   const int n = cta_row_set(p, trows);
@@ -61,6 +63,8 @@ __global__ void __launch_bounds__(512) tcl_rows_kernel(LayerParams p) {
 template <int EPI>
 __global__ void __launch_bounds__(256) tcl_prep_kernel(LayerParams p, int kin, int Npad,
                                                      __nv_bfloat16 *parts) {
+  pdl_wait();
+  pdl_trigger();
   if (flag_set(p.done)) return;
   const int n = *reinterpret_cast<const volatile int32_t *>(p.nrows);
   const bool ln = EPI == EPI_QKV || EPI == EPI_FFN1;
@@ -271,25 +275,52 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tcl_tma_kernel(
   __shared__ uint64_t all_done;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (flag_set(p.done)) return;
-  const int nrows = *reinterpret_cast<const volatile int32_t *>(p.nrows);
+  __shared__ int s_go;
   const int o0 = blockIdx.x * TL_M, n0 = blockIdx.y * nbox;
-  if (n0 >= nrows) return;
   const int kbt = kin / TL_BK, ks = blockIdx.z, nks = gridDim.z;
   const int kb0 = (int)((long long)ks * kbt / nks), kb1 = (int)((long long)(ks + 1) * kbt / nks);
   const int nkb = kb1 - kb0;
   const uint32_t tile_b = (uint32_t)nbox * 128u;
   const uint32_t stage_bytes = (uint32_t)TL_TILE_A + TL_PARTS * tile_b;
+  // the weights do not depend on the previous kernels: the first stages'
+  // weight blocks are requested before griddepcontrol.wait (programmatic
+  // dependent launch), the row parts after it
+  // (only tiles within the rows this call expects: the state's capacity may
+  // hold many more tiles that stay empty)
+  const int rows_exp = p.rows_hint > 16 ? (p.rows_hint + 15) / 16 * 16 : 16;
+  const int pre = n0 < rows_exp ? (nkb < stages ? nkb : stages) : 0;
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(&all_done, 1);
+    fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+    for (int i = 0; i < pre; ++i) {
+        mbar_arrive_expect_tx(&full[i], stage_bytes);
+        tma_load_2d(ring + (size_t)i * stage_bytes, &tmW, (kb0 + i) * TL_BK, o0, &full[i]);
+      }
   }
-  fence_mbar_init();
+  pdl_wait();
+  pdl_trigger();
+  if (tid == 0) {
+    const int nrows0 = *reinterpret_cast<const volatile int32_t *>(p.nrows);
+    s_go = !flag_set(p.done) && n0 < nrows0;
+    // complete the prefetched stages (their row parts) either way; drain
+    // them if this CTA has nothing to do
+    for (int i = 0; i < pre; ++i)
+#pragma unroll
+      for (int pp = 0; pp < TL_PARTS; ++pp)
+        tma_load_2d(ring + (size_t)i * stage_bytes + TL_TILE_A + pp * tile_b, &tmX,
+                    (kb0 + i) * TL_BK, pp * Npad + n0, &full[i]);
+    if (!s_go)
+      for (int i = 0; i < pre; ++i) mbar_wait(&full[i], 0);
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const int nrows = *reinterpret_cast<const volatile int32_t *>(p.nrows);
   if (warp == 5) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                  ::"r"(smem_u32(&tmem_base)), "n"(2 * TL_NT));
@@ -301,7 +332,7 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tcl_tma_kernel(
   const uint32_t tmem = tmem_base;
   if (warp == 4) {
     if (lane == 0) {
-      for (int i = 0; i < nkb; ++i) {
+      for (int i = pre; i < nkb; ++i) {
         const int s = i % stages;
         if (i >= stages) mbar_wait(&empty[s], ((i / stages) - 1) & 1);
         uint8_t *st = ring + (size_t)s * stage_bytes;
@@ -389,6 +420,8 @@ static bool tl_tensor_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint64
 template <int EPI>
 __global__ void __launch_bounds__(256) tcl_reduce_kernel(LayerParams p, int nout, int Npad,
                                                        int nks, const float *partial) {
+  pdl_wait();
+  pdl_trigger();
   if (flag_set(p.done)) return;
   const int n = *reinterpret_cast<const volatile int32_t *>(p.nrows);
   const long long total = (long long)n * nout;
@@ -403,6 +436,8 @@ __global__ void __launch_bounds__(256) tcl_reduce_kernel(LayerParams p, int nout
 
 // frontier of the advanced rows, newest-row copy (model.py:269-270), reset
 __global__ void tcl_finish_kernel(LayerParams p) {
+  pdl_wait();
+  pdl_trigger();
   if (flag_set(p.done)) return;
   const int n = *reinterpret_cast<const volatile int32_t *>(p.nrows);
   for (int i = threadIdx.x; i < n; i += blockDim.x) p.frontier[p.rows[i]] = p.layer + 1;
@@ -441,8 +476,8 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
   __nv_bfloat16 *parts = reinterpret_cast<__nv_bfloat16 *>(p.tc_scratch);
   float *partial = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(p.tc_scratch) +
                                              tcl_parts_bytes(p.d, p.ffn, p.row_cap));
-  tcl_prep_kernel<EPI><<<p.row_cap < 2 * sms ? p.row_cap : 2 * sms, 256, 0, s>>>(p, kin, Npad,
-                                                                                parts);
+  launch_pdl(tcl_prep_kernel<EPI>, p.row_cap < 2 * sms ? p.row_cap : 2 * sms, 256, 0, s, p, kin,
+             Npad, parts);
   // K split so that the live CTAs (expected row tiles) fill one wave
   // (rows_hint), bounded by the partial buffer and >= 8 K-blocks per split
   const int otiles = (nout + TL_M - 1) / TL_M;
@@ -496,8 +531,19 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
     const size_t tsm = (size_t)stages * stage + 1024;
     cudaFuncSetAttribute(tcl_tma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
     dim3 tgrid((unsigned)otiles, (unsigned)((Npad + nbox - 1) / nbox), (unsigned)nks);
-    tcl_tma_kernel<EPI><<<tgrid, TT_THREADS, tsm, s>>>(tmW, tmX, p, nout, kin, Npad, nbox, stages,
-                                                       partial);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = tgrid;
+    cfg.blockDim = dim3(TT_THREADS);
+    cfg.dynamicSmemBytes = tsm;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    static const int env_pdl = getenv("SPX_PDL_LAYERS") ? atoi(getenv("SPX_PDL_LAYERS")) : 1;
+    cfg.numAttrs = env_pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, tcl_tma_kernel<EPI>, tmW, tmX, p, nout, kin, Npad, nbox, stages,
+                       partial);
   } else {
   dim3 grid((unsigned)otiles, (unsigned)((Npad + TL_NT - 1) / TL_NT), (unsigned)nks);
   // SPX_TCL_AHEAD (A/B): K-blocks in flight ahead of the MMA (3 leaves one
@@ -511,7 +557,8 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
   if (nks > 1) {
     const long long work = (long long)(p.rows_hint > 0 ? p.rows_hint : 1) * nout;
     const int rg = (int)((work + 255) / 256 < 8 * sms ? (work + 255) / 256 : 8 * sms);
-    tcl_reduce_kernel<EPI><<<rg, 256, 0, s>>>(p, nout, Npad, nks, partial);
+    launch_pdl(tcl_reduce_kernel<EPI>, rg, 256, 0, s, p, nout, Npad, nks,
+               static_cast<const float *>(partial));
   }
 }
 
@@ -520,13 +567,13 @@ static void launch_layer_tcgen05(const LayerParams &p, int sms, cudaStream_t s) 
   const size_t rsm = (size_t)p.row_cap * 4;
   if (rsm > 48 * 1024)
     cudaFuncSetAttribute(tcl_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
-  tcl_rows_kernel<<<1, 512, rsm, s>>>(p);
+  launch_pdl(tcl_rows_kernel, 1, 512, rsm, s, p);
   tcl_matrix<EPI_QKV>(p, 3 * p.d, p.d, Npad, sms, s);
   launch_attn_fast(p, sms, s, true);
   tcl_matrix<EPI_WO>(p, p.d, p.d, Npad, sms, s);
   tcl_matrix<EPI_FFN1>(p, p.ffn, p.d, Npad, sms, s);
   tcl_matrix<EPI_FFN2>(p, p.d, p.ffn, Npad, sms, s);
-  tcl_finish_kernel<<<1, 256, 0, s>>>(p);
+  launch_pdl(tcl_finish_kernel, 1, 256, 0, s, p);
 }
 
 }  // namespace spx

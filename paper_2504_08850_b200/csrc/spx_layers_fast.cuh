@@ -580,7 +580,9 @@ static void launch_pdl(K kern, int grid, int block, size_t smem, cudaStream_t s,
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  // SPX_PDL_LAYERS=0 (A/B): plain stream order for the multi-row layer kernels
+  static const int env_pdl = getenv("SPX_PDL_LAYERS") ? atoi(getenv("SPX_PDL_LAYERS")) : 1;
+  cfg.numAttrs = env_pdl ? 1 : 0;
   cudaLaunchKernelEx(&cfg, kern, args...);
 }
 

@@ -468,7 +468,11 @@ static void launch_verify1(const VerParams &p, cudaStream_t stream) {
     if (sm1 > 48 * 1024)
       cudaFuncSetAttribute(verify1_kernel<TW, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)sm1);
-    verify1_kernel<TW, CPL><<<2 * num_sms(), VER_THREADS, sm1, stream>>>(p);
+    // SPX_VERIFY1_PER_SM: CTAs per SM (1 leaves room for the next layer
+    // kernel's CTA -- ~200 KB of shared memory -- to become resident and
+    // prefetch its weights while a no-op gated verify drains)
+    static const int per_sm = getenv("SPX_VERIFY1_PER_SM") ? atoi(getenv("SPX_VERIFY1_PER_SM")) : 2;
+    verify1_kernel<TW, CPL><<<per_sm * num_sms(), VER_THREADS, sm1, stream>>>(p);
   }
 }
 

@@ -2,6 +2,8 @@
 device-resident ExitEngine: tok/s of graph replays (device-timed) and of
 generate() end to end.  Iteration tool; bench.py carries the contract line."""
 import argparse
+import os
+import sys
 import json
 import time
 
@@ -41,6 +43,7 @@ def main():
     ap.add_argument("--thr", type=float, default=0.5)
     ap.add_argument("--mode", default="two-level")
     ap.add_argument("--numerics", default="fast")
+    ap.add_argument("--profile", default=None, help="path: per-kernel table of 8 token replays")
     args = ap.parse_args()
     numerics.set_mode(args.numerics)
     t0 = time.time()
@@ -63,6 +66,11 @@ def main():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     recs = eng._dev.records(args.tokens)
+    if args.profile:
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+        from kernel_table import kernel_table
+        eng.start(prompt)
+        kernel_table(lambda: [g.replay() for _ in range(8)], args.profile)
     el = np.mean([r.exit_layer for r in recs])
     fires = np.mean([r.predictor_fired for r in recs])
     ver = np.mean([r.verified for r in recs])
