@@ -29,6 +29,7 @@
 #pragma once
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <unordered_map>
 #include "spx_umma.cuh"
 
 namespace spx {
@@ -395,8 +396,34 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tcl_tma_kernel(
 }
 
 // 2-D bf16 tensor map, 64-element (128-byte) inner box, 128-byte swizzle
+static bool tl_tensor_map_encode(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t cols,
+                                 uint32_t box_rows);
+// encoded maps cached per (pointer, shape, box): the host cost of a layer call
+// matters where it is not graph-captured (the tree step)
+struct TlMapKey {
+  const void *ptr; uint64_t rows, cols; uint32_t box;
+  bool operator==(const TlMapKey &o) const {
+    return ptr == o.ptr && rows == o.rows && cols == o.cols && box == o.box;
+  }
+};
+struct TlMapHash {
+  size_t operator()(const TlMapKey &k) const {
+    return std::hash<const void *>()(k.ptr) ^ (k.rows * 0x9E3779B97F4A7C15ull) ^ (k.cols << 7) ^ k.box;
+  }
+};
 static bool tl_tensor_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t cols,
                           uint32_t box_rows) {
+  static std::unordered_map<TlMapKey, CUtensorMap, TlMapHash> cache;
+  const TlMapKey key{ptr, rows, cols, box_rows};
+  auto it = cache.find(key);
+  if (it != cache.end()) { *m = it->second; return true; }
+  if (!tl_tensor_map_encode(m, ptr, rows, cols, box_rows)) return false;
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, *m);
+  return true;
+}
+static bool tl_tensor_map_encode(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t cols,
+                                 uint32_t box_rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -529,7 +556,11 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
     while (nks > 1 && ((size_t)nks * Npad * nout * 4 > TL_PARTIAL_BYTES || kin / TL_BK / nks < 8))
       --nks;
     const size_t tsm = (size_t)stages * stage + 1024;
-    cudaFuncSetAttribute(tcl_tma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+    static size_t tsm_set = 0;
+    if (tsm > tsm_set) {
+      cudaFuncSetAttribute(tcl_tma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+      tsm_set = tsm;
+    }
     dim3 tgrid((unsigned)otiles, (unsigned)((Npad + nbox - 1) / nbox), (unsigned)nks);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = tgrid;

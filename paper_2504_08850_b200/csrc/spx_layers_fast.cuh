@@ -671,11 +671,18 @@ static void launch_attn_fast(const LayerParams &p, int sms, cudaStream_t s, bool
   if (env && p.d / p.nh == 128 && p.d % p.nh == 0) {
     const size_t ab = (size_t)(AT / 32) * ((p.att_cap + 3) / 4 * 4) * 4 +
                       (grows ? 0 : (size_t)p.row_cap * 4);
+    static size_t set_t = 0, set_f = 0;
     if (grows) {
-      cudaFuncSetAttribute(attn_fast128_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);
+      if (ab > set_t && ab > 48 * 1024) {
+        cudaFuncSetAttribute(attn_fast128_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);
+        set_t = ab;
+      }
       launch_pdl(attn_fast128_kernel<true>, 8 * sms, AT, ab, s, p);
     } else {
-      cudaFuncSetAttribute(attn_fast128_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);
+      if (ab > set_f && ab > 48 * 1024) {
+        cudaFuncSetAttribute(attn_fast128_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);
+        set_f = ab;
+      }
       launch_pdl(attn_fast128_kernel<false>, 2 * sms, AT, ab, s, p);
     }
     return;

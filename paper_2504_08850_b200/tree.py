@@ -350,6 +350,7 @@ class TreeEngine:
         preds = [None] * P
         evals = 0
         ran = False
+        frozen_keep = None
         for l in range(L):
             self.tstate.launch_layer(l)
             ran = True
@@ -395,13 +396,21 @@ class TreeEngine:
                 N.check(lib.spx_path_and(N.ptr(ver), N.ptr(d_path_ptr), N.ptr(d_path_nodes),
                                          N.ptr(path_fire), P, N.ptr(path_ok), stream),
                         "spx_path_and")
-                N.raise_device_error(int(err.item()) | int(self.tstate.err.item()))
-                ok = path_ok.cpu().numpy()
+                # one device->host read per active layer: error words, path
+                # flags, node tokens (and probabilities when recorded)
+                # (float64 holds every int32 word and the float64 probabilities exactly)
+                parts = [err.to(torch.float64), self.tstate.err.to(torch.float64),
+                         path_ok.to(torch.float64), tok.to(torch.float64)]
                 if self.record_probs:
-                    pr = prob.cpu().numpy()
+                    parts.append(prob)
+                hb = torch.cat(parts).cpu()
+                N.raise_device_error(int(hb[0]) | int(hb[1]))
+                ok = hb[2:2 + P].numpy() != 0
+                tk = hb[2 + P:2 + P + n_nodes].numpy().astype(np.int64)
+                if self.record_probs:
+                    pr = hb[2 + P + n_nodes:].numpy()
                     self.prob_log.extend([l, float(pr[j])] for j in live_nodes)
                 if ok.any():
-                    tk = tok.cpu().numpy()
                     for p in sorted(live):
                         if ok[p]:
                             exit_layer[p] = l
@@ -410,7 +419,9 @@ class TreeEngine:
                     live_mask.copy_(torch.as_tensor(
                         np.asarray([1 if p in live else 0 for p in range(P)], np.uint8)))
                 keep = {j for p in live for j in paths[p]} | ({0} if live else set())
-                self.tstate.freeze([rows[j] for j in range(n_nodes) if j not in keep])
+                if keep != frozen_keep:                  # the frozen set only grows on exits
+                    self.tstate.freeze([rows[j] for j in range(n_nodes) if j not in keep])
+                    frozen_keep = keep
             if not live:
                 break
         assert ran
