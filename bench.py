@@ -197,12 +197,17 @@ def cpu_reference_rate(head_dv, final_g, final_b, bank, ids, seconds, seed=7):
                 pass
             rng = np.random.default_rng(seed + p)
             hidden = rng.standard_normal((64, D)).astype(np.float32)
-            prev = np.full(K, np.float32(1.0 / K), np.float32)
+            hb = hidden.view(np.uint32)                      # bf16-valued rows (RNE), as the GPU arm
+            hidden = ((hb + 0x7FFF + ((hb >> 16) & 1)) & 0xFFFF0000).astype(np.uint32).view(np.float32)
+            uni = np.full(K, np.float32(1.0 / K), np.float32)
+            prev = uni
             n, t0 = 0, time.perf_counter()
             while time.perf_counter() - t0 < seconds:
                 l = n % PRED_LAYERS
-                _, prev2 = O.reference_chain(t, hidden[n % 64], ids[(n * 7 + p) % ids.shape[0]],
-                                             prev, bank[l], THRESHOLD, kern)
+                if l == 0:
+                    prev = uni                               # token start (engine.py:182-188)
+                _, prev = O.reference_chain(t, hidden[n % 64], ids[(n * 7 + p) % ids.shape[0]],
+                                            prev, bank[l], THRESHOLD, kern)
                 n += 1
             el = time.perf_counter() - t0
             os.write(w_fd, f"{n} {el}\n".encode())

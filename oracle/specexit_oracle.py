@@ -948,6 +948,11 @@ def reference_chain(t, hidden, ids, prev, w, threshold, kern=None):
     hn = xc / np.sqrt(var + LN_EPS)[..., None] * t["final_norm.g"] + t["final_norm.b"]
     cols = np.ascontiguousarray(t["lm_head"][:, ids])
     logits = mm(np.ascontiguousarray(hn, np.float32), cols)[0]
+    # extract_features' validation (predictor.py:47-50)
+    if not np.all(np.isfinite(logits)):
+        raise ValueError("non-finite speculative logits")
+    if abs(float(prev.sum()) - 1.0) > 1e-5:
+        raise ValueError("prev_local_probs must sum to 1")
     e = np.exp(logits - np.max(logits))
     local = e / ss(e[None, :])[0]
     f = np.concatenate([logits, local, local - prev]).astype(np.float32)
