@@ -47,6 +47,37 @@ constexpr size_t TL_TILE_B = (size_t)TL_NT * TL_BK * 2;
 constexpr size_t TL_STAGE = TL_TILE_A + TL_PARTS * TL_TILE_B;          // 48 KB
 
 inline int tl_npad(const LayerParams &p) { return (p.row_cap + 15) / 16 * 16; }
+__device__ __forceinline__ int tl_npad_dev(const LayerParams &p) { return (p.row_cap + 15) / 16 * 16; }
+
+// bytes of one row-part region (two bf16 planes of Npad x max(d, ffn)); the
+// scratch holds two regions (A: the QKV / Wo / FFN1 inputs, B: the FFN2
+// input, written by FFN1's epilogue while FFN1 still reads A) + the K-split
+// partials
+__host__ __device__ inline size_t tcl_parts_bytes(int d, int ffn, int row_cap) {
+  const size_t npad = (size_t)(row_cap + 15) / 16 * 16;
+  return ((size_t)TL_PARTS * npad * (size_t)(ffn > d ? ffn : d) * 2 + 255) / 256 * 256;
+}
+
+// the two bf16 parts of x (hi = RNE(x), lo = RNE(x - hi): tcl_prep_kernel's split)
+__device__ __forceinline__ void tl_put_parts(__nv_bfloat16 *parts, size_t plane, size_t idx,
+                                             float x) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(x);
+  parts[idx] = h;
+  parts[plane + idx] = __float2bfloat16_rn(x - __bfloat162float(h));
+}
+
+// the layer epilogue of output o of row-set entry n; FFN1 also emits FFN2's
+// input parts (relu(v + b1), no LayerNorm) into region B -- no FFN2 prep pass
+template <int EPI>
+__device__ __forceinline__ void tcl_epilogue(const LayerParams &p, int n, int o, float v) {
+  gemv_epilogue<EPI>(p, p.rows[n], o, v);
+  if (EPI == EPI_FFN1) {
+    const float z = __fadd_rn(v, p.b1[o]);
+    __nv_bfloat16 *pb = reinterpret_cast<__nv_bfloat16 *>(
+        reinterpret_cast<uint8_t *>(p.tc_scratch) + tcl_parts_bytes(p.d, p.ffn, p.row_cap));
+    tl_put_parts(pb, (size_t)tl_npad_dev(p) * p.ffn, (size_t)n * p.ffn + o, z > 0.f ? z : 0.f);
+  }
+}
 
 // the row set once per call, into p.rows / *p.nrows (global)
 __global__ void __launch_bounds__(512) tcl_rows_kernel(LayerParams p) {
@@ -230,7 +261,7 @@ __global__ void __launch_bounds__(TL_THREADS, 1) tcl_gemm_kernel(LayerParams p, 
       for (int j = 0; j < 32; ++j) {
         const int n = n0 + c0 + j;
         if (c0 + j < ntile && n < nrows) {
-          if (nks == 1) gemv_epilogue<EPI>(p, p.rows[n], my_o, __uint_as_float(v[j]));
+          if (nks == 1) tcl_epilogue<EPI>(p, n, my_o, __uint_as_float(v[j]));
           else partial[((size_t)ks * Npad + n) * nout + my_o] = __uint_as_float(v[j]);
         }
       }
@@ -277,8 +308,11 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tcl_tma_kernel(
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __shared__ int s_go;
-  const int o0 = blockIdx.x * TL_M, n0 = blockIdx.y * nbox;
-  const int kbt = kin / TL_BK, ks = blockIdx.z, nks = gridDim.z;
+  // grid (output tiles, K splits, row tiles): the row tile is the slowest
+  // index, so every live tile is scheduled before the (usually empty) tiles
+  // of rows beyond this call's expected count
+  const int o0 = blockIdx.x * TL_M, n0 = blockIdx.z * nbox;
+  const int kbt = kin / TL_BK, ks = blockIdx.y, nks = gridDim.y;
   const int kb0 = (int)((long long)ks * kbt / nks), kb1 = (int)((long long)(ks + 1) * kbt / nks);
   const int nkb = kb1 - kb0;
   const uint32_t tile_b = (uint32_t)nbox * 128u;
@@ -382,7 +416,7 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tcl_tma_kernel(
         for (int j = 0; j < 32; ++j) {
           const int n = n0 + c0 + j;
           if (c0 + j < nbox && n < nrows) {
-            if (nks == 1) gemv_epilogue<EPI>(p, p.rows[n], my_o, __uint_as_float(v[j]));
+            if (nks == 1) tcl_epilogue<EPI>(p, n, my_o, __uint_as_float(v[j]));
             else partial[((size_t)ks * Npad + n) * nout + my_o] = __uint_as_float(v[j]);
           }
         }
@@ -457,7 +491,7 @@ __global__ void __launch_bounds__(256) tcl_reduce_kernel(LayerParams p, int nout
     const int r = (int)(e / nout), o = (int)(e % nout);
     float s = 0.f;
     for (int k = 0; k < nks; ++k) s += __ldcg(partial + ((size_t)k * Npad + r) * nout + o);
-    gemv_epilogue<EPI>(p, p.rows[r], o, s);
+    tcl_epilogue<EPI>(p, r, o, s);
   }
 }
 
@@ -480,12 +514,8 @@ __global__ void tcl_finish_kernel(LayerParams p) {
 
 constexpr size_t TL_PARTIAL_BYTES = 96ull << 20;      // K-split partial sums
 
-inline size_t tcl_parts_bytes(int d, int ffn, int row_cap) {
-  const size_t npad = (size_t)(row_cap + 15) / 16 * 16;
-  return ((size_t)TL_PARTS * npad * (size_t)(ffn > d ? ffn : d) * 2 + 255) / 256 * 256;
-}
 inline size_t tcl_scratch_bytes(int d, int ffn, int row_cap) {
-  return tcl_parts_bytes(d, ffn, row_cap) + TL_PARTIAL_BYTES;
+  return 2 * tcl_parts_bytes(d, ffn, row_cap) + TL_PARTIAL_BYTES;
 }
 
 inline bool tcl_supported(const LayerParams &p) {
@@ -499,12 +529,14 @@ inline bool tcl_supported(const LayerParams &p) {
 
 template <int EPI>
 static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sms,
-                       cudaStream_t s) {
-  __nv_bfloat16 *parts = reinterpret_cast<__nv_bfloat16 *>(p.tc_scratch);
-  float *partial = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(p.tc_scratch) +
-                                             tcl_parts_bytes(p.d, p.ffn, p.row_cap));
-  launch_pdl(tcl_prep_kernel<EPI>, p.row_cap < 2 * sms ? p.row_cap : 2 * sms, 256, 0, s, p, kin,
-             Npad, parts);
+                       cudaStream_t s, bool prep = true) {
+  const size_t pbytes = tcl_parts_bytes(p.d, p.ffn, p.row_cap);
+  __nv_bfloat16 *parts = reinterpret_cast<__nv_bfloat16 *>(
+      reinterpret_cast<uint8_t *>(p.tc_scratch) + (EPI == EPI_FFN2 ? pbytes : 0));
+  float *partial = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(p.tc_scratch) + 2 * pbytes);
+  if (prep)
+    launch_pdl(tcl_prep_kernel<EPI>, p.row_cap < 2 * sms ? p.row_cap : 2 * sms, 256, 0, s, p, kin,
+               Npad, parts);
   // K split so that the live CTAs (expected row tiles) fill one wave
   // (rows_hint), bounded by the partial buffer and >= 8 K-blocks per split
   const int otiles = (nout + TL_M - 1) / TL_M;
@@ -561,7 +593,7 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
       cudaFuncSetAttribute(tcl_tma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
       tsm_set = tsm;
     }
-    dim3 tgrid((unsigned)otiles, (unsigned)((Npad + nbox - 1) / nbox), (unsigned)nks);
+    dim3 tgrid((unsigned)otiles, (unsigned)nks, (unsigned)((Npad + nbox - 1) / nbox));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = tgrid;
     cfg.blockDim = dim3(TT_THREADS);
@@ -600,10 +632,12 @@ static void launch_layer_tcgen05(const LayerParams &p, int sms, cudaStream_t s) 
     cudaFuncSetAttribute(tcl_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
   launch_pdl(tcl_rows_kernel, 1, 512, rsm, s, p);
   tcl_matrix<EPI_QKV>(p, 3 * p.d, p.d, Npad, sms, s);
-  launch_attn_fast(p, sms, s, true);
-  tcl_matrix<EPI_WO>(p, p.d, p.d, Npad, sms, s);
+  // head dim 128: the attention kernel emits Wo's input parts itself;
+  // FFN1's epilogue emits FFN2's
+  const bool att_parts = launch_attn_fast(p, sms, s, true);
+  tcl_matrix<EPI_WO>(p, p.d, p.d, Npad, sms, s, !att_parts);
   tcl_matrix<EPI_FFN1>(p, p.ffn, p.d, Npad, sms, s);
-  tcl_matrix<EPI_FFN2>(p, p.d, p.ffn, Npad, sms, s);
+  tcl_matrix<EPI_FFN2>(p, p.d, p.ffn, Npad, sms, s, false);
   launch_pdl(tcl_finish_kernel, 1, 256, 0, s, p);
 }
 

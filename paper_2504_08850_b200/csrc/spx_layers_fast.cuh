@@ -562,12 +562,28 @@ __global__ void __launch_bounds__(AT) attn_fast128_kernel(LayerParams p) {
     const float inv = 1.0f / sl;
     o4.x *= inv; o4.y *= inv; o4.z *= inv; o4.w *= inv;
     reinterpret_cast<float4 *>(p.s_att + (size_t)row * d + h * DH)[lane] = o4;
+    if (GROWS) {
+      // the tcgen05 path: Wo's input row parts (hi / lo bf16, row-set order)
+      // straight from here instead of a prep pass over s_att
+      __nv_bfloat16 *pa = reinterpret_cast<__nv_bfloat16 *>(p.tc_scratch);
+      const size_t plane = (size_t)((p.row_cap + 15) / 16 * 16) * d;
+      const size_t base = (size_t)(item / nh) * d + h * DH + 4 * lane;
+      const float ov[4] = {o4.x, o4.y, o4.z, o4.w};
+      __nv_bfloat16 hv[4], lv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        hv[e] = __float2bfloat16_rn(ov[e]);
+        lv[e] = __float2bfloat16_rn(ov[e] - __bfloat162float(hv[e]));
+      }
+      *reinterpret_cast<uint2 *>(pa + base) = *reinterpret_cast<uint2 *>(hv);
+      *reinterpret_cast<uint2 *>(pa + plane + base) = *reinterpret_cast<uint2 *>(lv);
+    }
     __syncwarp();
   }
 }
 
 // attention launch for the fast layer paths (dh == 128: attn_fast128_kernel)
-static void launch_attn_fast(const LayerParams &p, int sms, cudaStream_t s, bool grows);
+static bool launch_attn_fast(const LayerParams &p, int sms, cudaStream_t s, bool grows);
 
 template <typename K, typename... Args>
 static void launch_pdl(K kern, int grid, int block, size_t smem, cudaStream_t s, Args... args) {
@@ -666,7 +682,8 @@ static void launch_layer_fast(const LayerParams &p, int sms, cudaStream_t s) {
   launch_gemv<TW, EPI_FFN2>(p, p.d, p.ffn, sms, s);
 }
 
-static void launch_attn_fast(const LayerParams &p, int sms, cudaStream_t s, bool grows) {
+// returns true when the launched kernel also wrote Wo's input parts (grows)
+static bool launch_attn_fast(const LayerParams &p, int sms, cudaStream_t s, bool grows) {
   static const int env = getenv("SPX_ATTN128") ? atoi(getenv("SPX_ATTN128")) : 1;
   if (env && p.d / p.nh == 128 && p.d % p.nh == 0) {
     const size_t ab = (size_t)(AT / 32) * ((p.att_cap + 3) / 4 * 4) * 4 +
@@ -685,11 +702,12 @@ static void launch_attn_fast(const LayerParams &p, int sms, cudaStream_t s, bool
       }
       launch_pdl(attn_fast128_kernel<false>, 2 * sms, AT, ab, s, p);
     }
-    return;
+    return grows;
   }
   const size_t ab = (size_t)(p.att_cap + p.row_cap) * 4 + (size_t)(p.d / p.nh) * 4;
   cudaFuncSetAttribute(attn_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ab);
   launch_pdl(attn_fast_kernel, 2 * sms, AT, ab, s, p);
+  return false;
 }
 
 }  // namespace spx
