@@ -485,13 +485,21 @@ __global__ void __launch_bounds__(256) tcl_reduce_kernel(LayerParams p, int nout
   pdl_trigger();
   if (flag_set(p.done)) return;
   const int n = *reinterpret_cast<const volatile int32_t *>(p.nrows);
-  const long long total = (long long)n * nout;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(e / nout), o = (int)(e % nout);
-    float s = 0.f;
-    for (int k = 0; k < nks; ++k) s += __ldcg(partial + ((size_t)k * Npad + r) * nout + o);
-    tcl_epilogue<EPI>(p, r, o, s);
+  // grid (output quads, rows): 4 consecutive outputs per thread (16-byte
+  // partial loads, all splits in flight), rows strided by gridDim.y; the
+  // split order of the sum is unchanged (k = 0, 1, ...)
+  const int o = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (o >= nout) return;
+  for (int r = blockIdx.y; r < n; r += gridDim.y) {
+    float4 a = __ldcg(reinterpret_cast<const float4 *>(partial + (size_t)r * nout + o));
+    float sv[4] = {a.x, a.y, a.z, a.w};
+    sv[0] = 0.f + sv[0]; sv[1] = 0.f + sv[1]; sv[2] = 0.f + sv[2]; sv[3] = 0.f + sv[3];
+    for (int k = 1; k < nks; ++k) {
+      const float4 b = __ldcg(reinterpret_cast<const float4 *>(partial + ((size_t)k * Npad + r) * nout + o));
+      sv[0] += b.x; sv[1] += b.y; sv[2] += b.z; sv[3] += b.w;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) tcl_epilogue<EPI>(p, r, o + e, sv[e]);
   }
 }
 
@@ -620,8 +628,10 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
   if (nks > 1) {
     const long long work = (long long)(p.rows_hint > 0 ? p.rows_hint : 1) * nout;
     const int rg = (int)((work + 255) / 256 < 8 * sms ? (work + 255) / 256 : 8 * sms);
-    launch_pdl(tcl_reduce_kernel<EPI>, rg, 256, 0, s, p, nout, Npad, nks,
-               static_cast<const float *>(partial));
+    (void)rg;
+    const int rows_y = p.rows_hint > 0 ? (p.rows_hint < 256 ? p.rows_hint : 256) : 1;
+    launch_pdl(tcl_reduce_kernel<EPI>, dim3((unsigned)((nout / 4 + 255) / 256), (unsigned)rows_y),
+               256, 0, s, p, nout, Npad, nks, static_cast<const float *>(partial));
   }
 }
 

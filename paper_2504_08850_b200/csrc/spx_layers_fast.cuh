@@ -586,9 +586,9 @@ __global__ void __launch_bounds__(AT) attn_fast128_kernel(LayerParams p) {
 static bool launch_attn_fast(const LayerParams &p, int sms, cudaStream_t s, bool grows);
 
 template <typename K, typename... Args>
-static void launch_pdl(K kern, int grid, int block, size_t smem, cudaStream_t s, Args... args) {
+static void launch_pdl(K kern, dim3 grid, int block, size_t smem, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = grid;
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
