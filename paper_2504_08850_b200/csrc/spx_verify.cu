@@ -393,13 +393,19 @@ template <int CPL>
 __global__ void final_norm_kernel(const float *x, int64_t stride, const float *g, const float *b,
                                   float *hn, float *r_out, int N, int d, int mode,
                                   int layer_norm_out, int *err) {
+  // one warp per CTA and row; the row is normalised in shared memory (the
+  // element loops of warp_head_prep are dependent global round trips when
+  // run on a global buffer) and written out with coalesced 16-byte stores
+  extern __shared__ float fn_row[];
   const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int row = blockIdx.x;
   if (row >= N) return;
   int bad = 0;
   float r = 1.f;
-  warp_head_prep<CPL>(x + (size_t)row * stride, g, b, d, hn + (size_t)row * d, lane,
-                      mode == SPX_MODE_STRICT, &r, &bad, layer_norm_out != 0);
+  warp_head_prep<CPL>(x + (size_t)row * stride, g, b, d, fn_row, lane, mode == SPX_MODE_STRICT,
+                      &r, &bad, layer_norm_out != 0);
+  float4 *dst = reinterpret_cast<float4 *>(hn + (size_t)row * d);
+  for (int j = lane; j < d / 4; j += 32) dst[j] = reinterpret_cast<const float4 *>(fn_row)[j];
   if (lane == 0 && r_out) r_out[row] = r;
   if (bad && lane == 0) atomicOr(err, ERR_HIDDEN_NONFINITE);
 }
@@ -434,7 +440,10 @@ struct NormLaunch {
   const float *x; int64_t st; const float *g, *b; float *hn, *r; int N, d, mode, lno; int *err;
   unsigned grid; int threads; cudaStream_t stream;
   template <int CPL> void operator()() const {
-    final_norm_kernel<CPL><<<grid, threads, 0, stream>>>(x, st, g, b, hn, r, N, d, mode, lno, err);
+    const size_t sm = (size_t)d * sizeof(float);
+    if (sm > 48 * 1024)
+      cudaFuncSetAttribute(final_norm_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    final_norm_kernel<CPL><<<(unsigned)N, 32, sm, stream>>>(x, st, g, b, hn, r, N, d, mode, lno, err);
   }
 };
 
