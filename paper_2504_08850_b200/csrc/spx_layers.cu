@@ -505,27 +505,29 @@ __global__ void embed_kernel(const TW *emb, const float *pe, const int32_t *toke
                              const int32_t *pos_ids, int T, int d, int V, int max_ctx,
                              float *pending, int32_t *frontier, int32_t *n_ctx, int32_t *new_row,
                              const uint8_t *frozen_reset, int *err) {
+  // grid (rows, d / (4 * blockDim)): every thread owns 4 consecutive
+  // elements of one row (d % 4 == 0), so a single decode row is spread over
+  // d / 512 CTAs instead of one CTA's strided loop
   const int n0 = *n_ctx;
   for (int t = blockIdx.x; t < T; t += gridDim.x) {
     const int row = n0 + t;
     int tok = tokens[t];
     if (tok < 0 || tok >= V || row >= max_ctx) {
-      if (threadIdx.x == 0) atomicOr(err, ERR_ID_RANGE);
+      if (threadIdx.x == 0 && blockIdx.y == 0) atomicOr(err, ERR_ID_RANGE);
       continue;
     }
     const int pos = pos_ids ? pos_ids[t] : row;
     const TW *e = emb + (size_t)tok * d;
-    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    for (int j = 4 * (blockIdx.y * blockDim.x + threadIdx.x); j < d; j += 4 * blockDim.x * gridDim.y) {
       float w[4];
-      if ((j & 3) == 0 && j + 4 <= d) {
-        load4_f32<TW>(e + j, w);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (j + q < d) pending[(size_t)row * d + j + q] = __fadd_rn(w[q], pe[(size_t)pos * d + j + q]);
-        }
-      }
+      load4_f32<TW>(e + j, w);
+      const float4 pv = *reinterpret_cast<const float4 *>(pe + (size_t)pos * d + j);
+      float4 o;
+      o.x = __fadd_rn(w[0], pv.x); o.y = __fadd_rn(w[1], pv.y);
+      o.z = __fadd_rn(w[2], pv.z); o.w = __fadd_rn(w[3], pv.w);
+      *reinterpret_cast<float4 *>(pending + (size_t)row * d + j) = o;
     }
-    if (threadIdx.x == 0) frontier[row] = 0;
+    if (threadIdx.x == 0 && blockIdx.y == 0) frontier[row] = 0;
   }
   (void)frozen_reset;
 }
@@ -545,7 +547,7 @@ extern "C" int spx_embed(const void *embedding, int32_t w_dtype, const float *po
     return SPX_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   spx_debug_capture(s, "embed: entry");
-  const int grid = (int)(T < 1024 ? T : 1024);
+  const dim3 grid((unsigned)(T < 1024 ? T : 1024), (unsigned)((d + 511) / 512 < 16 ? (d + 511) / 512 : 16));
   if (w_dtype == SPX_DTYPE_BF16)
     embed_kernel<__nv_bfloat16><<<grid, 128, 0, s>>>((const __nv_bfloat16 *)embedding, pos_encoding,
                                                       tokens, pos_ids, (int)T, (int)d, (int)V,

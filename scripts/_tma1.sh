@@ -1,5 +1,3 @@
 cd $GRAFT_REPO_ROOT; export PYTHONPATH=$PWD; mkdir -p gpurun_out
-timeout 900 python scripts/batch_sweep.py --batches 1,2,4,8,16,32,64,128,256 --steps 6 > gpurun_out/f2_sweep.jsonl 2>&1; echo "sweep rc=$?" >> gpurun_out/f2_status.txt
-TAG=f2 bash scripts/gpu.sh bench benchref
-timeout 600 python scripts/tree_bench.py --steps 6 --profile gpurun_out/f2_kt_tree.txt > gpurun_out/f2_tree.log 2>&1; echo "tree rc=$?" >> gpurun_out/f2_status.txt
-timeout 600 python scripts/batch_sweep.py --batches 64,256 --steps 4 --profile gpurun_out/f2_kt > /dev/null 2>&1; echo "prof rc=$?" >> gpurun_out/f2_status.txt
+timeout 900 python -m pytest -q -m gpu tests/test_gpu_engine.py tests/test_gpu_batched.py tests/test_gpu_tree.py -x > gpurun_out/t22_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/t22_status.txt
+timeout 600 python scripts/decode_bench.py --tokens 64 --profile gpurun_out/t22_kt_decode.txt > gpurun_out/t22_decode.log 2>&1; echo "decode rc=$?" >> gpurun_out/t22_status.txt

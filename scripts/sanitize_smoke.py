@@ -1,7 +1,9 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck):
 the stream predictor kernel (d=4096, K=4, two CTAs per SM), the team kernel
 (tiny d), one device TreeEngine step and a few decode steps through the
-persistent layer kernel."""
+persistent layer kernel; the round-2 kernels (pipelined chain, tcgen05 K6,
+TMA-fed tcgen05 layer GEMMs, tensor-core K4 with top-K, head-dim-128
+attention, softmax_pick through the tree step)."""
 import os
 import sys
 
@@ -74,5 +76,15 @@ st2.check()
 be = spx.BatchedExitEngine(t, d, E.PredictorPolicy(bank), E.EngineConfig(threshold=0.5),
                            batch=17, context=16)
 be.generate([[84, 104, 101, 32]] * 17, 2)
+# round 2, later: head dim 128 (warp-per-item attention writing Wo's parts),
+# the TMA-fed tcgen05 GEMMs under PDL, the tensor-core K4 (+ draft top-K)
+m3 = spx.init_model(spx.ModelConfig(vocab_size=1024, hidden_dim=1024, num_layers=3, num_heads=8,
+                                    ffn_dim=2816, max_context=32, seed=11), dtype="bf16")
+d3 = spx.init_model(spx.ModelConfig(vocab_size=1024, hidden_dim=1024, num_layers=1, num_heads=8,
+                                    ffn_dim=2816, max_context=32, seed=12), dtype="bf16")
+bank3b = {l: spx.init_predictor(4, 512, rng.derive(78, l)) for l in range(2)}
+be3 = spx.BatchedExitEngine(m3, d3, E.PredictorPolicy(bank3b), E.EngineConfig(threshold=0.5),
+                            batch=20, context=16)
+be3.generate([[5, 6, 7, 8]] * 20, 2)
 torch.cuda.synchronize()
 print("sanitize workload ok")
