@@ -297,6 +297,15 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
       : "memory");
 }
 
+__device__ __forceinline__ void tl_mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Row tiles: the grid's z extent covers the rows this call expects
+// (rows_hint); a CTA then walks row tiles z, z + gridDim.z, ... while they
+// hold rows (lazily completed rows can exceed the expectation), with the
+// stage ring and the barrier phases running on across tiles and TMEM handed
+// back by the epilogue (tmem_free) before the next tile's first MMA.
 template <int EPI>
 __global__ void __launch_bounds__(TT_THREADS, 2) tcl_tma_kernel(
     const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
@@ -304,52 +313,49 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tcl_tma_kernel(
   extern __shared__ __align__(1024) uint8_t tlsm[];
   uint8_t *ring = reinterpret_cast<uint8_t *>(((uintptr_t)tlsm + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[TT_MAX_STAGES], empty[TT_MAX_STAGES];
-  __shared__ uint64_t all_done;
+  __shared__ uint64_t all_done, tmem_free;
   __shared__ uint32_t tmem_base;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   __shared__ int s_go;
-  // grid (output tiles, K splits, row tiles): the row tile is the slowest
-  // index, so every live tile is scheduled before the (usually empty) tiles
-  // of rows beyond this call's expected count
-  const int o0 = blockIdx.x * TL_M, n0 = blockIdx.z * nbox;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // grid (output tiles, K splits, row tiles)
+  const int o0 = blockIdx.x * TL_M;
   const int kbt = kin / TL_BK, ks = blockIdx.y, nks = gridDim.y;
   const int kb0 = (int)((long long)ks * kbt / nks), kb1 = (int)((long long)(ks + 1) * kbt / nks);
   const int nkb = kb1 - kb0;
   const uint32_t tile_b = (uint32_t)nbox * 128u;
   const uint32_t stage_bytes = (uint32_t)TL_TILE_A + TL_PARTS * tile_b;
-  // the weights do not depend on the previous kernels: the first stages'
-  // weight blocks are requested before griddepcontrol.wait (programmatic
-  // dependent launch), the row parts after it
-  // (only tiles within the rows this call expects: the state's capacity may
-  // hold many more tiles that stay empty)
-  const int rows_exp = p.rows_hint > 16 ? (p.rows_hint + 15) / 16 * 16 : 16;
-  const int pre = n0 < rows_exp ? (nkb < stages ? nkb : stages) : 0;
+  // the weights do not depend on the previous kernels: the first tile's
+  // first weight stages are requested before griddepcontrol.wait
+  // (programmatic dependent launch), its row parts after it
+  const int first_n0 = blockIdx.z * nbox;
+  const int pre = nkb < stages ? nkb : stages;
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(&all_done, 1);
+    mbar_init(&tmem_free, 128);
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
     for (int i = 0; i < pre; ++i) {
-        mbar_arrive_expect_tx(&full[i], stage_bytes);
-        tma_load_2d(ring + (size_t)i * stage_bytes, &tmW, (kb0 + i) * TL_BK, o0, &full[i]);
-      }
+      mbar_arrive_expect_tx(&full[i], stage_bytes);
+      tma_load_2d(ring + (size_t)i * stage_bytes, &tmW, (kb0 + i) * TL_BK, o0, &full[i]);
+    }
   }
   pdl_wait();
   pdl_trigger();
   if (tid == 0) {
     const int nrows0 = *reinterpret_cast<const volatile int32_t *>(p.nrows);
-    s_go = !flag_set(p.done) && n0 < nrows0;
+    s_go = !flag_set(p.done) && first_n0 < nrows0;
     // complete the prefetched stages (their row parts) either way; drain
     // them if this CTA has nothing to do
     for (int i = 0; i < pre; ++i)
 #pragma unroll
       for (int pp = 0; pp < TL_PARTS; ++pp)
         tma_load_2d(ring + (size_t)i * stage_bytes + TL_TILE_A + pp * tile_b, &tmX,
-                    (kb0 + i) * TL_BK, pp * Npad + n0, &full[i]);
+                    (kb0 + i) * TL_BK, pp * Npad + first_n0, &full[i]);
     if (!s_go)
       for (int i = 0; i < pre; ++i) mbar_wait(&full[i], 0);
   }
@@ -365,62 +371,80 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tcl_tma_kernel(
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base;
+  const int zstep = gridDim.z * nbox;
   if (warp == 4) {
     if (lane == 0) {
-      for (int i = pre; i < nkb; ++i) {
-        const int s = i % stages;
-        if (i >= stages) mbar_wait(&empty[s], ((i / stages) - 1) & 1);
-        uint8_t *st = ring + (size_t)s * stage_bytes;
-        const int k0 = (kb0 + i) * TL_BK;
-        mbar_arrive_expect_tx(&full[s], stage_bytes);
-        tma_load_2d(st, &tmW, k0, o0, &full[s]);
+      int it = 0;
+      for (int n0 = first_n0; n0 < nrows; n0 += zstep, ++it)
+        for (int i = 0; i < nkb; ++i) {
+          const int gi = it * nkb + i;
+          if (gi < pre) continue;                   // issued before the wait
+          const int s = gi % stages;
+          if (gi >= stages) mbar_wait(&empty[s], ((gi / stages) - 1) & 1);
+          uint8_t *st = ring + (size_t)s * stage_bytes;
+          const int k0 = (kb0 + i) * TL_BK;
+          mbar_arrive_expect_tx(&full[s], stage_bytes);
+          tma_load_2d(st, &tmW, k0, o0, &full[s]);
 #pragma unroll
-        for (int pp = 0; pp < TL_PARTS; ++pp)
-          tma_load_2d(st + TL_TILE_A + pp * tile_b, &tmX, k0, pp * Npad + n0, &full[s]);
-      }
+          for (int pp = 0; pp < TL_PARTS; ++pp)
+            tma_load_2d(st + TL_TILE_A + pp * tile_b, &tmX, k0, pp * Npad + n0, &full[s]);
+        }
     }
   } else if (warp == 5) {
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_bf16(TL_M, nbox);
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % stages;
-        mbar_wait(&full[s], (i / stages) & 1);
-        tc_fence_after();
-        const uint32_t sa = smem_u32(ring + (size_t)s * stage_bytes);
-#pragma unroll
-        for (int k = 0; k < TL_BK / 16; ++k) {
-          const uint64_t ad = umma_desc_sw128(sa + k * 32);
-          const uint32_t dt = tmem + (uint32_t)((k & 1) * TL_NT);
-#pragma unroll
-          for (int pp = 0; pp < TL_PARTS; ++pp) {
-            const uint64_t bd = umma_desc_sw128(sa + (uint32_t)TL_TILE_A + pp * tile_b + k * 32);
-            umma_bf16(dt, ad, bd, idesc, (i > 0 || k > 1 || pp > 0) ? 1u : 0u);
-          }
+      int it = 0;
+      for (int n0 = first_n0; n0 < nrows; n0 += zstep, ++it) {
+        if (it > 0) {                               // the epilogue has read the last tile
+          mbar_wait(&tmem_free, (it - 1) & 1);
+          tc_fence_after();
         }
-        umma_commit(&empty[s]);
-        if (i == nkb - 1) umma_commit(&all_done);
+        for (int i = 0; i < nkb; ++i) {
+          const int gi = it * nkb + i;
+          const int s = gi % stages;
+          mbar_wait(&full[s], (gi / stages) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(ring + (size_t)s * stage_bytes);
+#pragma unroll
+          for (int k = 0; k < TL_BK / 16; ++k) {
+            const uint64_t ad = umma_desc_sw128(sa + k * 32);
+            const uint32_t dt = tmem + (uint32_t)((k & 1) * TL_NT);
+#pragma unroll
+            for (int pp = 0; pp < TL_PARTS; ++pp) {
+              const uint64_t bd = umma_desc_sw128(sa + (uint32_t)TL_TILE_A + pp * tile_b + k * 32);
+              umma_bf16(dt, ad, bd, idesc, (i > 0 || k > 1 || pp > 0) ? 1u : 0u);
+            }
+          }
+          umma_commit(&empty[s]);
+          if (i == nkb - 1) umma_commit(&all_done);
+        }
       }
     }
   } else {
     const int my_o = o0 + tid;
-    mbar_wait(&all_done, 0);
-    tc_fence_after();
-    for (int c0 = 0; c0 < nbox; c0 += 32) {
-      uint32_t v[32], v1[32];
-      tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c0, v);
-      tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(TL_NT + c0), v1);
+    int it = 0;
+    for (int n0 = first_n0; n0 < nrows; n0 += zstep, ++it) {
+      mbar_wait(&all_done, it & 1);
+      tc_fence_after();
+      for (int c0 = 0; c0 < nbox; c0 += 32) {
+        uint32_t v[32], v1[32];
+        tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c0, v);
+        tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(TL_NT + c0), v1);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(v1[j]));
-      if (my_o < nout) {
+        for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(v1[j]));
+        if (my_o < nout) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = n0 + c0 + j;
-          if (c0 + j < nbox && n < nrows) {
-            if (nks == 1) tcl_epilogue<EPI>(p, n, my_o, __uint_as_float(v[j]));
-            else partial[((size_t)ks * Npad + n) * nout + my_o] = __uint_as_float(v[j]);
+          for (int j = 0; j < 32; ++j) {
+            const int n = n0 + c0 + j;
+            if (c0 + j < nbox && n < nrows) {
+              if (nks == 1) tcl_epilogue<EPI>(p, n, my_o, __uint_as_float(v[j]));
+              else partial[((size_t)ks * Npad + n) * nout + my_o] = __uint_as_float(v[j]);
+            }
           }
         }
       }
+      tc_fence_before();
+      tl_mbar_arrive(&tmem_free);
     }
   }
   tc_fence_before();
@@ -601,7 +625,10 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
       cudaFuncSetAttribute(tcl_tma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
       tsm_set = tsm;
     }
-    dim3 tgrid((unsigned)otiles, (unsigned)nks, (unsigned)((Npad + nbox - 1) / nbox));
+    // row tiles for the rows this call expects; more rows (lazy completion)
+    // are walked by the same CTAs
+    const int zt = (rows_exp + nbox - 1) / nbox;
+    dim3 tgrid((unsigned)otiles, (unsigned)nks, (unsigned)(zt < 1 ? 1 : zt));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = tgrid;
     cfg.blockDim = dim3(TT_THREADS);
