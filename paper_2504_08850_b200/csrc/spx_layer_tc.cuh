@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(256) tcl_prep_kernel(LayerParams p, int kin, i
     float mean = 0.f, den = 1.f;
     if (ln) {
       float sm = 0.f;
+#pragma unroll 4
       for (int j = tid; j < k4; j += 256) {
         const float4 v = __ldcg(x4 + j);
         sm += (v.x + v.y) + (v.z + v.w);
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(256) tcl_prep_kernel(LayerParams p, int kin, i
       mean = sm / (float)kin;
       __syncthreads();
       float v2 = 0.f;
+#pragma unroll 4
       for (int j = tid; j < k4; j += 256) {
         const float4 v = __ldcg(x4 + j);
         const float a0 = v.x - mean, a1 = v.y - mean, a2 = v.z - mean, a3 = v.w - mean;
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(256) tcl_prep_kernel(LayerParams p, int kin, i
       __syncthreads();
     }
     __nv_bfloat16 *o = parts + (size_t)i * kin;
+#pragma unroll 4
     for (int j = tid; j < k4; j += 256) {
       const float4 v4 = __ldcg(x4 + j);
       float v[4] = {v4.x, v4.y, v4.z, v4.w};
@@ -536,9 +539,12 @@ __global__ void tcl_finish_kernel(LayerParams p) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) p.frontier[p.rows[i]] = p.layer + 1;
   if (p.cur_hidden && p.new_row) {
     const int nw = *p.new_row;
-    if (nw >= 0)
-      for (int j = threadIdx.x; j < p.d; j += blockDim.x)
-        p.cur_hidden[j] = __ldcg(p.pending + (size_t)nw * p.d + j);
+    if (nw >= 0) {                                // 16-byte copies, all in flight at once
+      const float4 *src = reinterpret_cast<const float4 *>(p.pending + (size_t)nw * p.d);
+      float4 *dst = reinterpret_cast<float4 *>(p.cur_hidden);
+#pragma unroll 4
+      for (int j = threadIdx.x; j < p.d / 4; j += blockDim.x) dst[j] = __ldcg(src + j);
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) *p.nrows = 0;
@@ -675,7 +681,7 @@ static void launch_layer_tcgen05(const LayerParams &p, int sms, cudaStream_t s) 
   tcl_matrix<EPI_WO>(p, p.d, p.d, Npad, sms, s, !att_parts);
   tcl_matrix<EPI_FFN1>(p, p.ffn, p.d, Npad, sms, s);
   tcl_matrix<EPI_FFN2>(p, p.d, p.ffn, Npad, sms, s, false);
-  launch_pdl(tcl_finish_kernel, 1, 256, 0, s, p);
+  launch_pdl(tcl_finish_kernel, 1, 1024, 0, s, p);
 }
 
 }  // namespace spx

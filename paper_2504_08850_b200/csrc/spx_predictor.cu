@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(256) softmax_pick_kernel(const float *logits, 
                                                            const int32_t *ids, int K,
                                                            float *probs_out, int *err) {
   constexpr int WCH = 2048;
-  __shared__ float s_e[2][WCH];
+  __shared__ __align__(16) float s_e[2][WCH];
   __shared__ float s_red[8];
   __shared__ int s_bad;
   __shared__ float s_sum;
@@ -218,8 +218,17 @@ __global__ void __launch_bounds__(256) softmax_pick_kernel(const float *logits, 
     if (tid == 0) {
       const int len = n - c * WCH < WCH ? n - c * WCH : WCH;
       const float *e = s_e[c & 1];
-#pragma unroll 8
-      for (int j = 0; j < len; ++j) esum = __fadd_rn(esum, e[j]);
+      const float4 *e4 = reinterpret_cast<const float4 *>(e);
+      int j = 0;
+#pragma unroll 4
+      for (; j + 4 <= len; j += 4) {                // 16-byte loads, the chain stays sequential
+        const float4 q = e4[j >> 2];
+        esum = __fadd_rn(esum, q.x);
+        esum = __fadd_rn(esum, q.y);
+        esum = __fadd_rn(esum, q.z);
+        esum = __fadd_rn(esum, q.w);
+      }
+      for (; j < len; ++j) esum = __fadd_rn(esum, e[j]);
     } else if (tid >= 32 && c + 1 < nch) {
       const int b = (c + 1) * WCH, len = n - b < WCH ? n - b : WCH;
       for (int j = tid - 32; j < len; j += blockDim.x - 32)

@@ -141,15 +141,15 @@ __device__ __forceinline__ void warp_cdot(const TW *wrow, const float *hn, int d
   }
 }
 
-template <typename TW, int CPL>
+template <typename TW, int CPL, int VR>
 __global__ void __launch_bounds__(VER_THREADS)
 verify_kernel(VerParams p) {
   const TW *head = reinterpret_cast<const TW *>(p.head);
-  extern __shared__ float hn[];           // VER_ROWS * d
-  __shared__ int s_rows[VER_ROWS];
+  extern __shared__ float hn[];           // VR * d
+  __shared__ int s_rows[VR];
   __shared__ int s_nr, s_bad;
-  __shared__ float s_r[VER_ROWS];
-  __shared__ unsigned long long s_best[VER_THREADS / 32][VER_ROWS];
+  __shared__ float s_r[VR];
+  __shared__ unsigned long long s_best[VER_THREADS / 32][VR];
   __shared__ bool s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = VER_THREADS / 32;
   const bool strict = p.mode == SPX_MODE_STRICT;
@@ -157,10 +157,10 @@ verify_kernel(VerParams p) {
   __shared__ int s_next;
   int r0 = 0;
   while (true) {
-    // collect the next <= VER_ROWS gated rows (same on every CTA)
+    // collect the next <= VR gated rows (same on every CTA)
     if (threadIdx.x == 0) {
       int nr = 0, r = r0;
-      for (; r < p.B && nr < VER_ROWS; ++r)
+      for (; r < p.B && nr < VR; ++r)
         if (ver_row_on(p, r)) s_rows[nr++] = r;
       s_nr = nr;
       s_bad = 0;
@@ -179,20 +179,20 @@ verify_kernel(VerParams p) {
       if (bad && lane == 0) { atomicOr(p.err, ERR_HIDDEN_NONFINITE); s_bad = 1; }
     }
     __syncthreads();
-    unsigned long long best[VER_ROWS];
+    unsigned long long best[VR];
 #pragma unroll
-    for (int r = 0; r < VER_ROWS; ++r) best[r] = 0ull;
+    for (int r = 0; r < VR; ++r) best[r] = 0ull;
     const int gw = blockIdx.x * nwarps + warp, tw = gridDim.x * nwarps;
     if (!strict) {
-      float rs[VER_ROWS];
+      float rs[VR];
 #pragma unroll
-      for (int r = 0; r < VER_ROWS; ++r) rs[r] = s_r[r];
+      for (int r = 0; r < VR; ++r) rs[r] = s_r[r];
       for (int v = gw; v < p.V; v += tw) {
-        float lg[VER_ROWS];
-        warp_cdot<TW, VER_ROWS, CPL>(head + (size_t)v * p.d, hn, p.d, nr, lane, lg);
+        float lg[VR];
+        warp_cdot<TW, VR, CPL>(head + (size_t)v * p.d, hn, p.d, nr, lane, lg);
         const float bw = p.head_bw ? p.head_bw[v] : 0.f;
 #pragma unroll
-        for (int r = 0; r < VER_ROWS; ++r) {
+        for (int r = 0; r < VR; ++r) {
           lg[r] = __fadd_rn(__fmul_rn(rs[r], lg[r]), bw);
           if (r < nr) {
             const unsigned long long k = argmax_key(lg[r], (uint32_t)v);
@@ -206,19 +206,19 @@ verify_kernel(VerParams p) {
       const int gt = blockIdx.x * VER_THREADS + threadIdx.x, tt = gridDim.x * VER_THREADS;
       for (int v = gt; v < p.V; v += tt) {
         const TW *wr = head + (size_t)v * p.d;
-        float acc[VER_ROWS] = {0.f, 0.f, 0.f, 0.f};
+        float acc[VR] = {};
         for (int j = 0; j < p.d; j += CHUNK) {
           float wf[4];
           load4_f32<TW>(wr + j, wf);
 #pragma unroll
-          for (int r = 0; r < VER_ROWS; ++r)
+          for (int r = 0; r < VR; ++r)
             if (r < nr)
 #pragma unroll
               for (int e = 0; e < CHUNK; ++e)
                 acc[r] = __fadd_rn(acc[r], __fmul_rn(hn[(size_t)r * p.d + j + e], wf[e]));
         }
 #pragma unroll
-        for (int r = 0; r < VER_ROWS; ++r)
+        for (int r = 0; r < VR; ++r)
           if (r < nr) {
             const unsigned long long k = argmax_key(acc[r], (uint32_t)v);
             best[r] = k > best[r] ? k : best[r];
@@ -226,7 +226,7 @@ verify_kernel(VerParams p) {
           }
       }
 #pragma unroll
-      for (int r = 0; r < VER_ROWS; ++r)
+      for (int r = 0; r < VR; ++r)
 #pragma unroll
         for (int m = 16; m >= 1; m >>= 1) {
           const unsigned long long o = __shfl_xor_sync(0xffffffffu, best[r], m);
@@ -235,7 +235,7 @@ verify_kernel(VerParams p) {
     }
     if (lane == 0)
 #pragma unroll
-      for (int r = 0; r < VER_ROWS; ++r) s_best[warp][r] = best[r];
+      for (int r = 0; r < VR; ++r) s_best[warp][r] = best[r];
     __syncthreads();
     if (threadIdx.x < nr) {
       unsigned long long b = 0ull;
@@ -485,21 +485,43 @@ static void launch_verify1(const VerParams &p, cudaStream_t stream) {
   }
 }
 
+template <typename TW, int CPL>
+static void launch_verify_wide(const VerParams &p, cudaStream_t stream) {
+  if constexpr (std::is_same<TW, __nv_bfloat16>::value && CPL <= 8) {
+    const size_t sm8 = (size_t)8 * p.d * sizeof(float);
+    cudaFuncSetAttribute(verify_kernel<TW, CPL, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm8);
+    verify_kernel<TW, CPL, 8><<<num_sms(), VER_THREADS, sm8, stream>>>(p);
+  }
+}
+
 template <typename TW>
 static int launch_verify(const VerParams &p, int nchunk, int grid, size_t smem,
                          cudaStream_t stream) {
   const bool one = p.B == 1 && p.mode != SPX_MODE_STRICT &&
                    std::is_same<TW, __nv_bfloat16>::value && nchunk <= 8 * NPART;
+  // SPX_VERIFY_WIDE=1 (A/B, off): 8 rows per pass over the head for more than
+  // VER_ROWS rows.  Measured slower (tree draft level, 5-10 rows: 505 vs 283 us
+  // per launch): one CTA per SM and 8 shared-memory row reads per weight
+  // element make it shared-memory bound.
+  static const int env_wide = getenv("SPX_VERIFY_WIDE") ? atoi(getenv("SPX_VERIFY_WIDE")) : 0;
+  const bool wide = env_wide && !one && p.B > VER_ROWS && p.mode != SPX_MODE_STRICT &&
+                    std::is_same<TW, __nv_bfloat16>::value && nchunk <= 8 * NPART &&
+                    (size_t)8 * p.d * sizeof(float) <= 200 * 1024;
 #define SPX_LAUNCH_VER(CPL)                                                                    \
   do {                                                                                         \
     if (one) {                                                                                 \
       launch_verify1<TW, CPL>(p, stream);                                                      \
       break;                                                                                   \
     }                                                                                          \
+    if (wide) {                                                                                \
+      launch_verify_wide<TW, CPL>(p, stream);                                                  \
+      break;                                                                                   \
+    }                                                                                          \
     if (smem > 48 * 1024)                                                                      \
-      cudaFuncSetAttribute(verify_kernel<TW, CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)smem);                                                         \
-    verify_kernel<TW, CPL><<<grid, VER_THREADS, smem, stream>>>(p);                            \
+      cudaFuncSetAttribute(verify_kernel<TW, CPL, VER_ROWS>,                                   \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+    verify_kernel<TW, CPL, VER_ROWS><<<grid, VER_THREADS, smem, stream>>>(p);                  \
   } while (0)
   if (nchunk <= NPART) SPX_LAUNCH_VER(1);
   else if (nchunk <= 2 * NPART) SPX_LAUNCH_VER(2);
