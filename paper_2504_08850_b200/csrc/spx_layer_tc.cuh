@@ -622,6 +622,10 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
     // K split: the expected live CTAs fill one wave of per_sm CTAs per SM
     const int nt = (rows_exp + nbox - 1) / nbox;
     nks = per_sm * sms / (otiles * nt);
+    // SPX_TCL_MIN_OTILES_SPLIT (A/B): matrices with at least this many output
+    // tiles run without a K split (no partials, no reduce pass)
+    static const int env_nosplit = getenv("SPX_TCL_MIN_OTILES_SPLIT") ? atoi(getenv("SPX_TCL_MIN_OTILES_SPLIT")) : 0;
+    if (env_nosplit > 0 && otiles * nt >= env_nosplit) nks = 1;
     nks = nks < 1 ? 1 : nks > 8 ? 8 : nks;
     while (nks > 1 && ((size_t)nks * Npad * nout * 4 > TL_PARTIAL_BYTES || kin / TL_BK / nks < 8))
       --nks;

@@ -1,3 +1,3 @@
 cd $GRAFT_REPO_ROOT; export PYTHONPATH=$PWD; mkdir -p gpurun_out
-timeout 1500 python -m pytest -q -m gpu tests -x > gpurun_out/t26_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/t26_status.txt
-timeout 600 python scripts/tree_bench.py --steps 6 --profile gpurun_out/t26_kt_tree.txt > gpurun_out/t26_tree.log 2>&1; echo "tree rc=$?" >> gpurun_out/t26_status.txt
+for E in 0 80; do SPX_TCL_MIN_OTILES_SPLIT=$E timeout 600 python scripts/tree_bench.py --steps 6 > gpurun_out/t27_tree_$E.log 2>&1; SPX_TCL_MIN_OTILES_SPLIT=$E timeout 600 python scripts/batch_sweep.py --batches 16,64,256 --steps 4 > gpurun_out/t27_sweep_$E.jsonl 2>&1; done
+echo done >> gpurun_out/t27_status.txt
