@@ -243,6 +243,11 @@ __global__ void __launch_bounds__(256) softmax_pick_kernel(const float *logits, 
   __syncthreads();
   for (int j = tid; j < K; j += blockDim.x) {
     const int id = ids[(size_t)row * K + j];
+    if (id < 0 || id >= n) {                         // model.py:307-308
+      atomicOr(err, ERR_ID_RANGE);
+      probs_out[(size_t)row * K + j] = 0.f;
+      continue;
+    }
     probs_out[(size_t)row * K + j] = __fdiv_rn(np_expf(__fsub_rn(x[id], m)), s_sum);
   }
 }

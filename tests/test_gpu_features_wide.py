@@ -57,3 +57,18 @@ def test_softmax_pick_equals_feature_probs(n, V, K):
     for r in range(n):
         full = softmax_device(lg[r].contiguous())
         assert torch.equal(out[r], full[ids[r].long()])
+
+
+def test_softmax_pick_id_range_error():
+    """An id outside the vocabulary is the reference's ValueError, not a read."""
+    import torch
+    from paper_2504_08850_b200 import _native as N
+    lg = torch.zeros((1, 100), dtype=torch.float32, device="cuda")
+    ids = torch.as_tensor([[3, 100]], dtype=torch.int32, device="cuda")
+    out = torch.empty((1, 2), dtype=torch.float32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.check(N.lib().spx_softmax_pick(N.ptr(lg), 1, 100, N.ptr(ids), 2, N.ptr(out), N.ptr(err),
+                                     N.stream_ptr()), "spx_softmax_pick")
+    with pytest.raises(ValueError, match="out of range"):
+        N.raise_device_error(err.item())
+    assert out[0, 0].item() == pytest.approx(0.01)
