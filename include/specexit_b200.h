@@ -383,10 +383,12 @@ typedef struct {
 int spx_topk(const float *logits, int64_t n, int32_t K, int32_t *ids_out, void *stream);
 /* softmax_1d (src/specexit/model.py:149-152) of each of `rows` rows of n
  * logits, evaluated at the K ids ids[r*K + j] (speculation.py:80-84
- * draft_probs): bit-identical to extract_features' local probabilities with
- * the strict denominator chain.  Non-finite logits set ERR bit 4. */
+ * draft_probs).  STRICT: bit-identical to extract_features' local
+ * probabilities (the reference's left-to-right denominator); FAST: the
+ * denominator as a fixed-order parallel sum (FAST tolerance).  Non-finite
+ * logits set ERR bit 4, ids outside [0, n) bit 1. */
 int spx_softmax_pick(const float *logits, int64_t rows, int64_t n, const int32_t *ids,
-                     int32_t K, float *probs_out, int32_t *err, void *stream);
+                     int32_t K, float *probs_out, int32_t mode, int32_t *err, void *stream);
 /* spx_topk for `rows` independent rows of n logits (row-major), K ids each. */
 int spx_topk_rows(const float *logits, int64_t rows, int64_t n, int32_t K, int32_t *ids_out,
                   void *stream);

@@ -188,7 +188,7 @@ __global__ void features_wide_kernel(const float *logits, const float *prev, flo
 // shared-memory chunks that warps 1.. fill one chunk ahead.
 __global__ void __launch_bounds__(256) softmax_pick_kernel(const float *logits, int n,
                                                            const int32_t *ids, int K,
-                                                           float *probs_out, int *err) {
+                                                           float *probs_out, int mode, int *err) {
   constexpr int WCH = 2048;
   __shared__ __align__(16) float s_e[2][WCH];
   __shared__ float s_red[8];
@@ -210,6 +210,35 @@ __global__ void __launch_bounds__(256) softmax_pick_kernel(const float *logits, 
   __syncthreads();
   m = s_red[0];
   for (int w = 1; w < 8; ++w) m = fmaxf(m, s_red[w]);
+  if (mode != SPX_MODE_STRICT) {
+    // FAST: the denominator as a fixed-order block sum (each thread's strided
+    // share, then the warp and CTA trees) -- the FAST contract's tolerance,
+    // not the reference's left-to-right chain
+    float part = 0.f;
+    for (int i = tid; i < n; i += blockDim.x) part += np_expf(__fsub_rn(x[i], m));
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    __syncthreads();
+    if ((tid & 31) == 0) s_red[tid >> 5] = part;
+    __syncthreads();
+    if (tid == 0) {
+      float t = 0.f;
+      for (int w = 0; w < 8; ++w) t += s_red[w];
+      s_sum = t;
+      if (s_bad) atomicOr(err, ERR_LOGIT_NONFINITE);
+    }
+    __syncthreads();
+    for (int j = tid; j < K; j += blockDim.x) {
+      const int id = ids[(size_t)row * K + j];
+      if (id < 0 || id >= n) {
+        atomicOr(err, ERR_ID_RANGE);
+        probs_out[(size_t)row * K + j] = 0.f;
+        continue;
+      }
+      probs_out[(size_t)row * K + j] = __fdiv_rn(np_expf(__fsub_rn(x[id], m)), s_sum);
+    }
+    return;
+  }
   const int nch = (n + WCH - 1) / WCH;
   for (int i = tid; i < (n < WCH ? n : WCH); i += blockDim.x) s_e[0][i] = np_expf(__fsub_rn(x[i], m));
   __syncthreads();
@@ -544,13 +573,13 @@ extern "C" int spx_extract_features(const float *logits, const float *prev, floa
 }
 
 extern "C" int spx_softmax_pick(const float *logits, int64_t rows, int64_t n,
-                                const int32_t *ids, int32_t K, float *probs_out, int32_t *err,
-                                void *stream) {
+                                const int32_t *ids, int32_t K, float *probs_out, int32_t mode,
+                                int32_t *err, void *stream) {
   if (!logits || !ids || !probs_out || !err || rows < 0 || n < 1 || n > (1 << 30) || K < 1)
     return SPX_EINVAL;
   if (rows == 0) return 0;
   softmax_pick_kernel<<<(unsigned)rows, 256, 0, (cudaStream_t)stream>>>(logits, (int)n, ids, K,
-                                                                         probs_out, err);
+                                                                         probs_out, mode, err);
   return spx_launch_status("spx_softmax_pick");
 }
 

@@ -51,12 +51,18 @@ def test_softmax_pick_equals_feature_probs(n, V, K):
     ids = torch.as_tensor(rs.integers(0, V, size=(n, K)).astype(np.int32), device="cuda")
     out = torch.empty((n, K), dtype=torch.float32, device="cuda")
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
-    N.check(N.lib().spx_softmax_pick(N.ptr(lg), n, V, N.ptr(ids), K, N.ptr(out), N.ptr(err),
-                                     N.stream_ptr()), "spx_softmax_pick")
+    fast = torch.empty((n, K), dtype=torch.float32, device="cuda")
+    N.check(N.lib().spx_softmax_pick(N.ptr(lg), n, V, N.ptr(ids), K, N.ptr(out), N.SPX_MODE_STRICT,
+                                     N.ptr(err), N.stream_ptr()), "spx_softmax_pick")
+    N.check(N.lib().spx_softmax_pick(N.ptr(lg), n, V, N.ptr(ids), K, N.ptr(fast), N.SPX_MODE_FAST,
+                                     N.ptr(err), N.stream_ptr()), "spx_softmax_pick")
     assert err.item() == 0
     for r in range(n):
         full = softmax_device(lg[r].contiguous())
-        assert torch.equal(out[r], full[ids[r].long()])
+        assert torch.equal(out[r], full[ids[r].long()])          # STRICT: bit for bit
+    # FAST: parallel denominator, within the FAST probability tolerance (1e-3
+    # absolute; in practice a few ulps relative)
+    assert torch.allclose(fast, out, rtol=1e-5, atol=1e-7)
 
 
 def test_softmax_pick_id_range_error():
@@ -67,8 +73,8 @@ def test_softmax_pick_id_range_error():
     ids = torch.as_tensor([[3, 100]], dtype=torch.int32, device="cuda")
     out = torch.empty((1, 2), dtype=torch.float32, device="cuda")
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
-    N.check(N.lib().spx_softmax_pick(N.ptr(lg), 1, 100, N.ptr(ids), 2, N.ptr(out), N.ptr(err),
-                                     N.stream_ptr()), "spx_softmax_pick")
+    N.check(N.lib().spx_softmax_pick(N.ptr(lg), 1, 100, N.ptr(ids), 2, N.ptr(out), N.SPX_MODE_FAST,
+                                     N.ptr(err), N.stream_ptr()), "spx_softmax_pick")
     with pytest.raises(ValueError, match="out of range"):
         N.raise_device_error(err.item())
     assert out[0, 0].item() == pytest.approx(0.01)
