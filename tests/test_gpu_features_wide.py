@@ -61,8 +61,10 @@ def test_softmax_pick_equals_feature_probs(n, V, K):
         full = softmax_device(lg[r].contiguous())
         assert torch.equal(out[r], full[ids[r].long()])          # STRICT: bit for bit
     # FAST: parallel denominator, within the FAST probability tolerance (1e-3
-    # absolute; in practice a few ulps relative)
-    assert torch.allclose(fast, out, rtol=1e-5, atol=1e-7)
+    # absolute).  Relative differences reach ~2e-4 at V = 128000: that is the
+    # reference's own left-to-right chain drifting (~n u), not the parallel sum
+    assert (fast - out).abs().max().item() <= 1e-3
+    assert torch.allclose(fast, out, rtol=1e-3, atol=0)
 
 
 def test_softmax_pick_id_range_error():
