@@ -349,10 +349,12 @@ typedef struct {
                                    /* max_ctx.  Rows selecting more set SPX_ERR_ROW_CAP */
   void *tc_scratch;                /* optional: >= spx_layer_tc_scratch_bytes(d, ffn,  */
                                    /* row_cap or max_ctx) bytes; enables the tcgen05  */
-                                   /* path for calls advancing >= 16 rows (FAST, bf16) */
+                                   /* path for calls advancing >= 3 rows (FAST, bf16); */
+                                   /* zero-initialised once by the caller           */
 } spx_layer_args;
-/* scratch of the tensor-core multi-row layer path (three bf16 parts of the
- * advanced rows) */
+/* scratch of the tensor-core multi-row layer path: two regions of bf16 row
+ * parts, the K-split partial sums and the K-split tile counters (which must
+ * start at zero; they reset themselves after every use) */
 int64_t spx_layer_tc_scratch_bytes(int64_t d, int64_t ffn, int64_t row_cap);
 int spx_layer_forward(const spx_layer_args *args, void *stream);
 /* floats needed for s_part and int32s for s_flag at these dimensions */

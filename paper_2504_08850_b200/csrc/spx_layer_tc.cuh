@@ -58,6 +58,9 @@ __host__ __device__ inline size_t tcl_parts_bytes(int d, int ffn, int row_cap) {
   return ((size_t)TL_PARTS * npad * (size_t)(ffn > d ? ffn : d) * 2 + 255) / 256 * 256;
 }
 
+constexpr size_t TL_PARTIAL_BYTES = 96ull << 20;      // K-split partial sums
+constexpr int TL_FIX_SLOTS = 65536;                   // K-split tile counters (int32)
+
 // the two bf16 parts of x (hi = RNE(x), lo = RNE(x - hi): tcl_prep_kernel's split)
 __device__ __forceinline__ void tl_put_parts(__nv_bfloat16 *parts, size_t plane, size_t idx,
                                              float x) {
@@ -312,11 +315,13 @@ __device__ __forceinline__ void tl_mbar_arrive(uint64_t *bar) {
 template <int EPI>
 __global__ void __launch_bounds__(TT_THREADS, 2) tcl_tma_kernel(
     const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-    LayerParams p, int nout, int kin, int Npad, int nbox, int stages, float *partial) {
+    LayerParams p, int nout, int kin, int Npad, int nbox, int stages, float *partial,
+    int *fix) {
   extern __shared__ __align__(1024) uint8_t tlsm[];
   uint8_t *ring = reinterpret_cast<uint8_t *>(((uintptr_t)tlsm + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[TT_MAX_STAGES], empty[TT_MAX_STAGES];
   __shared__ uint64_t all_done, tmem_free;
+  __shared__ int s_last;
   __shared__ uint32_t tmem_base;
   __shared__ int s_go;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -448,6 +453,27 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tcl_tma_kernel(
       }
       tc_fence_before();
       tl_mbar_arrive(&tmem_free);
+      if (nks > 1 && fix) {
+        // K-split fixup: the last split CTA of this (output tile, row tile)
+        // sums the nks partials in split order (tcl_reduce_kernel's order)
+        // and runs the epilogue -- no separate reduce launch
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        int *ctr = fix + (size_t)blockIdx.x * (Npad / 16) + n0 / 16;
+        if (tid == 0) s_last = atomicAdd(ctr, 1) == nks - 1;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (s_last) {
+          __threadfence();
+          if (my_o < nout)
+            for (int c = 0; c < nbox && n0 + c < nrows; ++c) {
+              const int n = n0 + c;
+              float sum = 0.f;
+              for (int k = 0; k < nks; ++k) sum += __ldcg(partial + ((size_t)k * Npad + n) * nout + my_o);
+              tcl_epilogue<EPI>(p, n, my_o, sum);
+            }
+          if (tid == 0) *ctr = 0;
+        }
+      }
     }
   }
   tc_fence_before();
@@ -550,10 +576,11 @@ __global__ void tcl_finish_kernel(LayerParams p) {
   if (threadIdx.x == 0) *p.nrows = 0;
 }
 
-constexpr size_t TL_PARTIAL_BYTES = 96ull << 20;      // K-split partial sums
 
 inline size_t tcl_scratch_bytes(int d, int ffn, int row_cap) {
-  return 2 * tcl_parts_bytes(d, ffn, row_cap) + TL_PARTIAL_BYTES;
+  // parts A, parts B, partials, the K-split tile counters (zero-initialised
+  // by the caller, self-resetting)
+  return 2 * tcl_parts_bytes(d, ffn, row_cap) + TL_PARTIAL_BYTES + (size_t)TL_FIX_SLOTS * 4;
 }
 
 inline bool tcl_supported(const LayerParams &p) {
@@ -572,6 +599,15 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
   __nv_bfloat16 *parts = reinterpret_cast<__nv_bfloat16 *>(
       reinterpret_cast<uint8_t *>(p.tc_scratch) + (EPI == EPI_FFN2 ? pbytes : 0));
   float *partial = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(p.tc_scratch) + 2 * pbytes);
+  int *fix = reinterpret_cast<int *>(reinterpret_cast<uint8_t *>(p.tc_scratch) + 2 * pbytes +
+                                     TL_PARTIAL_BYTES);
+  // SPX_TCL_FIXUP=1 (A/B, off): the last split CTA of a tile reduces the
+  // partials itself instead of a reduce launch.  Measured slower (tree step
+  // 13.2 vs 10.4 ms, 13B B=64 21.2 vs 10.5 ms): one thread per output walks
+  // the tile's rows x splits as a dependent load chain, where the reduce
+  // kernel spreads the same sums over the whole GPU.
+  static const int env_fix = getenv("SPX_TCL_FIXUP") ? atoi(getenv("SPX_TCL_FIXUP")) : 0;
+  bool fixed = false;                               // K split reduced inside the GEMM
   if (prep)
     launch_pdl(tcl_prep_kernel<EPI>, p.row_cap < 2 * sms ? p.row_cap : 2 * sms, 256, 0, s, p, kin,
                Npad, parts);
@@ -650,8 +686,10 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
     cfg.attrs = attr;
     static const int env_pdl = getenv("SPX_PDL_LAYERS") ? atoi(getenv("SPX_PDL_LAYERS")) : 1;
     cfg.numAttrs = env_pdl ? 1 : 0;
+    const int otiles_l = (nout + TL_M - 1) / TL_M;
+    fixed = env_fix && nks > 1 && (size_t)otiles_l * (Npad / 16) <= (size_t)TL_FIX_SLOTS;
     cudaLaunchKernelEx(&cfg, tcl_tma_kernel<EPI>, tmW, tmX, p, nout, kin, Npad, nbox, stages,
-                       partial);
+                       partial, fixed ? fix : static_cast<int *>(nullptr));
   } else {
   dim3 grid((unsigned)otiles, (unsigned)((Npad + TL_NT - 1) / TL_NT), (unsigned)nks);
   // SPX_TCL_AHEAD (A/B): K-blocks in flight ahead of the MMA (3 leaves one
@@ -662,7 +700,7 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
   else
     tcl_gemm_kernel<EPI, 2><<<grid, TL_THREADS, smem, s>>>(p, nout, kin, Npad, parts, partial);
   }
-  if (nks > 1) {
+  if (nks > 1 && !fixed) {
     const long long work = (long long)(p.rows_hint > 0 ? p.rows_hint : 1) * nout;
     const int rg = (int)((work + 255) / 256 < 8 * sms ? (work + 255) / 256 : 8 * sms);
     (void)rg;

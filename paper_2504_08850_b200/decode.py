@@ -58,7 +58,8 @@ class DecodeState:
         if model.spx_dtype == N.SPX_DTYPE_BF16:
             nb = lib.spx_layer_tc_scratch_bytes(d, f, self.row_cap or C)
             if nb > 0:
-                self.tc_scratch = torch.empty(nb, dtype=torch.uint8, device=dev)
+                # zeroed once: the K-split tile counters at its end self-reset
+                self.tc_scratch = torch.zeros(nb, dtype=torch.uint8, device=dev)
         self.attn_ptr = None
         self.attn_idx = None
         self.done = done_flag
