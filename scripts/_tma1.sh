@@ -1,3 +1,2 @@
 cd $GRAFT_REPO_ROOT; export PYTHONPATH=$PWD; mkdir -p gpurun_out
-TAG=f4 bash scripts/gpu.sh test smoke bench
-timeout 600 python scripts/tree_bench.py --steps 6 --profile gpurun_out/f4_kt_tree.txt > gpurun_out/f4_tree.log 2>&1; echo "tree rc=$?" >> gpurun_out/status.txt
+timeout 900 python -m pytest -q -m gpu tests/test_gpu_engine.py -k "reuse or topk" > gpurun_out/t33_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/t33_status.txt

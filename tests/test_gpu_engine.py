@@ -381,3 +381,54 @@ def test_save_weights_byte_identical(tmp_path, name):
     assert ta.keys() == tb.keys()
     for k in ta:
         assert np.array_equal(ta[k], tb[k]), k
+
+
+def test_engine_reuse_keeps_online_window(golden, oracle):
+    """Two generate() calls on ONE engine in two-level mode: the online window
+    carries over (the reference creates it in __init__ and never resets it,
+    engine.py:122-160), so the second call's active layers, exits and tokens
+    follow the first call's exits -- as the oracle engine reused the same way."""
+    eg = golden.json("engine_tiny.json")
+    tr = [x for x in eg["traces"] if x["mode"] == "two-level"][0]
+    t, d = _engine_models(eg)
+    bank = {l: spx.init_predictor(4, 512, oracle.derive(eg["bank_seed"], l)) for l in range(5)}
+    prof = spx.OfflineProfile(6, np.asarray(eg["exit_counts"]), 0)
+    tc = oracle.ModelConfig(num_layers=6, seed=eg["target_seed"])
+    dc = oracle.ModelConfig(num_layers=2, seed=eg["draft_seed"])
+    obank = {l: oracle.init_predictor(4, 512, oracle.derive(eg["bank_seed"], l)) for l in range(5)}
+    ora = oracle.ExitEngineOracle(tc, oracle.init_model(tc, bf16=True), dc,
+                                  oracle.init_model(dc, bf16=True), obank, k=4,
+                                  threshold=tr["threshold"], schedule_mode="two-level",
+                                  exit_counts=np.asarray(eg["exit_counts"]),
+                                  schedule_config=oracle.ScheduleConfig(tr["queue_len"], tr["radius"],
+                                                                        tr["top_k"]))
+    with numerics.using("strict"):
+        eng = E.ExitEngine(t, d, E.PredictorPolicy(bank),
+                           E.EngineConfig(k=4, threshold=tr["threshold"], schedule_mode="two-level"),
+                           prof, spx.ScheduleConfig(tr["queue_len"], tr["radius"], tr["top_k"]))
+        for prompt in (tr["prompt"], [7, 9, 11, 13, 15]):
+            toks, trace = eng.generate(prompt, 10)
+            otoks, otrace = ora.generate(prompt, 10)
+            assert toks == otoks
+            for rec, ref in zip(trace, otrace):
+                assert (rec.token, rec.exit_layer, rec.predictor_fired, rec.verified,
+                        list(rec.active)) == (ref.token, ref.exit_layer, ref.predictor_fired,
+                                              ref.verified, list(ref.active))
+
+
+@pytest.mark.parametrize("k", [1, 4, 25, 64])
+def test_topk_matches_stable_argsort(k):
+    """spx_topk (speculation.py:57-60: np.argsort(-x, kind="stable")[:k]) for
+    k up to 64, with exact ties, on one row and on many rows at once."""
+    from paper_2504_08850_b200 import _native as N
+    from paper_2504_08850_b200.speculation import topk_from_logits
+    rs = np.random.default_rng(k)
+    x = rs.integers(-50, 50, size=(6, 4000)).astype(np.float32) / 8   # many exact ties
+    for r in range(x.shape[0]):
+        ids = np.asarray(topk_from_logits(x[r], k))
+        assert np.array_equal(ids, np.argsort(-x[r], kind="stable")[:k])
+    xs = torch.as_tensor(x, device="cuda")
+    out = torch.empty((x.shape[0], k), dtype=torch.int32, device="cuda")
+    N.check(N.lib().spx_topk_rows(N.ptr(xs), x.shape[0], x.shape[1], k, N.ptr(out),
+                                  N.stream_ptr()), "spx_topk_rows")
+    assert np.array_equal(out.cpu().numpy(), np.argsort(-x, axis=1, kind="stable")[:, :k])
