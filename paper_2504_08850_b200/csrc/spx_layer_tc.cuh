@@ -371,14 +371,21 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tcl_tma_kernel(
   if (!s_go) return;
   const int nrows = *reinterpret_cast<const volatile int32_t *>(p.nrows);
   if (warp == 5) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 ::"r"(smem_u32(&tmem_base)), "n"(2 * TL_NT));
+    // two accumulators (even / odd k-steps) of acc = max(nbox, 128) columns:
+    // 256 columns, or all 512 for 256-row tiles (one CTA per SM then)
+    if (nbox > TL_NT)
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                   ::"r"(smem_u32(&tmem_base)), "n"(4 * TL_NT));
+    else
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                   ::"r"(smem_u32(&tmem_base)), "n"(2 * TL_NT));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base;
+  const uint32_t acc = nbox > TL_NT ? 2 * TL_NT : TL_NT;    // accumulator column stride
   const int zstep = gridDim.z * nbox;
   if (warp == 4) {
     if (lane == 0) {
@@ -416,7 +423,7 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tcl_tma_kernel(
 #pragma unroll
           for (int k = 0; k < TL_BK / 16; ++k) {
             const uint64_t ad = umma_desc_sw128(sa + k * 32);
-            const uint32_t dt = tmem + (uint32_t)((k & 1) * TL_NT);
+            const uint32_t dt = tmem + (uint32_t)(k & 1) * acc;
 #pragma unroll
             for (int pp = 0; pp < TL_PARTS; ++pp) {
               const uint64_t bd = umma_desc_sw128(sa + (uint32_t)TL_TILE_A + pp * tile_b + k * 32);
@@ -437,7 +444,7 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tcl_tma_kernel(
       for (int c0 = 0; c0 < nbox; c0 += 32) {
         uint32_t v[32], v1[32];
         tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)c0, v);
-        tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(TL_NT + c0), v1);
+        tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + acc + (uint32_t)c0, v1);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(v1[j]));
         if (my_o < nout) {
@@ -478,8 +485,12 @@ __global__ void __launch_bounds__(TT_THREADS, 2) tcl_tma_kernel(
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * TL_NT));
+  if (warp == 5) {
+    if (nbox > TL_NT)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(4 * TL_NT));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * TL_NT));
+  }
 }
 
 // 2-D bf16 tensor map, 64-element (128-byte) inner box, 128-byte swizzle
@@ -633,7 +644,13 @@ static void tcl_matrix(const LayerParams &p, int nout, int kin, int Npad, int sm
   // row tile sized by the rows this call expects (rows_hint), not the state's
   // capacity: the B operand (two parts) is loaded box-sized per stage
   const int rows_exp = p.rows_hint > 16 ? (p.rows_hint + 15) / 16 * 16 : 16;
-  int nbox = Npad < TL_NT ? Npad : TL_NT;
+  // SPX_TCL_N256=1 (A/B, off): 256-row tiles (UMMA N = 256, weights read
+  // once for up to 256 rows, all 512 TMEM columns, 2 stages, one CTA per SM)
+  // when the call expects >= 256 rows.  Measured slower: 13B B=256 step 22.3
+  // vs 19.3 ms (two 80 KB stages per SM keep too few weight bytes in flight)
+  static const int env_n256 = getenv("SPX_TCL_N256") ? atoi(getenv("SPX_TCL_N256")) : 0;
+  const int nmax = (env_n256 && rows_exp >= 2 * TL_NT) ? 2 * TL_NT : TL_NT;
+  int nbox = Npad < nmax ? Npad : nmax;
   nbox = rows_exp < nbox ? rows_exp : nbox;
   CUtensorMap tmW, tmX;
   if (env_tma && tl_tensor_map(&tmW, gemv_weights_host<EPI>(p), (uint64_t)nout, (uint64_t)kin, TL_M) &&

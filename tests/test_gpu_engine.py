@@ -432,3 +432,33 @@ def test_topk_matches_stable_argsort(k):
     N.check(N.lib().spx_topk_rows(N.ptr(xs), x.shape[0], x.shape[1], k, N.ptr(out),
                                   N.stream_ptr()), "spx_topk_rows")
     assert np.array_equal(out.cpu().numpy(), np.argsort(-x, axis=1, kind="stable")[:, :k])
+
+
+def test_tcgen05_layers_256_row_tiles_and_lazy_rows():
+    """A 300-row prefill (three 128-row tiles; with SPX_TCL_N256=1 the
+    256-row UMMA tiles over all 512 TMEM columns), then a call whose row set
+    exceeds its expectation (20 new rows + 300 rows completing layer 2) makes
+    CTAs walk extra row tiles.  FAST vs the STRICT reference-order kernels,
+    FAST tolerance."""
+    d, f, nh = 1024, 2816, 8
+    cfg = spx.ModelConfig(vocab_size=512, hidden_dim=d, num_layers=3, num_heads=nh, ffn_dim=f,
+                          max_context=400, seed=23)
+    m = spx.init_model(cfg, dtype="bf16")
+    outs = {}
+    for mode in ("strict", "fast"):
+        with numerics.using(mode):
+            st = DecodeState(m)
+            res = []
+            st.begin([int(x) % 512 for x in range(7, 307)])
+            res.append(st.run_layer(0).cpu().numpy())
+            res.append(st.run_layer(1).cpu().numpy())
+            # 20 new rows; layer 2 then also completes the 300 rows left at it
+            st.begin(list(range(60, 80)))
+            for l in range(3):
+                res.append(st.run_layer(l).cpu().numpy())
+            st.check()
+            res.append(st.pending[:st.n].cpu().numpy())
+            outs[mode] = res
+    for a, b in zip(outs["strict"], outs["fast"]):
+        assert a.shape == b.shape
+        np.testing.assert_allclose(b, a, rtol=1e-3, atol=1e-3 * np.abs(a).max())
