@@ -218,6 +218,12 @@ typedef struct {
 #define SPX_VERIFY_TC_MIN_ROWS 8
 int spx_verify(const spx_verify_args *args, void *stream);
 int64_t spx_verify_tc_scratch_bytes(int64_t B, int64_t d, int64_t V);
+/* byte offset in tc_scratch of the tensor-core logits of the last
+ * tensor-core verify call: (computed rows in row order, V) f32, r * D + bw
+ * (FAST-tolerance logits; the exact ids come from topk_out / token_out).
+ * The tensor-core form runs for B >= SPX_VERIFY_TC_MIN_ROWS, or any B when
+ * topk_out is given. */
+int64_t spx_verify_tc_logits_offset(int64_t B, int64_t d, int64_t V);
 
 /* K5 -- two-level scheduler on device (src/specexit/scheduler.py:49-102).
  * Per row: ring of the last `queue_len` exit layers + neighbour counts. */

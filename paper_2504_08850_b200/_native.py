@@ -140,6 +140,8 @@ def lib():
     L.spx_predictor_gather_tail.argtypes = [ctypes.POINTER(PredictorArgs), _vp,
                                             ctypes.POINTER(PredictorArgs), _vp, _vp]
     L.spx_softmax_pick.argtypes = [_vp, _i64, _i64, _vp, _i32, _vp, _i32, _vp, _vp]
+    L.spx_verify_tc_logits_offset.argtypes = [_i64, _i64, _i64]
+    L.spx_verify_tc_logits_offset.restype = _i64
     L.spx_verify_tc_scratch_bytes.argtypes = [_i64, _i64, _i64]
     L.spx_verify_tc_scratch_bytes.restype = _i64
     L.spx_tree_tc_scratch_bytes.argtypes = [_i64, _i64, _i64, _i64]

@@ -554,7 +554,7 @@ extern "C" int spx_verify(const spx_verify_args *a, void *stream_) {
   static const int env_tc = getenv("SPX_VERIFY_TC") ? atoi(getenv("SPX_VERIFY_TC")) : 1;
   if (env_tc && a->tc_scratch && a->head_wmax && a->mode != SPX_MODE_STRICT &&
       a->head_dtype == SPX_DTYPE_BF16 && !a->logits_out && a->d % TV_BK == 0 &&
-      a->B >= SPX_VERIFY_TC_MIN_ROWS && a->B <= 0x7fff) {
+      (a->B >= SPX_VERIFY_TC_MIN_ROWS || a->topk_out) && a->B <= 0x7fff) {
     if (a->topk_out && (a->topk_k < 1 || a->topk_k > 64 || a->topk_k > a->V)) return SPX_EINVAL;
     p.topk_out = a->topk_out; p.topk_k = a->topk_out ? a->topk_k : 0;
     bool ok = false;
@@ -575,6 +575,11 @@ extern "C" int spx_verify(const spx_verify_args *a, void *stream_) {
     return launch_verify<__nv_bfloat16>(p, nchunk, grid, smem, stream);
   if (a->head_dtype == SPX_DTYPE_F32) return launch_verify<float>(p, nchunk, grid, smem, stream);
   return SPX_EINVAL;
+}
+
+extern "C" int64_t spx_verify_tc_logits_offset(int64_t B, int64_t d, int64_t V) {
+  if (B <= 0 || d <= 0 || V <= 0) return -1;
+  return (int64_t)tv_layout((int)B, (int)d, (int)V).tl;
 }
 
 extern "C" int64_t spx_verify_tc_scratch_bytes(int64_t B, int64_t d, int64_t V) {

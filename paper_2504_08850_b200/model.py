@@ -476,8 +476,10 @@ def verify_args(model: TransformerModel, hidden: torch.Tensor, B: int, token_out
     a.B, a.d, a.V = B, model.config.hidden_dim, model.config.vocab_size
     # many rows, bf16 head: the tensor-core form of K4 (spx_verify_tc.cuh) --
     # same tokens / flags; the library picks it only where it applies
-    if (kw.get("tensor_cores", True) and B >= N.SPX_VERIFY_TC_MIN_ROWS and model.dtype == "bf16"
-            and model.config.hidden_dim % 64 == 0 and kw.get("logits_out") is None):
+    if (kw.get("tensor_cores", True)
+            and (B >= N.SPX_VERIFY_TC_MIN_ROWS or kw.get("topk_out") is not None)
+            and model.dtype == "bf16" and model.config.hidden_dim % 64 == 0
+            and kw.get("logits_out") is None):
         a.head_wmax = N.ptr(model.head_wmax)
         a.tc_scratch = N.ptr(_verify_tc_scratch(B, model.config.hidden_dim, model.config.vocab_size))
         if kw.get("topk_out") is not None:

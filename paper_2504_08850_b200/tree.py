@@ -220,6 +220,12 @@ class TreeEngine:
         anc = {0: [0]}
         level = [0]
         logits = {}
+        K = self.config.k
+        k_sets = {}
+        kmax = max([K] + list(self.branching))
+        fast_sets = (getattr(self, "tc_draft", True) and numerics.mode() != N.SPX_MODE_STRICT
+                     and d.dtype == "bf16"
+                     and d.config.hidden_dim % 64 == 0 and 1 <= kmax <= min(64, d.config.vocab_size))
         for depth in range(len(self.branching) + 1):
             toks = [nodes[j].token for j in level]
             if depth == 0:
@@ -230,13 +236,33 @@ class TreeEngine:
             for l in range(d.config.num_layers):
                 ds.launch_layer(l)
             r0 = ds.n - len(level)
-            _, _, lg = head_argmax(d, ds.pending[r0:ds.n], want_logits=True)
-            for i, j in enumerate(level):
-                logits[j] = lg[i]
-            if depth == len(self.branching):
-                break
+            last = depth == len(self.branching)
+            if fast_sets:
+                # FAST, bf16 draft: K4's tensor-core form gives each node's
+                # exact stable top-max(K, b) ids (CDOT order, as the full
+                # logits would) without writing the (n, V) logits; the
+                # probabilities are the softmax of its tensor-core logits
+                # (FAST tolerance).  The first K ids are the node's feature
+                # set (merge_paths), the first b its children.
+                b = 0 if last else self.branching[depth]
+                kk = max(K, b)
+                ids_h, pr_h = self._level_topk(ds.pending[r0:ds.n], len(level), kk)
+                for i, j in enumerate(level):
+                    k_sets[(j, K)] = SpeculativeSet(tokens=tuple(int(t) for t in ids_h[i, :K]),
+                                                    draft_probs=tuple(float(p) for p in pr_h[i, :K]))
+                if last:
+                    break
+                sets = [SpeculativeSet(tokens=tuple(int(t) for t in ids_h[i, :b]),
+                                       draft_probs=tuple(float(p) for p in pr_h[i, :b]))
+                        for i in range(len(level))]
+            else:
+                _, _, lg = head_argmax(d, ds.pending[r0:ds.n], want_logits=True)
+                for i, j in enumerate(level):
+                    logits[j] = lg[i]
+                if last:
+                    break
+                sets = speculative_sets_from_rows(lg, self.branching[depth])    # one host read
             nxt = []
-            sets = speculative_sets_from_rows(lg, self.branching[depth])    # one host read
             for i, j in enumerate(level):
                 spec = sets[i]
                 for tok, pr in zip(spec.tokens, spec.draft_probs):
@@ -245,7 +271,33 @@ class TreeEngine:
                     anc[c] = anc[j] + [c]
                     nxt.append(c)
             level = nxt
-        return TokenTree(nodes=nodes, branching=self.branching), logits
+        return TokenTree(nodes=nodes, branching=self.branching), logits, k_sets
+
+    def _level_topk(self, hidden, n, kk):
+        """Exact stable top-kk ids of n draft rows (tensor-core K4 with
+        candidate re-evaluation) and FAST softmax probabilities at those ids
+        from the tensor-core logits; one host read."""
+        from .model import _VerifyScratch, _verify_tc_scratch, launch_verify, verify_args
+        d = self.draft
+        V, D = d.config.vocab_size, d.config.hidden_dim
+        ids = torch.empty((n, kk), dtype=torch.int32, device="cuda")
+        tok = torch.empty(n, dtype=torch.int32, device="cuda")
+        err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        scratch, counter = _VerifyScratch.get(n)
+        a = verify_args(d, hidden, n, tok, scratch, counter, err, topk_out=ids, topk_k=kk,
+                        mode=N.SPX_MODE_FAST)
+        launch_verify(a)
+        tl = _verify_tc_scratch(n, D, V)
+        off = int(N.lib().spx_verify_tc_logits_offset(n, D, V))
+        probs = torch.empty((n, kk), dtype=torch.float32, device="cuda")
+        N.check(N.lib().spx_softmax_pick(tl.data_ptr() + off, n, V, N.ptr(ids), kk, N.ptr(probs),
+                                         N.SPX_MODE_FAST, N.ptr(err), N.stream_ptr()),
+                "spx_softmax_pick")
+        hb = torch.cat([ids.to(torch.float64).view(-1), probs.to(torch.float64).view(-1),
+                        err.to(torch.float64)]).cpu().numpy()
+        N.raise_device_error(int(hb[-1]))
+        return (hb[:n * kk].astype(np.int64).reshape(n, kk),
+                hb[n * kk:2 * n * kk].reshape(n, kk))
 
     def _active_layers(self):
         L = self.target.config.num_layers
@@ -267,14 +319,14 @@ class TreeEngine:
         cfg = self.target.config
         L, K = cfg.num_layers, self.config.k
         self._merge_cache = {}
-        tree, node_logits = self._draft_tree()
-        ctx_len = len(self.context)
         if K > self.draft.config.vocab_size:
             raise ValueError("k exceeds vocabulary size")
+        tree, node_logits, k_sets = self._draft_tree()
+        ctx_len = len(self.context)
         # every node's draft top-K at once (merge_paths' per-node feature / leaf
-        # verify sets, tree.py:64-73): one batched top-K + softmax, one host read
-        k_sets = {}
-        if 1 <= K <= 64:
+        # verify sets, tree.py:64-73): one batched top-K + softmax, one host
+        # read (or already from the drafting levels)
+        if not k_sets and 1 <= K <= 64:
             order = sorted(node_logits)
             batch = speculative_sets_from_rows(torch.stack([node_logits[j] for j in order]), K)
             k_sets = {(j, K): s_ for j, s_ in zip(order, batch)}

@@ -213,3 +213,47 @@ def test_tree_merged_tensor_cores_match_cuda_cores(n_rows, n_ids, k):
     for x, y in zip(a, b):
         x, y = x.cpu().numpy(), y.cpu().numpy()
         assert np.all(np.abs(x - y) <= 1e-5 * np.abs(x).max() + 1e-6)
+
+
+@pytest.mark.parametrize("branching", [(5, 2, 1), (3, 2)])
+def test_tree_fast_tensor_core_drafting_matches_full_logits(branching):
+    """FAST, bf16 draft: the tree is drafted from K4's tensor-core form (exact
+    stable top-max(K, b) ids per node, probabilities from the tensor-core
+    logits) instead of the full CUDA-core draft logits.  The trees, exits,
+    accepted tokens and corrections must be identical; the draft
+    probabilities agree within the FAST tolerance."""
+    from paper_2504_08850_b200 import rng
+    V, D = 2048, 1024
+    tc = spx.ModelConfig(V, D, 4, 8, 2816, 128, 41)
+    dc = spx.ModelConfig(V, D, 1, 8, 2816, 128, 42)
+    t, d = spx.init_model(tc, dtype="bf16"), spx.init_model(dc, dtype="bf16")
+    bank = {l: spx.init_predictor(4, 512, rng.derive(43, l)) for l in range(3)}
+    prof = spx.OfflineProfile(4, np.asarray([5, 3, 2, 0], np.uint64), 0)
+    out = {}
+    with numerics.using("fast"):
+        for tcd in (False, True):
+            eng = T.TreeEngine(t, d, E.PredictorPolicy(bank), branching,
+                               E.EngineConfig(k=4, threshold=0.5, schedule_mode="two-level"), prof,
+                               spx.ScheduleConfig(5, 1, 2))
+            eng.tc_draft = tcd
+            trees = []
+            orig = eng._draft_tree
+
+            def rec(orig=orig, trees=trees):
+                r = orig()
+                trees.append(r[0])
+                return r
+            eng._draft_tree = rec
+            eng.start([int(x) % V for x in rng.splitmix64(44, 12)])
+            steps = []
+            for _ in range(3):
+                r = eng.step()
+                steps.append((r.accepted_tokens, r.correction_token, r.path_exit_layers,
+                              r.accepted_path, r.predictor_evals))
+            out[tcd] = (steps, trees)
+    assert out[False][0] == out[True][0]
+    for ta, tb in zip(out[False][1], out[True][1]):
+        assert [(n.token, n.parent, n.depth) for n in ta.nodes] == \
+            [(n.token, n.parent, n.depth) for n in tb.nodes]
+        np.testing.assert_allclose([n.prob for n in tb.nodes[1:]],
+                                   [n.prob for n in ta.nodes[1:]], rtol=1e-4, atol=1e-6)
