@@ -277,19 +277,48 @@ __global__ void __launch_bounds__(VER_THREADS) tcv_select_kernel(VerParams p,
     __syncthreads();
     return b;
   };
-  // the Kt largest tensor-core keys, one block max per round
+  // the Kt largest tensor-core keys
   unsigned long long below = ~0ull, last = 0ull;
   float E = 0.f;
-  for (int q = 0; q < Kt; ++q) {
-    unsigned long long best = 0ull;
+  if (Kt <= 8) {
+    // one scan: every thread keeps its 8 best keys in registers; Kt rounds
+    // of a block max pop the winner from its owner's list (a thread is asked
+    // for at most Kt <= 8 keys, so its list never runs dry)
+    unsigned long long l[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) l[q] = 0ull;
     for (int v = tid; v < p.V; v += VER_THREADS) {
-      const unsigned long long k = argmax_key(tl[v], (uint32_t)v);
-      if (k < below && k > best) best = k;
+      unsigned long long k = argmax_key(tl[v], (uint32_t)v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const bool sw = k > l[q];
+        const unsigned long long t = l[q];
+        l[q] = sw ? k : t;
+        k = sw ? t : k;
+      }
     }
-    last = block_max(best);
-    below = last;
-    const int vw = (int)(0xffffffffu - (uint32_t)(last & 0xffffffffull));
-    E = fmaxf(E, bound(vw, f32_from_order_key((uint32_t)(last >> 32))));
+    for (int q = 0; q < Kt; ++q) {
+      last = block_max(l[0]);
+      if (l[0] == last && last != 0ull) {
+#pragma unroll
+        for (int r = 0; r < 7; ++r) l[r] = l[r + 1];
+        l[7] = 0ull;
+      }
+      const int vw = (int)(0xffffffffu - (uint32_t)(last & 0xffffffffull));
+      E = fmaxf(E, bound(vw, f32_from_order_key((uint32_t)(last >> 32))));
+    }
+  } else {
+    for (int q = 0; q < Kt; ++q) {                // one block max per round
+      unsigned long long best = 0ull;
+      for (int v = tid; v < p.V; v += VER_THREADS) {
+        const unsigned long long k = argmax_key(tl[v], (uint32_t)v);
+        if (k < below && k > best) best = k;
+      }
+      last = block_max(best);
+      below = last;
+      const int vw = (int)(0xffffffffu - (uint32_t)(last & 0xffffffffull));
+      E = fmaxf(E, bound(vw, f32_from_order_key((uint32_t)(last >> 32))));
+    }
   }
   const float thr = f32_from_order_key((uint32_t)(last >> 32)) - E;
   // candidates, re-evaluated exactly (warp per candidate), keys into s_cand
