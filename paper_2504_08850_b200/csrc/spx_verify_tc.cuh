@@ -46,7 +46,7 @@ constexpr int TV_MAX_STAGES = 8;
 constexpr size_t TV_TILE_A = (size_t)TV_M * TV_BK * 2;
 
 struct TvLayout {
-  size_t rows, r, s, parts, tl, total;
+  size_t rows, r, s, parts, xg, tl, total;
 };
 __host__ __device__ inline int tv_npad(int B) { return (B + 15) / 16 * 16; }
 __host__ __device__ inline TvLayout tv_layout(int B, int d, int V) {
@@ -56,7 +56,8 @@ __host__ __device__ inline TvLayout tv_layout(int B, int d, int V) {
   L.r = L.rows + (np * 4 + 255) / 256 * 256;
   L.s = L.r + (np * 4 + 255) / 256 * 256;
   L.parts = L.s + (np * 4 + 255) / 256 * 256;
-  L.tl = L.parts + ((size_t)TV_PARTS * np * d * 2 + 255) / 256 * 256;
+  L.xg = L.parts + ((size_t)TV_PARTS * np * d * 2 + 255) / 256 * 256;
+  L.tl = L.xg + (np * (size_t)d * 4 + 255) / 256 * 256;
   L.total = L.tl + np * (size_t)V * 4;
   return L;
 }
@@ -91,10 +92,12 @@ __global__ void __launch_bounds__(32) tcv_prep_kernel(VerParams p, uint8_t *scra
                       &rr, &bad);
   if (bad && lane == 0) atomicOr(p.err, ERR_HIDDEN_NONFINITE);
   __nv_bfloat16 *parts = reinterpret_cast<__nv_bfloat16 *>(scratch + L.parts);
+  float *xg_out = reinterpret_cast<float *>(scratch + L.xg) + (size_t)want * p.d;
   const size_t plane = (size_t)Npad * p.d;
   float sa = 0.f;
   for (int j = lane; j < p.d; j += 32) {
     const float x = hn[j];
+    xg_out[j] = x;                                  // for tcv_select's exact dots
     const __nv_bfloat16 h = __float2bfloat16_rn(x);
     const float x1 = x - __bfloat162float(h);
     const __nv_bfloat16 m = __float2bfloat16_rn(x1);
@@ -248,12 +251,12 @@ __global__ void __launch_bounds__(VER_THREADS) tcv_select_kernel(VerParams p,
   const float *tl = reinterpret_cast<const float *>(scratch + L.tl) + (size_t)i * p.V;
   const TW *head = reinterpret_cast<const TW *>(p.head);
   const int Kt = p.topk_k > 0 ? p.topk_k : 1;
-  if (warp == 0) {
-    int bad = 0;
-    float rr = 1.f;
-    warp_head_prep<CPL>(p.hidden + (size_t)row * p.hidden_stride, p.g, p.b, p.d, hn, lane, false,
-                        &rr, &bad);
-    if (lane == 0) hn[p.d] = rr;
+  {
+    // the row's FAST normalisation as tcv_prep computed it (warp_head_prep:
+    // the very bits verify_kernel uses), staged with 16-byte loads
+    const float4 *src = reinterpret_cast<const float4 *>(scratch + L.xg) + (size_t)i * (p.d / 4);
+    for (int j = tid; j < p.d / 4; j += VER_THREADS) reinterpret_cast<float4 *>(hn)[j] = __ldcg(src + j);
+    if (tid == 0) hn[p.d] = reinterpret_cast<const float *>(scratch + L.r)[i];
   }
   if (tid == 0) s_nc = 0;
   __syncthreads();
